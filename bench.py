@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""bench.py — one speculation iteration of attention (SURVEY.md §8d unit of work) per step:
+per layer verify (gamma+1 rows over the full KV, fused Collect-2 score byproduct, fused append) ->
+top-k select (side stream) ; then gamma dependent sparse draft steps over all layers (fused
+append).  Metric (BASELINE.json): draft+verify attention tokens/s at 32K ctx = B*(2*gamma+1)/t_iter,
+with achieved HBM GB/s against ~8 TB/s and against the measured copy peak.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload config2] [--impl ours|reference]
+
+N > 1 runs under torchrun: one process per GPU, batch-sharded (weak scaling, no data-path
+collective in per-layer mode on batch shards), max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "draft+verify attention tokens/s at 32K ctx; achieved HBM GB/s vs ~8 TB/s"
+HBM_NOMINAL = 8000.0  # GB/s, BASELINE.json denominator
+
+WORKLOADS = {
+    # name: (layers, Hq, Hkv, ctx, gamma, batch_per_gpu, description)
+    "config2": (32, 32, 8, 32768, 4, 1,
+                "Llama-3.1-8B-shaped attention (32q/8kv, d128, 32 layers), 32K ctx, gamma 4, "
+                "k=selection_k(0.07,p,16)=2294, batch 1 per GPU"),
+    "config1": (1, 32, 8, 4096, 4, 1, "single-layer synthetic, 8 KV heads, d128, 4K ctx, gamma 4"),
+    "config3": (32, 32, 8, 65536, 6, 16, "Llama-3.1-8B-shaped, 64K ctx, gamma 6, batch 16 (sharded by batch)"),
+    "config4": (80, 64, 8, 131072, 4, 4, "Llama-3.1-70B-shaped (64q/8kv, 80 layers), 128K ctx, gamma 4, batch 4"),
+}
+RATIO, K_MIN, D = 0.07, 16, 128
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), float(pk.get("bf16_tflops", 1623.5)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+def selection_k(ratio, p, k_min):
+    return min(p, max(int(math.floor(ratio * p + 0.5)), k_min))
+
+
+def iteration_bytes(L, Hq, Hkv, p, gamma, k, B):
+    """Algorithmic HBM bytes of one iteration, bf16 KV (s = 2)."""
+    s, d = 2, D
+    per = ((p + gamma + 1) * 2 * Hkv * d * s                              # verify KV (+ window)
+           + sum((k + t) * 2 * Hkv * d * s for t in range(1, gamma + 1))  # draft gathers
+           + Hkv * p * 4 * 2                                              # score partial write + read
+           + (gamma + 1) * Hq * d * (s + 4) + gamma * Hq * d * (s + 4)    # Q in (bf16), O out (f32)
+           + (gamma + 1) * k * 4                                          # index write + reads
+           + (2 * gamma + 1) * 2 * Hkv * d * s)                           # appends
+    return per * L * B
+
+
+def verify_launch_bytes(Hq, Hkv, p, R, B):
+    """Algorithmic bytes of ONE verify launch (one layer): KV prefix + window rows + Q + O +
+    score byproduct + fused append."""
+    d = D
+    return B * (p * 2 * Hkv * d * 2 + R * 2 * Hkv * d * 2 + R * Hq * d * 2 + R * Hq * d * 4 + Hkv * p * 4
+                + R * 2 * Hkv * d * 2)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 5 + i and s[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------------------------- ours
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2602_07223_b200 import COLLECT2, PER_LAYER, Cache, Runner
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    L, Hq, Hkv, ctx, gamma, B_total, desc = WORKLOADS[args.workload]
+    B = B_total if args.workload in ("config3", "config4") else B_total
+    if args.workload in ("config3", "config4") and world > 1:
+        B = max(1, B_total // world)  # batch shards
+    R = gamma + 1
+    p0 = ctx
+    k = selection_k(RATIO, p0, K_MIN)
+    scale = 1.0 / math.sqrt(D)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+
+    cache = Cache(L, Hkv, D, p0 + R + 64, max_seqs=B, page_size=256)
+    # fill the prefix with synthetic post-RoPE keys/values (bf16), chunked appends
+    chunk = 2048
+    for b in range(B):
+        done = 0
+        while done < p0:
+            n = min(chunk, p0 - done)
+            kk = torch.randn((n, L * Hkv, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+            vv = torch.randn((n, L * Hkv, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+            cache.append(kk, vv, seq=b)
+            done += n
+    torch.cuda.synchronize()
+    runner = Runner(cache, Hq, max_rows=R, max_prefix=p0, max_batch=B, sparse_ratio=RATIO, k_min=K_MIN)
+    runner.set_batch(list(range(B)), [p0] * B)
+
+    def rnd(*shape):
+        return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+
+    qv, kvn, vvn = rnd(L, B, Hq, R, D), rnd(L, B, R, Hkv, D), rnd(L, B, R, Hkv, D)
+    qd, kdn, vdn = rnd(gamma, L, B, Hq, D), rnd(gamma, L, B, Hkv, D), rnd(gamma, L, B, Hkv, D)
+    out_v = torch.empty((L, B, Hq, R, D), dtype=torch.float32, device=dev)
+    out_d = torch.empty((gamma, L, B, Hq, D), dtype=torch.float32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    itargs = runner.iteration_args(gamma, qv, kvn, vvn, qd, kdn, vdn, out_v, out_d, strategy=COLLECT2,
+                                   mode=PER_LAYER, scale=scale, use_graph=not args.no_graph)
+    launches_per_step = runner.iteration_kernel_count(itargs)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident timing (inputs already in HBM)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            runner.iteration(itargs, stream=stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            runner.iteration(itargs, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    barrier()
+    ms = max_over_ranks(ms)
+
+    # ---- dominant kernel (verify) launch durations, CUDA events on the launching stream
+    nv = min(L, 32)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nv * 3)]
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for i, (a, b_) in enumerate(ev):
+            l = i % nv
+            a.record(stream)
+            runner.verify(l, qv[l], out_v[l], kvn[l], vvn[l], scale, score_row_mask=1 | (1 << gamma), stream=stream)
+            b_.record(stream)
+    torch.cuda.synchronize()
+    vms = sum(a.elapsed_time(b_) for a, b_ in ev[nv:]) / (len(ev) - nv)  # skip the first (warm) pass
+
+    # ---- end to end through the public API with host buffers (pinned), copies inside the region
+    host_in = [t.cpu().pin_memory() for t in (qv, kvn, vvn, qd, kdn, vdn)]
+    dev_in = [qv, kvn, vvn, qd, kdn, vdn]
+    host_out = [torch.empty(out_v.shape, dtype=torch.float32).pin_memory(),
+                torch.empty(out_d.shape, dtype=torch.float32).pin_memory()]
+    h2d = sum(t.numel() * t.element_size() for t in host_in)
+    d2h = sum(t.numel() * t.element_size() for t in host_out)
+
+    def e2e_step():
+        for h, d_ in zip(host_in, dev_in):
+            d_.copy_(h, non_blocking=True)
+        runner.iteration(itargs, stream=stream)
+        host_out[0].copy_(out_v, non_blocking=True)
+        host_out[1].copy_(out_d, non_blocking=True)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.warmup // 2)):
+            e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+
+    hbm_peak, _, peak_src = peaks()
+    tok_per_step = B * (2 * gamma + 1)
+    value = world * tok_per_step / (ms / 1e3)
+    it_bytes = iteration_bytes(L, Hq, Hkv, p0, gamma, k, B)
+    vb = verify_launch_bytes(Hq, Hkv, p0, R, B)
+    v_gbs = vb / (vms / 1e3) / 1e9
+    it_gbs = it_bytes / (ms / 1e3) / 1e9
+    result = {
+        "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn, post-RoPE K/V/Q, bf16)",
+        "config": {"workload": f"{args.workload}: {desc}", "global_batch": B * world, "seq_len": p0,
+                   "gamma": gamma, "k": k, "selection": "collect2, per-layer", "layers": L,
+                   "parallelism": f"dp{world} (batch-sharded, one process per GPU)",
+                   "l2": f"inputs > L2: KV cache {L * B * p0 * Hkv * D * 4 / 1e9:.1f} GB/GPU >> 126 MB",
+                   "cuda_graph": not args.no_graph},
+        "hbm": {"bytes_per_iter": it_bytes, "achieved_gbs": round(it_gbs, 1),
+                "frac_of_8tbs": round(it_gbs / HBM_NOMINAL, 4), "frac_of_measured": round(it_gbs / hbm_peak, 4),
+                "measured_peak_gbs": hbm_peak, "peak_source": peak_src},
+        "roofline": {"kernel": "verify_kernel (one layer)", "bound": "hbm", "achieved": round(v_gbs, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(v_gbs / hbm_peak, 4), "traffic": None,
+                     "bytes_per_launch": vb, "launch_us": round(vms * 1e3, 2), "peak_source": peak_src},
+        "e2e": {"value": round(world * tok_per_step / (ms_e2e / 1e3), 2), "unit": "tokens/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    return result
+
+
+# --------------------------------------------------------------------------------------------- CPU
+
+def cpu_reference_sample(workload, threads):
+    """Reference CPU path (oracle/_ref = the reference's own TUs) on a bounded sample: one layer of
+    the workload (verify of all q-heads x rows over the full prefix, Collect-2 select, gamma draft
+    steps), extrapolated x layers.  Returns (tokens/s, seconds, sample description, kind)."""
+    import numpy as np
+
+    from oracle.pyoracle import COLLECT2, REF_SO, Oracle, Ref
+    L, Hq, Hkv, ctx, gamma, B, _ = WORKLOADS[workload]
+    kind = "reference"
+    try:
+        impl = Ref() if os.path.exists(REF_SO) else None
+    except Exception:
+        impl = None
+    if impl is None:
+        impl, kind, threads = Oracle(), "port", 1
+    p0, R, G = ctx, gamma + 1, Hq // Hkv
+    rng = np.random.default_rng(7)
+    kv = impl.kv(1, Hkv, D, p0 + R + 8)
+    K = rng.standard_normal((p0 + R, Hkv, D), dtype=np.float32)
+    V = rng.standard_normal((p0 + R, Hkv, D), dtype=np.float32)
+    for t in range(p0 + R):
+        kv.append(K[t], V[t])
+    q = rng.standard_normal((Hq, R, D), dtype=np.float32)
+    scale = 1.0 / math.sqrt(D)
+    t0 = time.perf_counter()
+    kwargs = {"threads": threads} if kind == "reference" else {}
+    _, logits = kv.verify_layer(0, Hq, q, p0, R, scale, **kwargs)
+    t1 = time.perf_counter()
+    sel = impl.select(COLLECT2, logits, list(range(1, R + 1)), RATIO, K_MIN)
+    t2 = time.perf_counter()
+    kv.truncate(p0)
+    for j in range(1, gamma + 1):
+        kv.append(K[p0 + j - 1], V[p0 + j - 1])
+        kv.draft_layer(0, Hq, rng.standard_normal((Hq, D), dtype=np.float32), [sel], p0, j, scale, **kwargs)
+    t3 = time.perf_counter()
+    per_layer = t3 - t0
+    it_s = per_layer * L * B
+    tps = B * (2 * gamma + 1) / it_s
+    sample = (f"1 of {L} layers x batch 1 of {B} ({workload}): verify {Hq}x{R} attend_collect over {p0} keys "
+              f"{t1 - t0:.2f}s + collect2 select {t2 - t1:.2f}s + {gamma} draft steps {t3 - t2:.2f}s; "
+              f"extrapolated x{L * B}")
+    return tps, per_layer, sample, kind
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    vals = []
+    for _ in range(max(1, args.steps if args.steps <= 3 else 3)):
+        tps, secs, sample, kind = cpu_reference_sample(args.workload, threads)
+        vals.append(tps)
+    v = statistics.median(vals)
+    L, Hq, Hkv, ctx, gamma, B, desc = WORKLOADS[args.workload]
+    cores = threads if kind == "reference" else 1
+    return {
+        "metric": METRIC, "value": round(v, 4), "unit": "tokens/s", "n_gpus": world, "steps": len(vals),
+        "warmup": 0, "ms_per_step": round(1e3 * B * (2 * gamma + 1) / v, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64 (reference CPU arithmetic)",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.workload}: {desc}", "global_batch": B, "seq_len": ctx, "gamma": gamma},
+        "cpu_baseline": {"value": round(v, 4), "unit": "tokens/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": round(v, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if not args.no_cpu_baseline:
+            try:
+                tps, _, sample, kind = cpu_reference_sample(args.workload, os.cpu_count() or 1)
+                res["cpu_baseline"] = {"value": round(tps, 4), "unit": "tokens/s",
+                                       "cores": (os.cpu_count() or 1) if kind == "reference" else 1,
+                                       "kind": kind, "sample": sample}
+            except Exception as e:  # reported, never fatal
+                res["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,223 @@
+/* specattn_b200.h — C ABI of the B200-native SpecAttn hot path (libspecattn_b200.so).
+ *
+ * Drop-in boundary for the reference's operator API (/root/reference/proj, namespace specattn):
+ *
+ *   reference (C++, Eigen, CPU)                                   this ABI (sm_100a, device-resident)
+ *   ------------------------------------------------------------  ---------------------------------------
+ *   KvStore::KvStore(ModelConfig)        kv_store.hpp:21          sa_cache_create
+ *   KvStore::append(keys, values)        kv_store.hpp:33-36       sa_kv_append (n tokens at once)
+ *   KvStore::truncate(to_len)            kv_store.hpp:38-40       sa_kv_truncate
+ *   KvStore::set_committed(len)          kv_store.hpp:42          sa_kv_set_committed
+ *   KvStore::gather(layer, head, idx)    kv_store.hpp:44-46       sa_kv_gather
+ *   KvStore::keys()/values() views       kv_store.hpp:48-54       sa_kv_read
+ *   KvStore::size()/committed()          kv_store.hpp:23-24       sa_kv_size / sa_kv_committed
+ *   KvStore::bytes_per_token()           kv_store.hpp:30          sa_kv_bytes_per_token
+ *   attend_collect(q, Kp, Vp, Kw, Vw, s) attention.hpp:63-67      sa_verify_attention (all q-heads x
+ *     + LogitMatrix byproduct            attention.hpp:22-41        gamma+1 rows of one layer, fused
+ *                                                                   append, fused score byproduct)
+ *   score_columns + selection_k          selection.hpp:48-55      sa_select_topk (per layer or per
+ *     + topk_indices + select_collect2   selection.hpp:61-69        KV head; Collect-2 / AllDraft rows)
+ *     / select_all_draft
+ *   KvStore::gather + attend(q, K, V, s) kv_store.hpp:44, attention.hpp:49-53
+ *                                                                 sa_draft_attention (index gather fused
+ *                                                                   with attention, fused append)
+ *   SPEC decode_iteration (absent in code) SPEC.md:350-457        sa_iteration_run (verify -> select ->
+ *                                                                   gamma drafts for all layers; CUDA graph)
+ *
+ * Conventions
+ *  - Plain pointers and sizes; device pointers unless a parameter says "host".  Every
+ *    device-side call takes a cudaStream_t (passed as void*; NULL = legacy default stream).
+ *  - No exceptions cross the ABI.  sa_status mirrors the reference's exception taxonomy
+ *    (SURVEY.md §8b): std::invalid_argument -> SA_INVALID_ARGUMENT, std::domain_error ->
+ *    SA_DOMAIN_ERROR, std::out_of_range -> SA_OUT_OF_RANGE, std::length_error -> SA_LENGTH_ERROR.
+ *    sa_last_error() returns the message of the last failure on the calling thread.
+ *  - Device KV storage is bf16 (the reference stores fp32, config.hpp:40-42; bf16 is required to
+ *    fit config 3 in one B200's HBM).  fp32 inputs are rounded to nearest-even bf16.
+ *  - Threading (kv_store.hpp:16-18): one writer stream per cache; read-only calls may
+ *    run on other streams after an event.
+ *  - head_dim must be 128 (all BASELINE configs); page_size a power of two >= 64.
+ */
+#ifndef SPECATTN_B200_H_
+#define SPECATTN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SA_API __attribute__((visibility("default")))
+
+typedef enum sa_status {
+  SA_OK = 0,
+  SA_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  SA_DOMAIN_ERROR = 2,     /* std::domain_error     */
+  SA_OUT_OF_RANGE = 3,     /* std::out_of_range     */
+  SA_LENGTH_ERROR = 4,     /* std::length_error     */
+  SA_CUDA_ERROR = 5,
+  SA_NOT_SUPPORTED = 6,
+  SA_NCCL_ERROR = 7
+} sa_status;
+
+typedef enum sa_dtype { SA_F32 = 0, SA_BF16 = 1 } sa_dtype;
+
+/* selection.hpp:15-22 — the logit-guided strategies on the hot path. */
+typedef enum sa_strategy {
+  SA_LAST_ACCEPTED = 2,   /* one row: a+1 (needs all rows' raw logits)        selection.cpp:198-207 */
+  SA_ALL_DRAFT = 3,       /* all gamma+1 rows                                 selection.cpp:183-185 */
+  SA_COLLECT2 = 4,        /* rows {1, gamma+1} (the paper's method)           selection.cpp:187-196 */
+  SA_COLLECT2_WEIGHTS = 5 /* rows {1, gamma+1}, softmax-weights metric        selection.cpp:110-135 */
+} sa_strategy;
+
+/* Selection granularity.  SA_PER_LAYER is the reference contract (one set per layer shared by
+ * all heads, scores averaged over ALL q-heads: selection.cpp:96); SA_PER_KV_HEAD
+ * averages over the G q-heads of each KV head and selects per KV head (north star). */
+typedef enum sa_select_mode { SA_PER_LAYER = 0, SA_PER_KV_HEAD = 1 } sa_select_mode;
+
+typedef struct sa_cache sa_cache;   /* paged bf16 KV cache for up to max_seqs sequences */
+typedef struct sa_runner sa_runner; /* workspaces + batch binding for the fused kernels  */
+
+SA_API const char* sa_status_string(sa_status s);
+SA_API const char* sa_last_error(void);
+SA_API const char* sa_version(void);
+
+/* ------------------------------------------------------------------------------------ cache */
+
+typedef struct sa_cache_config {
+  int64_t n_layers;    /* ModelConfig::n_layers   (kv_store.cpp:8-15 reads these four) */
+  int64_t n_kv_heads;  /* ModelConfig::n_kv_heads */
+  int64_t head_dim;    /* ModelConfig::head_dim (must be 128) */
+  int64_t max_context; /* ModelConfig::max_context, per sequence */
+  int64_t max_seqs;    /* sequences addressable by seq id 0..max_seqs-1 (reference: 1) */
+  int64_t page_size;   /* tokens per page (power of two >= 64); 0 -> 256 */
+  int64_t num_pages;   /* page pool size; 0 -> max_seqs * ceil(max_context / page_size) */
+} sa_cache_config;
+
+SA_API sa_status sa_cache_create(const sa_cache_config* cfg, sa_cache** out);
+SA_API sa_status sa_cache_destroy(sa_cache* cache);
+SA_API sa_status sa_kv_size(const sa_cache* cache, int32_t seq, int64_t* len);
+SA_API sa_status sa_kv_committed(const sa_cache* cache, int32_t seq, int64_t* committed);
+/* Reference accounting (fp32: 2*L*Hkv*d*4, kv_store.hpp:30) and the device (bf16) figure. */
+SA_API sa_status sa_kv_bytes_per_token(const sa_cache* cache, int64_t* ref_fp32_bytes, int64_t* device_bytes);
+
+/* Append n_tokens tokens (kv_store.cpp:29-49, batched).  keys/values: [n_tokens][n_layers*n_kv_heads]
+ * [head_dim] in layer-major row order, dtype SA_F32 or SA_BF16, device or host memory
+ * (keys_on_host != 0).  All-or-nothing: SA_LENGTH_ERROR if len + n_tokens > max_context. */
+SA_API sa_status sa_kv_append(sa_cache* cache, int32_t seq, int64_t n_tokens, const void* keys,
+                              const void* values, sa_dtype dtype, int keys_on_host, void* stream);
+/* kv_store.cpp:51-58: SA_OUT_OF_RANGE if to_len > len; committed = min(committed, to_len). */
+SA_API sa_status sa_kv_truncate(sa_cache* cache, int32_t seq, int64_t to_len);
+/* kv_store.cpp:60-65 */
+SA_API sa_status sa_kv_set_committed(sa_cache* cache, int32_t seq, int64_t len);
+/* Pre-allocate pages so rows [0, len) are addressable by fused appends (no length change). */
+SA_API sa_status sa_kv_reserve(sa_cache* cache, int32_t seq, int64_t len);
+/* Set the length after device-side fused appends (verify/draft wrote rows [len, new_len)). */
+SA_API sa_status sa_kv_set_size(sa_cache* cache, int32_t seq, int64_t new_len);
+/* kv_store.cpp:67-88: host indices, strictly increasing and < len (SA_OUT_OF_RANGE otherwise);
+ * K_out/V_out: device fp32 [n][head_dim]. */
+SA_API sa_status sa_kv_gather(const sa_cache* cache, int32_t seq, int64_t layer, int64_t kv_head,
+                              const int64_t* indices_host, int64_t n, float* K_out, float* V_out,
+                              void* stream);
+/* keys()/values() rows [begin, begin+n) as device fp32 [n][head_dim] (kv_store.hpp:48-54). */
+SA_API sa_status sa_kv_read(const sa_cache* cache, int32_t seq, int64_t layer, int64_t kv_head,
+                            int64_t begin, int64_t n, float* K_out, float* V_out, void* stream);
+
+/* ----------------------------------------------------------------------------------- runner */
+
+typedef struct sa_runner_config {
+  int32_t max_batch;     /* sequences per call */
+  int32_t n_q_heads;     /* Hq (multiple of n_kv_heads); G = Hq/Hkv */
+  int32_t max_rows;      /* gamma+1 upper bound; G*max_rows + 2 <= 64 */
+  int64_t max_prefix;    /* largest prefix length p0 a call will see */
+  double sparse_ratio;   /* SelectorConfig::sparse_ratio (selection.hpp:31) */
+  int64_t k_min;         /* SelectorConfig::k_min        (selection.hpp:32) */
+  int32_t n_layers_buf;  /* score/index buffers kept per layer (iteration keeps all L) ; 0 -> L */
+} sa_runner_config;
+
+SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, sa_runner** out);
+SA_API sa_status sa_runner_destroy(sa_runner* r);
+/* Bind a batch: seq_ids_host[n], prefix_len_host[n] (p0 = columns of the logit matrix; the
+ * gamma+1 verify rows sit at p0..p0+gamma).  Reserves pages for p0 + max_rows. */
+SA_API sa_status sa_runner_set_batch(sa_runner* r, int32_t n, const int32_t* seq_ids_host,
+                                     const int64_t* prefix_len_host);
+/* Per-layer device buffers owned by the runner (valid until destroy). */
+SA_API float* sa_runner_scores(sa_runner* r, int32_t layer_slot, int64_t* ld);      /* [B][Hkv][ld] */
+SA_API int32_t* sa_runner_indices(sa_runner* r, int32_t layer_slot, int32_t* k_cap); /* [B][sets][k_cap] */
+SA_API int32_t* sa_runner_counts(sa_runner* r, int32_t layer_slot);                  /* [B][sets] */
+
+/* Verify attention for one layer (attend_collect for every q-head x row):
+ * row t = 1..n_rows of q-head h sees prefix [0,p0) and window [p0, p0+t).  Emits the Collect-k
+ * score byproduct (raw q.k summed over the G heads of each KV head and the rows in
+ * score_row_mask) into the runner's score buffer for layer_slot, fused with the attention pass. */
+typedef struct sa_verify_args {
+  int32_t layer;            /* cache layer */
+  int32_t layer_slot;       /* runner score-buffer slot */
+  int32_t n_rows;           /* gamma+1 */
+  const void* q;            /* bf16 [B][Hq][n_rows][128] */
+  const void* k_new;        /* bf16 [B][n_rows][Hkv][128] appended at p0.. (fused); NULL = in cache */
+  const void* v_new;
+  float scale;              /* 1/sqrt(d) (attention.hpp:51) */
+  uint32_t score_row_mask;  /* bit r -> row r+1 contributes to the score (Collect-2: rows 1,gamma+1) */
+  float* out;               /* f32 [B][Hq][n_rows][128] */
+  float* logits;            /* optional raw prefix logits f32 [B][Hq][n_collect][ld_logits]; NULL = off */
+  int64_t ld_logits;
+  uint32_t collect_row_mask;/* rows whose raw logits go to `logits` (n_collect = popcount) */
+} sa_verify_args;
+SA_API sa_status sa_verify_attention(sa_runner* r, const sa_verify_args* a, void* stream);
+
+/* Top-k selection from the score byproduct (score_columns + selection_k + topk_indices,
+ * selection.cpp:89-108,63-66,137-158): k = clamp(llround(ratio*p0), k_min, p0) per sequence,
+ * descending score, ties to the lower index, output ascending int32. */
+typedef struct sa_select_args {
+  int32_t layer_slot;
+  sa_select_mode mode;
+  int32_t rows_in_score;    /* popcount(score_row_mask) used by verify: divisor = heads*rows */
+} sa_select_args;
+SA_API sa_status sa_select_topk(sa_runner* r, const sa_select_args* a, void* stream);
+
+/* Sparse draft attention for one layer (gather(T) ++ tail, then attend; kv_store.cpp:67-88,
+ * attention.cpp:70-76): query of q-head h at position p0+step-1 attends to the
+ * selected prefix T (layer_slot's index list; per-layer or per-KV-head) and the tail rows
+ * [p0, p0+step).  If k_new/v_new are given they are row p0+step-1, appended (fused). */
+typedef struct sa_draft_args {
+  int32_t layer;
+  int32_t layer_slot;
+  sa_select_mode mode;
+  int32_t step;             /* 1..gamma: tail length */
+  const void* q;            /* bf16 [B][Hq][128] */
+  const void* k_new;        /* bf16 [B][Hkv][128] or NULL */
+  const void* v_new;
+  float scale;
+  float* out;               /* f32 [B][Hq][128] */
+} sa_draft_args;
+SA_API sa_status sa_draft_attention(sa_runner* r, const sa_draft_args* a, void* stream);
+
+/* One speculation iteration of attention for all layers of the bound batch (SURVEY.md §8d unit):
+ * per layer verify (+fused append of gamma+1 rows) -> select (side stream, overlapped with the
+ * next layer's verify) ; then gamma draft steps, each over all layers in order (+fused append).
+ * Inputs are per-layer contiguous blocks:
+ *   qv  [L][B][Hq][gamma+1][128] bf16   kv_new/vv_new [L][B][gamma+1][Hkv][128] bf16
+ *   qd  [gamma][L][B][Hq][128] bf16     kd_new/vd_new [gamma][L][B][Hkv][128] bf16
+ *   out_v [L][B][Hq][gamma+1][128] f32   out_d [gamma][L][B][Hq][128] f32
+ * use_graph != 0 captures the launch sequence into a CUDA graph on first use and replays it. */
+typedef struct sa_iteration_args {
+  int32_t gamma;
+  sa_strategy strategy;     /* SA_COLLECT2 or SA_ALL_DRAFT on this path */
+  sa_select_mode mode;
+  float scale;
+  const void *qv, *kv_new, *vv_new, *qd, *kd_new, *vd_new;
+  float *out_v, *out_d;
+  int32_t use_graph;
+} sa_iteration_args;
+SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void* stream);
+/* Number of kernels one sa_iteration_run launches (for gpu_launches accounting). */
+SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_args* a);
+
+/* Reference helper: selection_k (selection.cpp:63-66). */
+SA_API int64_t sa_selection_k(double sparse_ratio, int64_t prefix_len, int64_t k_min);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECATTN_B200_H_ */

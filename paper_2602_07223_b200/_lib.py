@@ -1,0 +1,321 @@
+"""ctypes binding of include/specattn_b200.h (no torch types cross the ABI: plain pointers/sizes)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(HERE, "lib", "libspecattn_b200.so")
+
+SA_OK = 0
+STATUS = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 4: "length_error",
+          5: "cuda_error", 6: "not_supported", 7: "nccl_error"}
+LAST_ACCEPTED, ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS = 2, 3, 4, 5
+PER_LAYER, PER_KV_HEAD = 0, 1
+F32, BF16 = 0, 1
+
+
+class SpecAttnError(RuntimeError):
+    """Raised for any non-OK sa_status; .status carries the reference exception class name."""
+
+    def __init__(self, status: int, message: str):
+        self.status = STATUS.get(status, str(status))
+        super().__init__(f"{self.status}: {message}")
+
+
+_i64, _i32, _u32, _vp, _f32 = C.c_int64, C.c_int32, C.c_uint32, C.c_void_p, C.c_float
+
+
+class CacheConfig(C.Structure):
+    _fields_ = [("n_layers", _i64), ("n_kv_heads", _i64), ("head_dim", _i64), ("max_context", _i64),
+                ("max_seqs", _i64), ("page_size", _i64), ("num_pages", _i64)]
+
+
+class RunnerConfig(C.Structure):
+    _fields_ = [("max_batch", _i32), ("n_q_heads", _i32), ("max_rows", _i32), ("max_prefix", _i64),
+                ("sparse_ratio", C.c_double), ("k_min", _i64), ("n_layers_buf", _i32)]
+
+
+class VerifyArgs(C.Structure):
+    _fields_ = [("layer", _i32), ("layer_slot", _i32), ("n_rows", _i32), ("q", _vp), ("k_new", _vp),
+                ("v_new", _vp), ("scale", _f32), ("score_row_mask", _u32), ("out", _vp), ("logits", _vp),
+                ("ld_logits", _i64), ("collect_row_mask", _u32)]
+
+
+class SelectArgs(C.Structure):
+    _fields_ = [("layer_slot", _i32), ("mode", C.c_int), ("rows_in_score", _i32)]
+
+
+class DraftArgs(C.Structure):
+    _fields_ = [("layer", _i32), ("layer_slot", _i32), ("mode", C.c_int), ("step", _i32), ("q", _vp),
+                ("k_new", _vp), ("v_new", _vp), ("scale", _f32), ("out", _vp)]
+
+
+class IterationArgs(C.Structure):
+    _fields_ = [("gamma", _i32), ("strategy", C.c_int), ("mode", C.c_int), ("scale", _f32), ("qv", _vp),
+                ("kv_new", _vp), ("vv_new", _vp), ("qd", _vp), ("kd_new", _vp), ("vd_new", _vp), ("out_v", _vp),
+                ("out_d", _vp), ("use_graph", _i32)]
+
+
+# exported symbol -> (restype, argtypes)
+SIGNATURES = {
+    "sa_status_string": (C.c_char_p, [C.c_int]),
+    "sa_last_error": (C.c_char_p, []),
+    "sa_version": (C.c_char_p, []),
+    "sa_selection_k": (_i64, [C.c_double, _i64, _i64]),
+    "sa_cache_create": (C.c_int, [C.POINTER(CacheConfig), C.POINTER(_vp)]),
+    "sa_cache_destroy": (C.c_int, [_vp]),
+    "sa_kv_size": (C.c_int, [_vp, _i32, C.POINTER(_i64)]),
+    "sa_kv_committed": (C.c_int, [_vp, _i32, C.POINTER(_i64)]),
+    "sa_kv_bytes_per_token": (C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
+    "sa_kv_append": (C.c_int, [_vp, _i32, _i64, _vp, _vp, C.c_int, C.c_int, _vp]),
+    "sa_kv_truncate": (C.c_int, [_vp, _i32, _i64]),
+    "sa_kv_set_committed": (C.c_int, [_vp, _i32, _i64]),
+    "sa_kv_reserve": (C.c_int, [_vp, _i32, _i64]),
+    "sa_kv_set_size": (C.c_int, [_vp, _i32, _i64]),
+    "sa_kv_gather": (C.c_int, [_vp, _i32, _i64, _i64, C.POINTER(_i64), _i64, _vp, _vp, _vp]),
+    "sa_kv_read": (C.c_int, [_vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "sa_runner_create": (C.c_int, [_vp, C.POINTER(RunnerConfig), C.POINTER(_vp)]),
+    "sa_runner_destroy": (C.c_int, [_vp]),
+    "sa_runner_set_batch": (C.c_int, [_vp, _i32, C.POINTER(_i32), C.POINTER(_i64)]),
+    "sa_runner_scores": (_vp, [_vp, _i32, C.POINTER(_i64)]),
+    "sa_runner_indices": (_vp, [_vp, _i32, C.POINTER(_i32)]),
+    "sa_runner_counts": (_vp, [_vp, _i32]),
+    "sa_verify_attention": (C.c_int, [_vp, C.POINTER(VerifyArgs), _vp]),
+    "sa_select_topk": (C.c_int, [_vp, C.POINTER(SelectArgs), _vp]),
+    "sa_draft_attention": (C.c_int, [_vp, C.POINTER(DraftArgs), _vp]),
+    "sa_iteration_run": (C.c_int, [_vp, C.POINTER(IterationArgs), _vp]),
+    "sa_iteration_kernel_count": (_i64, [_vp, C.POINTER(IterationArgs)]),
+}
+
+_LIB = None
+
+
+def build() -> None:
+    """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    subprocess.run(["make", "-s", "-j8", "-C", os.path.join(HERE, "csrc")], check=True)
+
+
+def lib() -> C.CDLL:
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(lib_path):
+            raise SpecAttnError(6, f"{lib_path} missing — run __graft_entry__.build(); there is no CPU fallback")
+        L = C.CDLL(lib_path)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def _check(st: int) -> None:
+    if st != SA_OK:
+        raise SpecAttnError(st, lib().sa_last_error().decode())
+
+
+def selection_k(ratio: float, p: int, k_min: int) -> int:
+    return int(lib().sa_selection_k(ratio, p, k_min))
+
+
+def _ptr(t) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise SpecAttnError(1, "device tensor expected")
+    if not t.is_contiguous():
+        raise SpecAttnError(1, "contiguous tensor expected")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Cache:
+    """Device KV store (sa_cache): the KvStore API of kv_store.hpp:19-89 over a paged bf16 pool."""
+
+    def __init__(self, n_layers, n_kv_heads, head_dim=128, max_context=4096, max_seqs=1, page_size=256,
+                 num_pages=0):
+        import torch
+        if not torch.cuda.is_available():
+            raise SpecAttnError(5, "no CUDA device: the SpecAttn hot path has no CPU fallback")
+        self.L, self.Hkv, self.d = n_layers, n_kv_heads, head_dim
+        self.max_context, self.max_seqs = max_context, max_seqs
+        cfg = CacheConfig(n_layers, n_kv_heads, head_dim, max_context, max_seqs, page_size, num_pages)
+        h = _vp()
+        _check(lib().sa_cache_create(C.byref(cfg), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sa_cache_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def size(self, seq=0):
+        n = _i64()
+        _check(lib().sa_kv_size(self.h, seq, C.byref(n)))
+        return n.value
+
+    def committed(self, seq=0):
+        n = _i64()
+        _check(lib().sa_kv_committed(self.h, seq, C.byref(n)))
+        return n.value
+
+    def bytes_per_token(self):
+        a, b = _i64(), _i64()
+        _check(lib().sa_kv_bytes_per_token(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def append(self, keys, values, seq=0, stream=None):
+        """keys/values: [n_tokens][L*Hkv][d] (or one token [L*Hkv][d]); fp32 or bf16, device or host."""
+        import torch
+        if keys.dim() == 2:
+            keys, values = keys.unsqueeze(0), values.unsqueeze(0)
+        keys, values = keys.contiguous(), values.contiguous()
+        dt = F32 if keys.dtype == torch.float32 else BF16
+        if keys.dtype not in (torch.float32, torch.bfloat16) or values.dtype != keys.dtype:
+            raise SpecAttnError(1, "append expects fp32 or bf16")
+        _check(lib().sa_kv_append(self.h, seq, keys.shape[0], keys.data_ptr(), values.data_ptr(), dt,
+                                  0 if keys.is_cuda else 1, _stream(stream)))
+        return self.size(seq)
+
+    def truncate(self, to_len, seq=0):
+        _check(lib().sa_kv_truncate(self.h, seq, to_len))
+
+    def set_committed(self, n, seq=0):
+        _check(lib().sa_kv_set_committed(self.h, seq, n))
+
+    def reserve(self, n, seq=0):
+        _check(lib().sa_kv_reserve(self.h, seq, n))
+
+    def set_size(self, n, seq=0):
+        _check(lib().sa_kv_set_size(self.h, seq, n))
+
+    def gather(self, layer, kv_head, indices, seq=0, stream=None):
+        import torch
+        idx = [int(i) for i in indices]
+        arr = (_i64 * max(len(idx), 1))(*idx)
+        K = torch.empty((len(idx), self.d), dtype=torch.float32, device="cuda")
+        V = torch.empty_like(K)
+        _check(lib().sa_kv_gather(self.h, seq, layer, kv_head, arr, len(idx), K.data_ptr() if len(idx) else None,
+                                  V.data_ptr() if len(idx) else None, _stream(stream)))
+        return K, V
+
+    def read(self, layer, kv_head, begin, n, seq=0, stream=None):
+        import torch
+        K = torch.empty((n, self.d), dtype=torch.float32, device="cuda")
+        V = torch.empty_like(K)
+        _check(lib().sa_kv_read(self.h, seq, layer, kv_head, begin, n, K.data_ptr() if n else None,
+                                V.data_ptr() if n else None, _stream(stream)))
+        return K, V
+
+
+class Runner:
+    """Workspaces + batch binding for the fused verify / select / draft kernels."""
+
+    def __init__(self, cache: Cache, n_q_heads, max_rows, max_prefix, max_batch=1, sparse_ratio=0.07, k_min=16,
+                 n_layers_buf=0):
+        self.cache = cache
+        self.Hq, self.G = n_q_heads, n_q_heads // cache.Hkv
+        cfg = RunnerConfig(max_batch, n_q_heads, max_rows, max_prefix, sparse_ratio, k_min, n_layers_buf)
+        h = _vp()
+        _check(lib().sa_runner_create(cache.h, C.byref(cfg), C.byref(h)))
+        self.h = h
+        self.sparse_ratio, self.k_min = sparse_ratio, k_min
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sa_runner_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def set_batch(self, seq_ids, prefix_lens):
+        n = len(seq_ids)
+        s = (_i32 * n)(*seq_ids)
+        p = (_i64 * n)(*prefix_lens)
+        _check(lib().sa_runner_set_batch(self.h, n, s, p))
+        self.B = n
+
+    def scores(self, slot):
+        ld = _i64()
+        ptr = lib().sa_runner_scores(self.h, slot, C.byref(ld))
+        return ptr, ld.value
+
+    def selection(self, slot, n_sets):
+        """(indices [B][n_sets][k_cap] int32, counts [B][n_sets]) copied to host numpy."""
+        import numpy as np
+        import torch
+        kc = _i32()
+        ip = lib().sa_runner_indices(self.h, slot, C.byref(kc))
+        cp = lib().sa_runner_counts(self.h, slot)
+        torch.cuda.synchronize()
+        nidx = self.B * n_sets * kc.value
+        idx = np.empty(nidx, np.int32)
+        cnt = np.empty(self.B * n_sets, np.int32)
+        cudart_memcpy(idx.ctypes.data, ip, idx.nbytes)
+        cudart_memcpy(cnt.ctypes.data, cp, cnt.nbytes)
+        return idx.reshape(self.B, n_sets, kc.value), cnt.reshape(self.B, n_sets)
+
+    def verify(self, layer, q, out, k_new=None, v_new=None, scale=None, score_row_mask=None, layer_slot=None,
+               logits=None, collect_row_mask=0, stream=None):
+        R = q.shape[-2]
+        if scale is None:
+            scale = float((1.0 / 128 ** 0.5))
+        if score_row_mask is None:
+            score_row_mask = 1 | (1 << (R - 1))
+        a = VerifyArgs(layer, layer if layer_slot is None else layer_slot, R, _ptr(q), _ptr(k_new), _ptr(v_new),
+                       scale, score_row_mask, _ptr(out), _ptr(logits),
+                       0 if logits is None else logits.shape[-1], collect_row_mask)
+        _check(lib().sa_verify_attention(self.h, C.byref(a), _stream(stream)))
+
+    def select(self, layer_slot, mode=PER_LAYER, rows_in_score=2, stream=None):
+        a = SelectArgs(layer_slot, mode, rows_in_score)
+        _check(lib().sa_select_topk(self.h, C.byref(a), _stream(stream)))
+
+    def draft(self, layer, step, q, out, k_new=None, v_new=None, mode=PER_LAYER, scale=None, layer_slot=None,
+              stream=None):
+        if scale is None:
+            scale = float((1.0 / 128 ** 0.5))
+        a = DraftArgs(layer, layer if layer_slot is None else layer_slot, mode, step, _ptr(q), _ptr(k_new),
+                      _ptr(v_new), scale, _ptr(out))
+        _check(lib().sa_draft_attention(self.h, C.byref(a), _stream(stream)))
+
+    def iteration_args(self, gamma, qv, kv_new, vv_new, qd, kd_new, vd_new, out_v, out_d, strategy=COLLECT2,
+                       mode=PER_LAYER, scale=None, use_graph=True):
+        if scale is None:
+            scale = float((1.0 / 128 ** 0.5))
+        return IterationArgs(gamma, strategy, mode, scale, _ptr(qv), _ptr(kv_new), _ptr(vv_new), _ptr(qd),
+                             _ptr(kd_new), _ptr(vd_new), _ptr(out_v), _ptr(out_d), int(use_graph))
+
+    def iteration(self, args: IterationArgs, stream=None):
+        _check(lib().sa_iteration_run(self.h, C.byref(args), _stream(stream)))
+
+    def iteration_kernel_count(self, args: IterationArgs) -> int:
+        return int(lib().sa_iteration_kernel_count(self.h, C.byref(args)))
+
+
+def cudart_memcpy(dst: int, src: int, nbytes: int) -> None:
+    """Device->host copy of raw device memory through torch (no second CUDA runtime in Python)."""
+    if nbytes == 0:
+        return
+    host = _device_bytes(src, nbytes).cpu().numpy()
+    C.memmove(dst, host.ctypes.data, nbytes)
+
+
+def _device_bytes(ptr: int, nbytes: int):
+    """A uint8 CUDA tensor aliasing raw device memory (via the __cuda_array_interface__)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
+
+    return torch.as_tensor(_Arr(), device="cuda")

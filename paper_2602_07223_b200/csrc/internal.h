@@ -1,0 +1,122 @@
+// internal.h — host-side structures shared by the C-ABI translation units.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/specattn_b200.h"
+#include "common.cuh"
+
+namespace sa {
+
+// Thread-local error message set by every failing entry point.
+sa_status fail(sa_status st, const std::string& msg);
+sa_status cuda_fail(cudaError_t e, const char* where);
+#define SA_CUDA_CHECK(expr)                                         \
+  do {                                                              \
+    cudaError_t _e = (expr);                                        \
+    if (_e != cudaSuccess) return ::sa::cuda_fail(_e, #expr);       \
+  } while (0)
+
+bool encode_tensor_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t box_rows, std::string* err);
+
+}  // namespace sa
+
+struct sa_cache {
+  int64_t n_layers = 0, n_kv_heads = 0, head_dim = 0, max_context = 0, max_seqs = 0;
+  int64_t page_size = 0, page_shift = 0, num_pages = 0, max_pages_per_seq = 0;
+  __nv_bfloat16* k_pool = nullptr;
+  __nv_bfloat16* v_pool = nullptr;
+  int32_t* d_block_table = nullptr;          // [max_seqs][max_pages_per_seq]
+  std::vector<int32_t> h_block_table;
+  std::vector<int64_t> len, committed, pages_of_seq;
+  std::vector<int32_t> free_pages;           // LIFO free list
+  CUtensorMap tmap_k{}, tmap_v{};            // 2-D [rows][128] bf16, box {64, 64}, SWIZZLE_128B
+  int device = 0;
+
+  sa::CacheView view() const {
+    sa::CacheView v;
+    v.k = k_pool;
+    v.v = v_pool;
+    v.block_table = d_block_table;
+    v.max_pages_per_seq = static_cast<int32_t>(max_pages_per_seq);
+    v.num_pages = static_cast<int32_t>(num_pages);
+    v.page_shift = static_cast<int32_t>(page_shift);
+    v.n_kv_heads = static_cast<int32_t>(n_kv_heads);
+    v.n_layers = static_cast<int32_t>(n_layers);
+    v.max_context = static_cast<int32_t>(max_context);
+    return v;
+  }
+  sa_status reserve(int32_t seq, int64_t rows);  // allocate pages for [0, rows)
+};
+
+namespace sa {
+
+// ---- kernel launch parameter blocks (also used by the launchers in verify.cu / draft.cu / select.cu)
+
+struct VerifyParams {
+  CacheView cache;
+  int layer, B, Hkv, G, R, M, MT, hi_row;
+  const int32_t* seq_ids;
+  const int32_t* p0;
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k_new;
+  const __nv_bfloat16* v_new;
+  float scale_log2;
+  uint32_t score_mask;
+  float* out;
+  float* scores;
+  int64_t ld_scores;
+  float* logits;
+  int64_t ld_logits;
+  uint32_t collect_mask;
+  int n_collect;
+  int n_splits, chunk;
+  float* part_o;   // [B*Hkv][n_splits][MT*16][128]
+  float* part_ml;  // [B*Hkv][n_splits][MT*16][2]
+  int* counters;   // [B*Hkv]
+};
+
+struct DraftParams {
+  CacheView cache;
+  int layer, B, Hkv, G, step;
+  const int32_t* seq_ids;
+  const int32_t* p0;
+  const __nv_bfloat16* q;
+  const __nv_bfloat16* k_new;
+  const __nv_bfloat16* v_new;
+  const int32_t* idx;
+  const int32_t* k_act;
+  int n_sets, k_cap;
+  float scale_log2;
+  float* out;
+  int n_splits, chunk;
+  float* part_o;   // [B*Hkv][n_splits][16][128]
+  float* part_ml;
+  int* counters;
+};
+
+struct SelectParams {
+  int B, Hkv, n_sets;
+  const int32_t* p0;
+  const float* scores;
+  int64_t ld_scores;
+  double count;  // (#q-heads in the set) * rows_in_score
+  double ratio;
+  int64_t k_min;
+  int k_cap;
+  uint32_t* keys;  // workspace [B][n_sets][ld_scores]
+  int32_t* idx;    // [B][n_sets][k_cap]
+  int32_t* k_out;  // [B][n_sets]
+};
+
+cudaError_t launch_verify(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
+cudaError_t launch_draft(const DraftParams& p, cudaStream_t s);
+cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+size_t verify_smem_bytes(int MT);
+int verify_max_ctas_per_sm(int MT);
+
+}  // namespace sa

@@ -1,0 +1,430 @@
+// runner.cu — batch binding, workspaces, per-layer entry points and the iteration driver.
+//
+// The iteration driver is the GPU-side analogue of the SPEC decode_iteration (SPEC.md:409-417,
+// absent from the reference code): per layer verify -> select, the select on a side stream so it
+// overlaps the next layer's verify (it is consumed only by the next draft phase), then gamma
+// dependent draft steps over all layers.  The whole launch sequence is captured once into a CUDA
+// graph and replayed.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+using sa::fail;
+
+struct sa_runner {
+  sa_cache* cache = nullptr;
+  sa_runner_config cfg{};
+  int Hq = 0, Hkv = 0, G = 0, n_slots = 0, num_sms = 148;
+  // bound batch
+  int B = 0;
+  std::vector<int32_t> h_seq;
+  std::vector<int64_t> h_p0;
+  int64_t p_max = 0;
+  int32_t* d_seq = nullptr;
+  int32_t* d_p0 = nullptr;
+  // selection buffers
+  int64_t ld = 0;
+  float* scores = nullptr;     // [slots][max_batch][Hkv][ld]
+  int k_cap = 0;
+  int32_t* idx = nullptr;      // [slots][max_batch][Hkv][k_cap]
+  int32_t* kcnt = nullptr;     // [slots][max_batch][Hkv]
+  uint32_t* keys = nullptr;    // [max_batch][Hkv][ld]
+  // split-KV workspaces
+  int64_t v_units_cap = 0, d_units_cap = 0;
+  float *v_po = nullptr, *v_pml = nullptr, *d_po = nullptr, *d_pml = nullptr;
+  int *v_cnt = nullptr, *d_cnt = nullptr;
+  // streams / graph
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev_v, ev_s;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<char> gkey;
+};
+
+namespace {
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// Pick the split count for `units` independent (sequence, KV head) units of `len` keys: minimise
+// (waves x per-CTA keys) + a per-split merge cost, chunks a multiple of `gran`.
+int choose_splits(int64_t units, int64_t len, int64_t gran, int64_t max_chunk, int64_t slots_per_wave,
+                  int64_t max_ctas, int* chunk_out) {
+  len = std::max<int64_t>(len, 1);
+  int best_n = 1;
+  int64_t best_chunk = round_up(len, gran), best_cost = -1;
+  for (int64_t n = 1; n <= 256; ++n) {
+    int64_t chunk = round_up((len + n - 1) / n, gran);
+    if (max_chunk && chunk > max_chunk) continue;
+    const int64_t nn = (len + chunk - 1) / chunk;
+    if (nn != n) continue;
+    if (units * nn > max_ctas) break;
+    const int64_t waves = (units * nn + slots_per_wave - 1) / slots_per_wave;
+    const int64_t cost = waves * chunk + 2 * gran * nn / std::max<int64_t>(1, slots_per_wave / units);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best_n = static_cast<int>(nn);
+      best_chunk = chunk;
+    }
+  }
+  *chunk_out = static_cast<int>(best_chunk);
+  return best_n;
+}
+
+int mtiles_for(int G, int R) { return (G * R + 2 + 15) / 16; }
+
+}  // namespace
+
+extern "C" {
+
+SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, sa_runner** out) {
+  if (!cache || !cfg || !out) return fail(SA_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (cfg->n_q_heads < 1 || cfg->n_q_heads % cache->n_kv_heads)
+    return fail(SA_INVALID_ARGUMENT, "n_q_heads must be a positive multiple of n_kv_heads");
+  const int G = cfg->n_q_heads / static_cast<int>(cache->n_kv_heads);
+  if (G > 16) return fail(SA_NOT_SUPPORTED, "GQA group size > 16");
+  if (cfg->max_rows < 1 || mtiles_for(G, cfg->max_rows) > 4)
+    return fail(SA_NOT_SUPPORTED, "G*(gamma+1)+2 must be <= 64");
+  if (cfg->max_batch < 1 || cfg->max_batch > cache->max_seqs) return fail(SA_INVALID_ARGUMENT, "max_batch");
+  if (cfg->max_prefix < 0 || cfg->max_prefix + cfg->max_rows > cache->max_context)
+    return fail(SA_LENGTH_ERROR, "max_prefix + max_rows exceeds max_context");
+  if (!(cfg->sparse_ratio > 0.0) || cfg->sparse_ratio > 1.0)
+    return fail(SA_INVALID_ARGUMENT, "SelectorConfig: sparse_ratio must be in (0, 1]");  // selection.cpp:50-53
+  if (cfg->k_min < 0) return fail(SA_INVALID_ARGUMENT, "SelectorConfig: k_min must be >= 0");
+  auto* r = new sa_runner();
+  r->cache = cache;
+  r->cfg = *cfg;
+  r->Hkv = static_cast<int>(cache->n_kv_heads);
+  r->Hq = cfg->n_q_heads;
+  r->G = G;
+  r->n_slots = cfg->n_layers_buf > 0 ? cfg->n_layers_buf : static_cast<int>(cache->n_layers);
+  cudaDeviceGetAttribute(&r->num_sms, cudaDevAttrMultiProcessorCount, cache->device);
+  r->ld = std::max<int64_t>(64, round_up(cfg->max_prefix, 64));
+  r->k_cap = static_cast<int>(std::max<int64_t>(1, sa_selection_k(cfg->sparse_ratio, cfg->max_prefix, cfg->k_min)));
+  const int64_t mb = cfg->max_batch, H = r->Hkv, S = r->n_slots;
+  r->v_units_cap = std::max<int64_t>(4 * r->num_sms, mb * H);
+  r->d_units_cap = std::max<int64_t>(8 * r->num_sms, mb * H);
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) e = cudaMemset(*p, 0, std::max<size_t>(bytes, 16));
+  };
+  alloc(reinterpret_cast<void**>(&r->d_seq), sizeof(int32_t) * mb);
+  alloc(reinterpret_cast<void**>(&r->d_p0), sizeof(int32_t) * mb);
+  alloc(reinterpret_cast<void**>(&r->scores), sizeof(float) * S * mb * H * r->ld);
+  alloc(reinterpret_cast<void**>(&r->idx), sizeof(int32_t) * S * mb * H * r->k_cap);
+  alloc(reinterpret_cast<void**>(&r->kcnt), sizeof(int32_t) * S * mb * H);
+  alloc(reinterpret_cast<void**>(&r->keys), sizeof(uint32_t) * mb * H * r->ld);
+  alloc(reinterpret_cast<void**>(&r->v_po), sizeof(float) * r->v_units_cap * 64 * 128);
+  alloc(reinterpret_cast<void**>(&r->v_pml), sizeof(float) * r->v_units_cap * 64 * 2);
+  alloc(reinterpret_cast<void**>(&r->v_cnt), sizeof(int) * mb * H);
+  alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
+  alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
+  alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
+  r->ev_v.resize(S);
+  r->ev_s.resize(S);
+  for (int64_t i = 0; i < S && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&r->ev_v[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_s[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->ev_join, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    sa_runner_destroy(r);
+    return sa::cuda_fail(e, "sa_runner_create");
+  }
+  *out = r;
+  return SA_OK;
+}
+
+SA_API sa_status sa_runner_destroy(sa_runner* r) {
+  if (!r) return SA_OK;
+  if (r->gexec) cudaGraphExecDestroy(r->gexec);
+  for (auto ev : r->ev_v) if (ev) cudaEventDestroy(ev);
+  for (auto ev : r->ev_s) if (ev) cudaEventDestroy(ev);
+  if (r->ev_fork) cudaEventDestroy(r->ev_fork);
+  if (r->ev_join) cudaEventDestroy(r->ev_join);
+  if (r->side) cudaStreamDestroy(r->side);
+  for (void* p : {static_cast<void*>(r->d_seq), static_cast<void*>(r->d_p0), static_cast<void*>(r->scores),
+                  static_cast<void*>(r->idx), static_cast<void*>(r->kcnt), static_cast<void*>(r->keys),
+                  static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_cnt),
+                  static_cast<void*>(r->d_po), static_cast<void*>(r->d_pml), static_cast<void*>(r->d_cnt)})
+    cudaFree(p);
+  delete r;
+  return SA_OK;
+}
+
+SA_API sa_status sa_runner_set_batch(sa_runner* r, int32_t n, const int32_t* seq_ids, const int64_t* p0) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  if (n < 1 || n > r->cfg.max_batch) return fail(SA_INVALID_ARGUMENT, "batch size out of range");
+  std::vector<int32_t> s32(n), p32(n);
+  int64_t pm = 0;
+  for (int i = 0; i < n; ++i) {
+    if (seq_ids[i] < 0 || seq_ids[i] >= r->cache->max_seqs) return fail(SA_OUT_OF_RANGE, "sequence id out of range");
+    for (int j2 = 0; j2 < i; ++j2)
+      if (seq_ids[j2] == seq_ids[i]) return fail(SA_INVALID_ARGUMENT, "duplicate sequence in batch");
+    if (p0[i] < 0 || p0[i] > r->cfg.max_prefix) return fail(SA_OUT_OF_RANGE, "prefix length beyond runner max_prefix");
+    if (p0[i] > r->cache->len[seq_ids[i]]) return fail(SA_OUT_OF_RANGE, "prefix beyond store length");
+    if (sa_status st = r->cache->reserve(seq_ids[i], p0[i] + r->cfg.max_rows)) return st;
+    s32[i] = seq_ids[i];
+    p32[i] = static_cast<int32_t>(p0[i]);
+    pm = std::max(pm, p0[i]);
+  }
+  SA_CUDA_CHECK(cudaMemcpy(r->d_seq, s32.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  SA_CUDA_CHECK(cudaMemcpy(r->d_p0, p32.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  r->B = n;
+  r->h_seq.assign(seq_ids, seq_ids + n);
+  r->h_p0.assign(p0, p0 + n);
+  r->p_max = pm;
+  return SA_OK;
+}
+
+SA_API float* sa_runner_scores(sa_runner* r, int32_t slot, int64_t* ld) {
+  if (!r || slot < 0 || slot >= r->n_slots) return nullptr;
+  if (ld) *ld = r->ld;
+  return r->scores + static_cast<size_t>(slot) * r->cfg.max_batch * r->Hkv * r->ld;
+}
+SA_API int32_t* sa_runner_indices(sa_runner* r, int32_t slot, int32_t* k_cap) {
+  if (!r || slot < 0 || slot >= r->n_slots) return nullptr;
+  if (k_cap) *k_cap = r->k_cap;
+  return r->idx + static_cast<size_t>(slot) * r->cfg.max_batch * r->Hkv * r->k_cap;
+}
+SA_API int32_t* sa_runner_counts(sa_runner* r, int32_t slot) {
+  if (!r || slot < 0 || slot >= r->n_slots) return nullptr;
+  return r->kcnt + static_cast<size_t>(slot) * r->cfg.max_batch * r->Hkv;
+}
+
+static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t s) {
+  if (!a || !a->q || !a->out) return fail(SA_INVALID_ARGUMENT, "verify: null argument");
+  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "verify: no batch bound");
+  if (a->layer < 0 || a->layer >= r->cache->n_layers) return fail(SA_OUT_OF_RANGE, "verify: layer out of range");
+  if (a->layer_slot < 0 || a->layer_slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "verify: layer_slot");
+  if (a->n_rows < 1 || a->n_rows > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "verify: n_rows out of range");
+  if (!(a->scale > 0.f)) return fail(SA_INVALID_ARGUMENT, "softmax_stable: scale must be positive");
+  if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(SA_INVALID_ARGUMENT, "verify: k_new/v_new");
+  if (a->score_row_mask >> a->n_rows) return fail(SA_INVALID_ARGUMENT, "score_columns: row label not collected");
+  if (a->logits && (a->collect_row_mask == 0 || (a->collect_row_mask >> a->n_rows) || a->ld_logits < r->p_max))
+    return fail(SA_INVALID_ARGUMENT, "verify: logits collection arguments");
+  if (!a->k_new)
+    for (int i = 0; i < r->B; ++i)
+      if (r->h_p0[i] + a->n_rows > r->cache->len[r->h_seq[i]])
+        return fail(SA_OUT_OF_RANGE, "verify: window rows not in the store");
+  sa::VerifyParams p{};
+  p.cache = r->cache->view();
+  p.layer = a->layer;
+  p.B = r->B;
+  p.Hkv = r->Hkv;
+  p.G = r->G;
+  p.R = a->n_rows;
+  p.M = r->G * a->n_rows;
+  p.MT = mtiles_for(r->G, a->n_rows);
+  p.hi_row = std::max(p.M, 16 * (p.MT - 1));
+  p.seq_ids = r->d_seq;
+  p.p0 = r->d_p0;
+  p.q = static_cast<const __nv_bfloat16*>(a->q);
+  p.k_new = static_cast<const __nv_bfloat16*>(a->k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(a->v_new);
+  p.scale_log2 = a->scale * sa::kLog2e;
+  p.score_mask = a->score_row_mask;
+  p.out = a->out;
+  p.scores = a->score_row_mask ? sa_runner_scores(r, a->layer_slot, &p.ld_scores) : nullptr;
+  p.logits = a->logits;
+  p.ld_logits = a->ld_logits;
+  p.collect_mask = a->collect_row_mask;
+  p.n_collect = __builtin_popcount(a->collect_row_mask);
+  const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
+  p.n_splits = choose_splits(units, r->p_max, 64, 0, r->num_sms * sa::verify_max_ctas_per_sm(p.MT),
+                             r->v_units_cap, &p.chunk);
+  p.part_o = r->v_po;
+  p.part_ml = r->v_pml;
+  p.counters = r->v_cnt;
+  cudaError_t e = sa::launch_verify(p, r->cache->tmap_k, r->cache->tmap_v, s);
+  if (e != cudaSuccess) return sa::cuda_fail(e, "verify launch");
+  return SA_OK;
+}
+
+static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t s) {
+  if (!a) return fail(SA_INVALID_ARGUMENT, "select: null argument");
+  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "select: no batch bound");
+  if (a->layer_slot < 0 || a->layer_slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "select: layer_slot");
+  if (a->rows_in_score < 1) return fail(SA_INVALID_ARGUMENT, "score_columns: empty row subset");
+  sa::SelectParams p{};
+  p.B = r->B;
+  p.Hkv = r->Hkv;
+  p.n_sets = a->mode == SA_PER_LAYER ? 1 : r->Hkv;
+  p.p0 = r->d_p0;
+  p.scores = sa_runner_scores(r, a->layer_slot, &p.ld_scores);
+  p.count = static_cast<double>(a->mode == SA_PER_LAYER ? r->Hq : r->G) * a->rows_in_score;
+  p.ratio = r->cfg.sparse_ratio;
+  p.k_min = r->cfg.k_min;
+  p.k_cap = r->k_cap;
+  p.keys = r->keys;
+  p.idx = sa_runner_indices(r, a->layer_slot, nullptr);
+  p.k_out = sa_runner_counts(r, a->layer_slot);
+  // per-layer sets live at set 0 of each sequence's [Hkv] block; keep the stride = Hkv sets
+  // by addressing with n_sets below (the kernel indexes [b][n_sets]); use a dense layout.
+  cudaError_t e = sa::launch_select(p, s);
+  if (e != cudaSuccess) return sa::cuda_fail(e, "select launch");
+  return SA_OK;
+}
+
+static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s) {
+  if (!a || !a->q || !a->out) return fail(SA_INVALID_ARGUMENT, "draft: null argument");
+  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "draft: no batch bound");
+  if (a->layer < 0 || a->layer >= r->cache->n_layers) return fail(SA_OUT_OF_RANGE, "draft: layer out of range");
+  if (a->layer_slot < 0 || a->layer_slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "draft: layer_slot");
+  if (a->step < 1 || a->step > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "draft: step out of range");
+  if (!(a->scale > 0.f)) return fail(SA_INVALID_ARGUMENT, "softmax_stable: scale must be positive");
+  if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(SA_INVALID_ARGUMENT, "draft: k_new/v_new");
+  for (int i = 0; i < r->B; ++i) {
+    const int64_t need = r->h_p0[i] + a->step - (a->k_new ? 1 : 0);
+    if (need > r->cache->len[r->h_seq[i]] && !a->k_new)
+      return fail(SA_OUT_OF_RANGE, "KvStore: gather indices must be strictly increasing and in range");
+  }
+  sa::DraftParams p{};
+  p.cache = r->cache->view();
+  p.layer = a->layer;
+  p.B = r->B;
+  p.Hkv = r->Hkv;
+  p.G = r->G;
+  p.step = a->step;
+  p.seq_ids = r->d_seq;
+  p.p0 = r->d_p0;
+  p.q = static_cast<const __nv_bfloat16*>(a->q);
+  p.k_new = static_cast<const __nv_bfloat16*>(a->k_new);
+  p.v_new = static_cast<const __nv_bfloat16*>(a->v_new);
+  p.n_sets = a->mode == SA_PER_LAYER ? 1 : r->Hkv;
+  p.idx = sa_runner_indices(r, a->layer_slot, &p.k_cap);
+  p.k_act = sa_runner_counts(r, a->layer_slot);
+  p.scale_log2 = a->scale * sa::kLog2e;
+  p.out = a->out;
+  const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
+  p.n_splits = choose_splits(units, r->k_cap + a->step, 64, 128, 3 * r->num_sms, r->d_units_cap, &p.chunk);
+  p.part_o = r->d_po;
+  p.part_ml = r->d_pml;
+  p.counters = r->d_cnt;
+  cudaError_t e = sa::launch_draft(p, s);
+  if (e != cudaSuccess) return sa::cuda_fail(e, "draft launch");
+  return SA_OK;
+}
+
+SA_API sa_status sa_verify_attention(sa_runner* r, const sa_verify_args* a, void* stream) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  return verify_impl(r, a, static_cast<cudaStream_t>(stream));
+}
+SA_API sa_status sa_select_topk(sa_runner* r, const sa_select_args* a, void* stream) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  return select_impl(r, a, static_cast<cudaStream_t>(stream));
+}
+SA_API sa_status sa_draft_attention(sa_runner* r, const sa_draft_args* a, void* stream) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  return draft_impl(r, a, static_cast<cudaStream_t>(stream));
+}
+
+SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_args* a) {
+  if (!r || !a) return 0;
+  const int64_t L = r->cache->n_layers;
+  return L /*verify*/ + L /*select*/ + static_cast<int64_t>(a->gamma) * L /*draft*/;
+}
+
+static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cudaStream_t main) {
+  const int L = static_cast<int>(r->cache->n_layers), B = r->B, R = a->gamma + 1;
+  const uint32_t mask = a->strategy == SA_ALL_DRAFT ? ((1u << R) - 1u) : (1u | (1u << a->gamma));
+  const int rows_in_score = __builtin_popcount(mask);
+  const size_t qv_l = static_cast<size_t>(B) * r->Hq * R * 128, kv_l = static_cast<size_t>(B) * R * r->Hkv * 128;
+  const size_t qd_l = static_cast<size_t>(B) * r->Hq * 128, kd_l = static_cast<size_t>(B) * r->Hkv * 128;
+  const auto* qv = static_cast<const __nv_bfloat16*>(a->qv);
+  const auto* kvn = static_cast<const __nv_bfloat16*>(a->kv_new);
+  const auto* vvn = static_cast<const __nv_bfloat16*>(a->vv_new);
+  const auto* qd = static_cast<const __nv_bfloat16*>(a->qd);
+  const auto* kdn = static_cast<const __nv_bfloat16*>(a->kd_new);
+  const auto* vdn = static_cast<const __nv_bfloat16*>(a->vd_new);
+  SA_CUDA_CHECK(cudaEventRecord(r->ev_fork, main));
+  SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
+  for (int l = 0; l < L; ++l) {
+    sa_verify_args v{};
+    v.layer = l;
+    v.layer_slot = l;
+    v.n_rows = R;
+    v.q = qv + l * qv_l;
+    v.k_new = kvn ? kvn + l * kv_l : nullptr;
+    v.v_new = vvn ? vvn + l * kv_l : nullptr;
+    v.scale = a->scale;
+    v.score_row_mask = mask;
+    v.out = a->out_v + l * qv_l;
+    if (sa_status st = verify_impl(r, &v, main)) return st;
+    SA_CUDA_CHECK(cudaEventRecord(r->ev_v[l], main));
+    SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_v[l], 0));
+    sa_select_args sel{};
+    sel.layer_slot = l;
+    sel.mode = a->mode;
+    sel.rows_in_score = rows_in_score;
+    if (sa_status st = select_impl(r, &sel, r->side)) return st;
+    SA_CUDA_CHECK(cudaEventRecord(r->ev_s[l], r->side));
+  }
+  for (int j = 1; j <= a->gamma; ++j) {
+    for (int l = 0; l < L; ++l) {
+      if (j == 1) SA_CUDA_CHECK(cudaStreamWaitEvent(main, r->ev_s[l], 0));
+      sa_draft_args d{};
+      d.layer = l;
+      d.layer_slot = l;
+      d.mode = a->mode;
+      d.step = j;
+      const size_t off = (static_cast<size_t>(j - 1) * L + l);
+      d.q = qd + off * qd_l;
+      d.k_new = kdn ? kdn + off * kd_l : nullptr;
+      d.v_new = vdn ? vdn + off * kd_l : nullptr;
+      d.scale = a->scale;
+      d.out = a->out_d + off * qd_l;
+      if (sa_status st = draft_impl(r, &d, main)) return st;
+    }
+  }
+  SA_CUDA_CHECK(cudaEventRecord(r->ev_join, r->side));
+  SA_CUDA_CHECK(cudaStreamWaitEvent(main, r->ev_join, 0));
+  return SA_OK;
+}
+
+SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void* stream) {
+  if (!r || !a) return fail(SA_INVALID_ARGUMENT, "null argument");
+  if (a->gamma < 0 || a->gamma + 1 > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "gamma out of range");
+  if (a->gamma < 1) return fail(SA_INVALID_ARGUMENT, "DecodeParams: gamma must be >= 1");
+  if (a->strategy != SA_COLLECT2 && a->strategy != SA_ALL_DRAFT)
+    return fail(SA_NOT_SUPPORTED, "iteration: strategy must be collect2 or all_draft");
+  if (r->n_slots < r->cache->n_layers) return fail(SA_INVALID_ARGUMENT, "iteration needs n_layers_buf >= n_layers");
+  if (!a->qv || !a->qd || !a->out_v || !a->out_d) return fail(SA_INVALID_ARGUMENT, "iteration: null buffer");
+  cudaStream_t main = static_cast<cudaStream_t>(stream);
+  if (!a->use_graph) return enqueue_iteration(r, a, main);
+  std::vector<char> key(sizeof(sa_iteration_args) + sizeof(int) + r->h_p0.size() * sizeof(int64_t) +
+                        r->h_seq.size() * sizeof(int32_t));
+  std::memcpy(key.data(), a, sizeof(*a));
+  std::memcpy(key.data() + sizeof(*a), &r->B, sizeof(int));
+  std::memcpy(key.data() + sizeof(*a) + sizeof(int), r->h_p0.data(), r->h_p0.size() * sizeof(int64_t));
+  std::memcpy(key.data() + sizeof(*a) + sizeof(int) + r->h_p0.size() * sizeof(int64_t), r->h_seq.data(),
+              r->h_seq.size() * sizeof(int32_t));
+  if (!r->gexec || key != r->gkey) {
+    if (r->gexec) {
+      cudaGraphExecDestroy(r->gexec);
+      r->gexec = nullptr;
+    }
+    cudaGraph_t graph = nullptr;
+    SA_CUDA_CHECK(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+    sa_status st = enqueue_iteration(r, a, main);
+    cudaError_t e = cudaStreamEndCapture(main, &graph);
+    if (st != SA_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return sa::cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&r->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return sa::cuda_fail(e, "cudaGraphInstantiate");
+    r->gkey = std::move(key);
+  }
+  SA_CUDA_CHECK(cudaGraphLaunch(r->gexec, main));
+  return SA_OK;
+}
+
+}  // extern "C"

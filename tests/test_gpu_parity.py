@@ -1,0 +1,303 @@
+"""GPU parity: every op through the C ABI vs the reference's own CPU code (oracle/_ref) on the
+same seeded bf16-representable inputs.  Bars (north star / SURVEY.md §8c):
+  attention outputs  <= 2e-3 max relative error (we also assert the much tighter measured level)
+  logits             |d| <= 1e-5 * sum_j |q_j k_j|
+  index sets         bit-exact outside the 2e-3 score tie band; exact on planted exact ties
+"""
+import numpy as np
+import pytest
+
+from oracle.counter_rng import normal_bf16
+from oracle.pyoracle import ALL_DRAFT, COLLECT2, scale_for
+
+from .helpers import D, Matched, check_selection, rel_err_elem, rel_err_rows, to_dev_bf16
+
+pytestmark = pytest.mark.gpu
+SCALE = scale_for(D)
+
+
+def _lib():
+    from paper_2602_07223_b200 import Runner, SpecAttnError, selection_k
+    return Runner, SpecAttnError, selection_k
+
+
+# ----------------------------------------------------------------------------------- KV cache
+
+def test_cache_append_read_gather_truncate(cuda, ref):
+    torch = cuda
+    _, SpecAttnError, _ = _lib()
+    m = Matched(ref, L=2, Hkv=2, n_tokens=300, seed=11, max_context=400, page_size=64)
+    c, kv = m.cache, m.refs[0]
+    assert c.size() == kv.size() == 300
+    for layer in range(2):
+        for h in range(2):
+            K, V = c.read(layer, h, 0, 300)
+            Kr, Vr = kv.rows(layer, h, 0, 300)
+            assert np.array_equal(K.cpu().numpy(), Kr) and np.array_equal(V.cpu().numpy(), Vr)
+    idx = [0, 5, 63, 64, 65, 200, 299]
+    K, V = c.gather(1, 1, idx)
+    Kr, Vr = kv.gather(1, 1, idx)
+    assert np.array_equal(K.cpu().numpy(), Kr) and np.array_equal(V.cpu().numpy(), Vr)
+    # rollback semantics: truncate then append overwrites
+    c.set_committed(250)
+    kv.set_committed(250)
+    c.truncate(120)
+    kv.truncate(120)
+    assert c.committed() == kv.committed() == 120
+    newk = normal_bf16(12, 1, (1, 4, D))
+    newv = normal_bf16(12, 2, (1, 4, D))
+    c.append(torch.from_numpy(newk).cuda(), torch.from_numpy(newv).cuda())
+    kv.append(newk[0], newv[0])
+    K, _ = c.read(0, 1, 118, 3)
+    Kr, _ = kv.rows(0, 1, 118, 3)
+    assert np.array_equal(K.cpu().numpy(), Kr)
+    # error taxonomy
+    with pytest.raises(SpecAttnError) as e:
+        c.truncate(500)
+    assert e.value.status == "out_of_range"
+    with pytest.raises(SpecAttnError) as e:
+        c.gather(0, 0, [3, 2])
+    assert e.value.status == "out_of_range"
+    with pytest.raises(SpecAttnError) as e:
+        c.gather(0, 0, [121])
+    assert e.value.status == "out_of_range"
+    big = torch.zeros((400, 4, D), dtype=torch.float32, device="cuda")
+    with pytest.raises(SpecAttnError) as e:
+        c.append(big, big)
+    assert e.value.status == "length_error"
+    assert c.bytes_per_token() == (2 * 2 * 2 * D * 4, 2 * 2 * 2 * D * 2)
+    # fp32 input that is not bf16-representable rounds to nearest even (documented deviation)
+    x = torch.full((1, 4, D), 1.0 + 2.0 ** -10, dtype=torch.float32, device="cuda")
+    c.append(x, x)
+    K, _ = c.read(0, 0, c.size() - 1, 1)
+    assert float(K[0, 0]) == 1.0
+
+
+# ----------------------------------------------------------------------------------- verify
+
+VERIFY_CASES = [
+    # (Hkv, G, R, p0s, page)   — covers MT = 1..4, ragged / tiny / empty prefixes, batching
+    (8, 4, 5, [4096], 256),      # config 1 (G*R = 20 -> MT 2)
+    (2, 4, 7, [1000], 64),       # gamma 6 (config 3 shape), ragged p0
+    (2, 8, 5, [777], 128),       # 70B group (G = 8) -> MT 3
+    (1, 8, 7, [300], 64),        # G*R + 2 = 58 -> MT 4
+    (2, 1, 2, [130], 64),        # MT 1
+    (2, 4, 5, [0, 50, 2049], 64),  # empty prefix, < one tile, multi-sequence batch
+]
+
+
+def _run_verify(ref, Hkv, G, R, p0s, page, seed=31, collect_all=True):
+    import torch
+    Runner, _, _ = _lib()
+    Hq = Hkv * G
+    B = len(p0s)
+    m = Matched(ref, L=2, Hkv=Hkv, n_tokens=0, seed=seed, max_context=max(p0s) + R + 64, page_size=page,
+                n_seqs=B, lens=p0s)
+    r = Runner(m.cache, Hq, max_rows=R, max_prefix=max(p0s), max_batch=B)
+    r.set_batch(list(range(B)), p0s)
+    layer = 1
+    q = normal_bf16(seed, 10, (B, Hq, R, D))
+    kn = normal_bf16(seed, 11, (B, R, Hkv, D))
+    vn = normal_bf16(seed, 12, (B, R, Hkv, D))
+    out = torch.zeros((B, Hq, R, D), dtype=torch.float32, device="cuda")
+    ld = max(64, max(p0s))
+    logits = torch.full((B, Hq, R, ld), float("nan"), dtype=torch.float32, device="cuda")
+    mask = (1 | (1 << (R - 1)))
+    r.verify(layer, to_dev_bf16(q), out, to_dev_bf16(kn), to_dev_bf16(vn), SCALE, score_row_mask=mask,
+             logits=logits, collect_row_mask=(1 << R) - 1)
+    torch.cuda.synchronize()
+    sp, sld = r.scores(layer)
+    from paper_2602_07223_b200._lib import _device_bytes
+    scores = _device_bytes(sp, B * Hkv * sld * 4).view(torch.float32).reshape(B, Hkv, sld).cpu().numpy()
+    res = []
+    for b in range(B):
+        kv = m.refs[b]
+        # the reference appends the gamma+1 verify tokens for all layers
+        for t in range(R):
+            kk = normal_bf16(seed + 99, t, (2 * Hkv, D))
+            vv = normal_bf16(seed + 98, t, (2 * Hkv, D))
+            kk[Hkv:] = kn[b, t]
+            vv[Hkv:] = vn[b, t]
+            kv.append(kk, vv)
+        o_ref, l_ref = kv.verify_layer(layer, Hq, q[b], p0s[b], R, SCALE, threads=8)
+        res.append((o_ref, l_ref))
+    return m, r, q, kn, vn, out.cpu().numpy(), logits.cpu().numpy(), scores, res
+
+
+@pytest.mark.parametrize("Hkv,G,R,p0s,page", VERIFY_CASES)
+def test_verify_parity(cuda, ref, Hkv, G, R, p0s, page):
+    torch = cuda
+    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, p0s, page)
+    Hq = Hkv * G
+    for b, p0 in enumerate(p0s):
+        o_ref, l_ref = res[b]
+        assert rel_err_rows(out[b], o_ref) < 2e-4, rel_err_rows(out[b], o_ref)
+        assert rel_err_elem(out[b], o_ref) < 2e-3
+        if p0:
+            # logits byproduct: |d| <= 1e-5 * sum_j |q_j k_j|
+            Kh = m.K[b][:p0].reshape(p0, 2, Hkv, D)[:, 1]  # layer 1
+            g_of_h = np.arange(Hq) // G
+            bound = np.einsum("hrd,phd->hrp", np.abs(q[b]), np.abs(Kh[:, g_of_h]))
+            assert np.all(np.abs(logits[b][:, :, :p0] - l_ref) <= 1e-5 * bound + 1e-30)
+            # fused Collect-2 score byproduct == score_columns over rows {1, R} (per KV head sums)
+            rows = sorted({0, R - 1})
+            want = l_ref[:, rows, :].astype(np.float64).reshape(Hkv, G * len(rows), p0).sum(1)
+            tol = 1e-5 * np.einsum("hrd,phd->hp", np.abs(q[b][:, rows].sum(1, keepdims=True)) + 0,
+                                   np.abs(Kh[:, g_of_h])).reshape(Hkv, G, p0).sum(1) + 1e-4
+            assert np.all(np.abs(scores[b][:, :p0] - want) <= tol)
+        # fused append: window rows landed in the cache
+        K, V = m.cache.read(1, Hkv - 1, p0, R, seq=b) if m.cache.size(b) >= p0 + R else (None, None)
+        if K is None:
+            m.cache.set_size(p0 + R, seq=b)
+            K, V = m.cache.read(1, Hkv - 1, p0, R, seq=b)
+        assert np.array_equal(K.cpu().numpy(), kn[b, :, Hkv - 1]) and np.array_equal(V.cpu().numpy(), vn[b, :, Hkv - 1])
+    torch.cuda.synchronize()
+
+
+def test_verify_deterministic(cuda, ref):
+    a = _run_verify(ref, 2, 4, 5, [1500], 64, seed=41)
+    b = _run_verify(ref, 2, 4, 5, [1500], 64, seed=41)
+    assert np.array_equal(a[5], b[5]) and np.array_equal(a[7], b[7])
+
+
+# ----------------------------------------------------------------------------------- select
+
+def _gpu_select(r, slot, mode, n_sets, rows_in_score):
+    r.select(slot, mode=mode, rows_in_score=rows_in_score)
+    idx, cnt = r.selection(slot, n_sets)
+    return idx, cnt
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_select_parity(cuda, ref, mode):
+    Hkv, G, R, p0 = 8, 4, 5, 4096
+    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=51)
+    Runner, _, selection_k = _lib()
+    l_ref = res[0][1]  # [Hq][R][p0]
+    n_sets = 1 if mode == 0 else Hkv
+    idx, cnt = _gpu_select(r, 1, mode, n_sets, 2)
+    k = selection_k(r.sparse_ratio, p0, r.k_min)
+    exact = 0
+    for s in range(n_sets):
+        heads = range(Hkv * G) if mode == 0 else range(s * G, (s + 1) * G)
+        L = l_ref[list(heads)]
+        want = ref.select(COLLECT2, L, list(range(1, R + 1)), r.sparse_ratio, r.k_min)
+        ref_scores = ref.score_columns(L, list(range(1, R + 1)), [1, R])
+        got = idx[0, s, : cnt[0, s]]
+        assert cnt[0, s] == k == len(want)
+        check_selection(got, ref_scores, k)
+        exact += int(np.array_equal(got, want))
+    assert exact >= n_sets - 1  # random data: identical sets except at most a rare near-tie
+
+
+def test_select_exact_ties_lower_index(cuda, ref):
+    """Planted exact ties: duplicate key rows give identical scores; the lower index must win."""
+    import torch
+    Runner, _, selection_k = _lib()
+    from paper_2602_07223_b200 import Cache
+    Hkv, G, R, p0 = 2, 4, 3, 640
+    base = normal_bf16(61, 1, (8, 2 * Hkv, D))
+    K = base[np.arange(p0) % 8]  # every key repeats every 8 positions -> massive exact ties
+    V = normal_bf16(61, 2, (p0, 2 * Hkv, D))
+    cache = Cache(2, Hkv, D, p0 + 64, page_size=64)
+    cache.append(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    kv = ref.kv(2, Hkv, D, p0 + 64)
+    for t in range(p0):
+        kv.append(K[t], V[t])
+    r = Runner(cache, Hkv * G, max_rows=R, max_prefix=p0, sparse_ratio=0.1, k_min=16)
+    r.set_batch([0], [p0])
+    q = normal_bf16(61, 3, (1, Hkv * G, R, D))
+    kn, vn = normal_bf16(61, 4, (1, R, Hkv, D)), normal_bf16(61, 5, (1, R, Hkv, D))
+    out = torch.zeros((1, Hkv * G, R, D), dtype=torch.float32, device="cuda")
+    r.verify(0, to_dev_bf16(q), out, to_dev_bf16(kn), to_dev_bf16(vn), SCALE, score_row_mask=1 | (1 << (R - 1)))
+    for t in range(R):
+        kk, vv = np.zeros((2 * Hkv, D), np.float32), np.zeros((2 * Hkv, D), np.float32)
+        kk[:Hkv], vv[:Hkv] = kn[0, t], vn[0, t]
+        kv.append(kk, vv)
+    _, l_ref = kv.verify_layer(0, Hkv * G, q[0], p0, R, SCALE, threads=8)
+    idx, cnt = _gpu_select(r, 0, 0, 1, 2)
+    want = ref.select(COLLECT2, l_ref, list(range(1, R + 1)), 0.1, 16)
+    assert cnt[0, 0] == selection_k(0.1, p0, 16) == len(want)
+    assert np.array_equal(idx[0, 0, : cnt[0, 0]], want)
+
+
+# ----------------------------------------------------------------------------------- draft
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_draft_parity(cuda, ref, mode):
+    torch = cuda
+    Hkv, G, R, p0 = 8, 4, 5, 4096
+    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=71)
+    n_sets = 1 if mode == 0 else Hkv
+    idx, cnt = _gpu_select(r, 1, mode, n_sets, 2)
+    sets = [idx[0, s, : cnt[0, s]].astype(np.int64) for s in range(n_sets)]
+    kv = m.refs[0]
+    kv.truncate(p0)  # draft chain: provisional rows p0.. are re-appended step by step
+    m.cache.set_size(p0)
+    Hq = Hkv * G
+    for step in range(1, R):
+        qd = normal_bf16(72, step, (1, Hq, D))
+        kd, vd = normal_bf16(73, step, (1, Hkv, D)), normal_bf16(74, step, (1, Hkv, D))
+        o = torch.zeros((1, Hq, D), dtype=torch.float32, device="cuda")
+        r.draft(1, step, to_dev_bf16(qd), o, to_dev_bf16(kd), to_dev_bf16(vd), mode=mode, scale=SCALE)
+        kk, vv = np.zeros((2 * Hkv, D), np.float32), np.zeros((2 * Hkv, D), np.float32)
+        kk[Hkv:], vv[Hkv:] = kd[0], vd[0]
+        kv.append(kk, vv)
+        o_ref = kv.draft_layer(1, Hq, qd[0], sets, p0, step, SCALE, threads=8)
+        got = o.cpu().numpy()[0]
+        assert rel_err_rows(got, o_ref) < 2e-4, (step, rel_err_rows(got, o_ref))
+        assert rel_err_elem(got, o_ref) < 2e-3
+
+
+# ----------------------------------------------------------------------------------- iteration
+
+@pytest.mark.parametrize("strategy,mode,use_graph", [(COLLECT2, 0, True), (ALL_DRAFT, 1, False)])
+def test_iteration_parity(cuda, ref, strategy, mode, use_graph):
+    """One full speculation iteration (verify -> select -> gamma drafts, all layers) through
+    sa_iteration_run vs the reference composition (SURVEY.md §8d unit of work)."""
+    torch = cuda
+    Runner, _, selection_k = _lib()
+    L, Hkv, G, gamma, p0 = 3, 2, 4, 4, 1200
+    R, Hq = gamma + 1, Hkv * G
+    m = Matched(ref, L=L, Hkv=Hkv, n_tokens=p0, seed=81, max_context=p0 + 64, page_size=64)
+    r = Runner(m.cache, Hq, max_rows=R, max_prefix=p0, sparse_ratio=0.07, k_min=16)
+    r.set_batch([0], [p0])
+    qv = normal_bf16(82, 1, (L, 1, Hq, R, D))
+    kvn, vvn = normal_bf16(82, 2, (L, 1, R, Hkv, D)), normal_bf16(82, 3, (L, 1, R, Hkv, D))
+    qd = normal_bf16(82, 4, (gamma, L, 1, Hq, D))
+    kdn, vdn = normal_bf16(82, 5, (gamma, L, 1, Hkv, D)), normal_bf16(82, 6, (gamma, L, 1, Hkv, D))
+    out_v = torch.zeros((L, 1, Hq, R, D), dtype=torch.float32, device="cuda")
+    out_d = torch.zeros((gamma, L, 1, Hq, D), dtype=torch.float32, device="cuda")
+    dev = [to_dev_bf16(x) for x in (qv, kvn, vvn, qd, kdn, vdn)]
+    args = r.iteration_args(gamma, *dev, out_v, out_d, strategy=strategy, mode=mode, scale=SCALE,
+                            use_graph=use_graph)
+    assert r.iteration_kernel_count(args) == L * (2 + gamma)
+    for _ in range(2):  # second launch replays the graph
+        r.iteration(args)
+    torch.cuda.synchronize()
+    ov, od = out_v.cpu().numpy(), out_d.cpu().numpy()
+    kv = m.refs[0]
+    for t in range(R):
+        kv.append(kvn[:, 0, t].reshape(L * Hkv, D), vvn[:, 0, t].reshape(L * Hkv, D))
+    n_sets = 1 if mode == 0 else Hkv
+    rows = [1, R] if strategy == COLLECT2 else list(range(1, R + 1))
+    k = selection_k(0.07, p0, 16)
+    sets_by_layer = []
+    for layer in range(L):
+        o_ref, l_ref = kv.verify_layer(layer, Hq, qv[layer, 0], p0, R, SCALE, threads=8)
+        assert rel_err_rows(ov[layer, 0], o_ref) < 2e-4
+        idx, cnt = r.selection(layer, n_sets)
+        sets = []
+        for s in range(n_sets):
+            heads = list(range(Hq)) if mode == 0 else list(range(s * G, (s + 1) * G))
+            sc = ref.score_columns(l_ref[heads], list(range(1, R + 1)), rows)
+            got = idx[0, s, : cnt[0, s]]
+            check_selection(got, sc, k)
+            sets.append(got.astype(np.int64))
+        sets_by_layer.append(sets)
+    kv.truncate(p0)
+    for j in range(1, gamma + 1):
+        kv.append(kdn[j - 1, :, 0].reshape(L * Hkv, D), vdn[j - 1, :, 0].reshape(L * Hkv, D))
+        for layer in range(L):
+            o_ref = kv.draft_layer(layer, Hq, qd[j - 1, layer, 0], sets_by_layer[layer], p0, j, SCALE, threads=8)
+            assert rel_err_rows(od[j - 1, layer, 0], o_ref) < 2e-4, (j, layer)
