@@ -176,30 +176,67 @@ __device__ __forceinline__ void cta_partial_to_global(const float* wps, float* p
 
 // Last-arriving CTA of a (b, kv-head) unit merges the n_splits partials (split order fixed) and
 // writes normalised rows.  out_row(r) returns the f32 destination of output row r < rows_out.
-// Must be called by all `nthreads` participating threads; `bar_id` is a named barrier for them.
+// Latency-aware: (m, l) of every (split, row) are staged in shared memory in one pass, the per-row
+// merge weights w[s][r] = 2^(m_s - m*) / L are computed once, and each thread then streams float4
+// column groups with all split loads independent (unrolled) so the L2 round trips overlap.
+// `smem_w` must hold n_splits * rows_out * 2 floats.  Called by all `nthreads` threads.
 template <typename OutRow>
 __device__ __forceinline__ void combine_splits(const float* part_o_unit, const float* part_ml_unit, int n_splits,
-                                               int rows_pad, int rows_out, int* counter, int* smem_flag, int tid,
-                                               int nthreads, int bar_id, OutRow out_row) {
+                                               int rows_pad, int rows_out, int* counter, int* smem_flag,
+                                               float* smem_w, int tid, int nthreads, int bar_id, OutRow out_row) {
   __threadfence();
   named_bar_sync(bar_id, nthreads);
   if (tid == 0) *smem_flag = atomicAdd(counter, 1);
   named_bar_sync(bar_id, nthreads);
   if (*smem_flag != n_splits - 1) return;
   __threadfence();
-  for (int i = tid; i < rows_out * 128; i += nthreads) {
-    const int row = i >> 7, col = i & 127;
+  float2* ml = reinterpret_cast<float2*>(smem_w);  // [n_splits][rows_out] (m, l) -> (w, -)
+  for (int i = tid; i < n_splits * rows_out; i += nthreads) {
+    const int s = i / rows_out, row = i % rows_out;
+    ml[i] = __ldcg(reinterpret_cast<const float2*>(part_ml_unit) + s * rows_pad + row);
+  }
+  named_bar_sync(bar_id, nthreads);
+  for (int row = tid; row < rows_out; row += nthreads) {
     float mstar = -INFINITY;
-    for (int s = 0; s < n_splits; ++s) mstar = fmaxf(mstar, __ldcg(part_ml_unit + (s * rows_pad + row) * 2));
-    float acc = 0.f, lsum = 0.f;
+    for (int s = 0; s < n_splits; ++s) mstar = fmaxf(mstar, ml[s * rows_out + row].x);
+    float lsum = 0.f;
     for (int s = 0; s < n_splits; ++s) {
-      const float ms = __ldcg(part_ml_unit + (s * rows_pad + row) * 2);
-      if (ms == -INFINITY) continue;
-      const float f = fast_exp2(ms - mstar);
-      acc += __ldcg(part_o_unit + (s * rows_pad + row) * 128 + col) * f;
-      lsum += __ldcg(part_ml_unit + (s * rows_pad + row) * 2 + 1) * f;
+      const float2 v = ml[s * rows_out + row];
+      const float f = v.x == -INFINITY ? 0.f : fast_exp2(v.x - mstar);
+      ml[s * rows_out + row].x = f;
+      lsum += v.y * f;
     }
-    out_row(row)[col] = acc / lsum;
+    const float inv = 1.f / lsum;
+    for (int s = 0; s < n_splits; ++s) ml[s * rows_out + row].x *= inv;
+  }
+  named_bar_sync(bar_id, nthreads);
+  for (int i = tid; i < rows_out * 32; i += nthreads) {
+    const int row = i >> 5, c4 = i & 31;
+    const float4* src = reinterpret_cast<const float4*>(part_o_unit) + row * 32 + c4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int s = 0;
+    for (; s + 4 <= n_splits; s += 4) {
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + (s + u) * rows_pad * 32);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float w = ml[(s + u) * rows_out + row].x;
+        acc.x += v[u].x * w;
+        acc.y += v[u].y * w;
+        acc.z += v[u].z * w;
+        acc.w += v[u].w * w;
+      }
+    }
+    for (; s < n_splits; ++s) {
+      const float4 v = __ldcg(src + s * rows_pad * 32);
+      const float w = ml[s * rows_out + row].x;
+      acc.x += v.x * w;
+      acc.y += v.y * w;
+      acc.z += v.z * w;
+      acc.w += v.w * w;
+    }
+    reinterpret_cast<float4*>(out_row(row))[c4] = acc;
   }
   if (tid == 0) *counter = 0;  // re-arm for the next launch (stream/graph ordered)
 }

@@ -150,7 +150,7 @@ SA_API sa_status sa_cache_create(const sa_cache_config* cfg, sa_cache** out) {
   if (cfg->n_layers < 1 || cfg->n_kv_heads < 1 || cfg->max_context < 1 || cfg->max_seqs < 1)
     return fail(SA_INVALID_ARGUMENT, "ModelConfig: n_layers, n_kv_heads, max_context, max_seqs must be >= 1");
   const int64_t P = cfg->page_size ? cfg->page_size : 256;
-  if (P < 64 || (P & (P - 1))) return fail(SA_INVALID_ARGUMENT, "page_size must be a power of two >= 64");
+  if (P < 128 || (P & (P - 1))) return fail(SA_INVALID_ARGUMENT, "page_size must be a power of two >= 128");
   auto* c = new sa_cache();
   c->n_layers = cfg->n_layers;
   c->n_kv_heads = cfg->n_kv_heads;
@@ -187,7 +187,9 @@ SA_API sa_status sa_cache_create(const sa_cache_config* cfg, sa_cache** out) {
   for (int64_t i = 0; i < c->num_pages; ++i) c->free_pages[i] = static_cast<int32_t>(c->num_pages - 1 - i);
   std::string err;
   if (!sa::encode_tensor_map(&c->tmap_k, c->k_pool, rows, 64, &err) ||
-      !sa::encode_tensor_map(&c->tmap_v, c->v_pool, rows, 64, &err)) {
+      !sa::encode_tensor_map(&c->tmap_v, c->v_pool, rows, 64, &err) ||
+      !sa::encode_tensor_map(&c->tmap_k128, c->k_pool, rows, 128, &err) ||
+      !sa::encode_tensor_map(&c->tmap_v128, c->v_pool, rows, 128, &err)) {
     sa_cache_destroy(c);
     return fail(SA_CUDA_ERROR, err);
   }

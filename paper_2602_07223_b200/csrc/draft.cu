@@ -25,7 +25,8 @@ struct DCfg {
   static constexpr int kQHalf = 16 * 128;
   static constexpr int kOffMisc = kOffQ + 2 * kQHalf;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
-  static_assert(4 * kWpFloats * 4 <= kOffQ, "epilogue partials must fit");
+  static constexpr int kMaxSplits = 192;
+  static_assert(4 * kWpFloats * 4 <= kOffQ && kMaxSplits * 16 * 8 <= kOffQ, "epilogue scratch must fit");
 };
 
 __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams p) {
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
   cta_partial_to_global<1, 4>(wps, po + static_cast<size_t>(split) * 16 * 128,
                               pml + static_cast<size_t>(split) * 16 * 2, tid, DCfg::kThreads);
   float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128;
-  combine_splits(po, pml, p.n_splits, 16, p.G, p.counters + unit, misc, tid, DCfg::kThreads, 1,
+  combine_splits(po, pml, p.n_splits, 16, p.G, p.counters + unit, misc, wps, tid, DCfg::kThreads, 1,
                  [&](int row) { return out_unit + static_cast<size_t>(row) * 128; });
 }
 

@@ -35,6 +35,7 @@ struct sa_cache {
   std::vector<int64_t> len, committed, pages_of_seq;
   std::vector<int32_t> free_pages;           // LIFO free list
   CUtensorMap tmap_k{}, tmap_v{};            // 2-D [rows][128] bf16, box {64, 64}, SWIZZLE_128B
+  CUtensorMap tmap_k128{}, tmap_v128{};      // same tensors, box {64, 128} (tcgen05 verify tiles)
   int device = 0;
 
   sa::CacheView view() const {
@@ -114,6 +115,7 @@ struct SelectParams {
 };
 
 cudaError_t launch_verify(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
+cudaError_t launch_verify_tc(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 size_t verify_smem_bytes(int MT);

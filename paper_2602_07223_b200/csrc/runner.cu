@@ -6,7 +6,9 @@
 // dependent draft steps over all layers.  The whole launch sequence is captured once into a CUDA
 // graph and replayed.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -37,6 +39,7 @@ struct sa_runner {
   int *v_cnt = nullptr, *d_cnt = nullptr;
   // streams / graph
   cudaStream_t side = nullptr;
+  cudaStream_t capture = nullptr;  // graphs are captured here (the caller's stream may be legacy)
   std::vector<cudaEvent_t> ev_v, ev_s;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaGraphExec_t gexec = nullptr;
@@ -50,11 +53,11 @@ int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 // Pick the split count for `units` independent (sequence, KV head) units of `len` keys: minimise
 // (waves x per-CTA keys) + a per-split merge cost, chunks a multiple of `gran`.
 int choose_splits(int64_t units, int64_t len, int64_t gran, int64_t max_chunk, int64_t slots_per_wave,
-                  int64_t max_ctas, int* chunk_out) {
+                  int64_t max_ctas, int64_t max_splits, int* chunk_out) {
   len = std::max<int64_t>(len, 1);
   int best_n = 1;
   int64_t best_chunk = round_up(len, gran), best_cost = -1;
-  for (int64_t n = 1; n <= 256; ++n) {
+  for (int64_t n = 1; n <= max_splits; ++n) {
     int64_t chunk = round_up((len + n - 1) / n, gran);
     if (max_chunk && chunk > max_chunk) continue;
     const int64_t nn = (len + chunk - 1) / chunk;
@@ -124,6 +127,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
   alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->capture, cudaStreamNonBlocking);
   r->ev_v.resize(S);
   r->ev_s.resize(S);
   for (int64_t i = 0; i < S && e == cudaSuccess; ++i) {
@@ -148,6 +152,7 @@ SA_API sa_status sa_runner_destroy(sa_runner* r) {
   if (r->ev_fork) cudaEventDestroy(r->ev_fork);
   if (r->ev_join) cudaEventDestroy(r->ev_join);
   if (r->side) cudaStreamDestroy(r->side);
+  if (r->capture) cudaStreamDestroy(r->capture);
   for (void* p : {static_cast<void*>(r->d_seq), static_cast<void*>(r->d_p0), static_cast<void*>(r->scores),
                   static_cast<void*>(r->idx), static_cast<void*>(r->kcnt), static_cast<void*>(r->keys),
                   static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_cnt),
@@ -236,12 +241,24 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   p.collect_mask = a->collect_row_mask;
   p.n_collect = __builtin_popcount(a->collect_row_mask);
   const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
-  p.n_splits = choose_splits(units, r->p_max, 64, 0, r->num_sms * sa::verify_max_ctas_per_sm(p.MT),
-                             r->v_units_cap, &p.chunk);
-  p.part_o = r->v_po;
-  p.part_ml = r->v_pml;
-  p.counters = r->v_cnt;
-  cudaError_t e = sa::launch_verify(p, r->cache->tmap_k, r->cache->tmap_v, s);
+  static const bool use_mma_sync = [] {
+    const char* v = getenv("SA_VERIFY_IMPL");
+    return v && std::string(v) == "mma";
+  }();
+  cudaError_t e;
+  if (use_mma_sync) {
+    p.n_splits = choose_splits(units, r->p_max, 64, 0, r->num_sms, r->v_units_cap, 128, &p.chunk);
+    p.part_o = r->v_po;
+    p.part_ml = r->v_pml;
+    p.counters = r->v_cnt;
+    e = sa::launch_verify(p, r->cache->tmap_k, r->cache->tmap_v, s);
+  } else {
+    p.n_splits = choose_splits(units, r->p_max, 128, 0, r->num_sms, r->v_units_cap, 128, &p.chunk);
+    p.part_o = r->v_po;
+    p.part_ml = r->v_pml;
+    p.counters = r->v_cnt;
+    e = sa::launch_verify_tc(p, r->cache->tmap_k128, r->cache->tmap_v128, s);
+  }
   if (e != cudaSuccess) return sa::cuda_fail(e, "verify launch");
   return SA_OK;
 }
@@ -302,7 +319,7 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.scale_log2 = a->scale * sa::kLog2e;
   p.out = a->out;
   const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
-  p.n_splits = choose_splits(units, r->k_cap + a->step, 64, 128, 3 * r->num_sms, r->d_units_cap, &p.chunk);
+  p.n_splits = choose_splits(units, r->k_cap + a->step, 64, 128, 3 * r->num_sms, r->d_units_cap, 192, &p.chunk);
   p.part_o = r->d_po;
   p.part_ml = r->d_pml;
   p.counters = r->d_cnt;
@@ -410,9 +427,9 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
       r->gexec = nullptr;
     }
     cudaGraph_t graph = nullptr;
-    SA_CUDA_CHECK(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
-    sa_status st = enqueue_iteration(r, a, main);
-    cudaError_t e = cudaStreamEndCapture(main, &graph);
+    SA_CUDA_CHECK(cudaStreamBeginCapture(r->capture, cudaStreamCaptureModeThreadLocal));
+    sa_status st = enqueue_iteration(r, a, r->capture);
+    cudaError_t e = cudaStreamEndCapture(r->capture, &graph);
     if (st != SA_OK) {
       if (graph) cudaGraphDestroy(graph);
       return st;

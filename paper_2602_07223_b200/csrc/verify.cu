@@ -40,7 +40,8 @@ struct VCfg {
   static constexpr int kOffBar = kOffQ + 2 * kQHalf;
   static constexpr int kOffMisc = kOffBar + 2 * kStages * 8;
   static constexpr int kSmem = kOffMisc + 64 + 1024;
-  static_assert(kNCW * kWpFloats * 4 <= kOffWinK, "epilogue partials must fit in the stage ring");
+  static constexpr int kMaxSplits = 128;
+  static_assert(kNCW * kWpFloats * 4 <= kOffWinK && kMaxSplits * 64 * 8 <= kOffWinK, "epilogue scratch must fit");
 };
 
 template <int MT, int TG>
@@ -255,8 +256,8 @@ __global__ void __launch_bounds__(VCfg<MT, TG>::kThreads, 1)
   cta_partial_to_global<MT, TG>(wps, po + static_cast<size_t>(split) * rows_pad * 128,
                                 pml + static_cast<size_t>(split) * rows_pad * 2, tid, nct);
   float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
-  combine_splits(po, pml, p.n_splits, rows_pad, M, p.counters + unit, misc, tid, nct, 1,
-                 [&](int row) { return out_unit + static_cast<size_t>(row) * 128; });
+  combine_splits(po, pml, p.n_splits, rows_pad, M, p.counters + unit, misc, wps, tid, nct,
+                 1, [&](int row) { return out_unit + static_cast<size_t>(row) * 128; });
 }
 
 size_t verify_smem_bytes(int MT) {
