@@ -2,39 +2,165 @@
 //
 // Reference: KvStore::gather (kv_store.cpp:67-88) followed by attend (attention.cpp:70-76) over
 // [K_T ; K_tail], the SPEC draft-forward key set T ∪ {positions >= draft window start}
-// (SPEC.md:385,447).  The reference materialises the gathered K/V copies; here each CTA
-// gathers its slice of the virtual key list straight into shared memory with 16-byte cp.async
-// (warp-coalesced: 16 lanes per 256-byte row) in the same swizzled layout the TMA path produces,
-// then runs the shared mma.sync flash step for the G q-heads of the KV head (one 16-row tile).
+// (SPEC.md:385,447).  The reference materialises the gathered K/V copies; here each CTA gathers
+// its slice of the virtual key list T[0..k) ++ [p0, p0+step) straight into shared memory with
+// 16-byte cp.async (16 lanes per 256-byte row, coalesced) in the swizzled layout the mma.sync
+// flash step of attn_core.cuh reads, for the G q-heads of its KV head (one 16-row tile).
 //
-// Grid (n_splits, Hkv, B): split s covers virtual keys [s*chunk, (s+1)*chunk) of
-// T[0..k) ++ [p0, p0+step); the last-arriving CTA merges the splits.
+// Grid (CS, Hkv, B) launched as clusters of CS CTAs: the CS splits of one (sequence, KV head)
+// merge their partial (max, sum, O) through distributed shared memory — no global round trip.
+//
+// Programmatic dependent launch: the selected prefix rows (T from the select kernel, positions
+// < p0, never written during the draft phase) are gathered BEFORE griddepcontrol.wait, overlapping
+// the previous layer's kernel; the query, the tail rows and this step's new row (which a real model
+// produces in the previous layer) are read after it.
 #include "attn_core.cuh"
 #include "internal.h"
 
 namespace sa {
 
+// Swap-AB mma.sync flash step for <= 8 query rows (the G q-heads of one KV head):
+//   S^T(16 tok x 8 rows) = K(16x128) Q^T            8 x mma.m16n8k16 per 16 tokens
+//   O^T(128 d x 8 rows) += V^T(128 x 16 tok) P^T      8 d-blocks x (hi, lo) = 16 mma per 16 tokens
+// Thread (gid = lane/4, t4 = lane%4) holds S^T for tokens gid / gid+8 and query rows 2*t4, 2*t4+1;
+// P^T is re-laid out as the B operand with movmatrix (8x8 transpose), so no shared-memory trip.
+struct DraftWarp {
+  float o[8][4];     // O^T accumulators: d-block jj rows gid / gid+8, query rows 2t4 / 2t4+1
+  float m[2], l[2];  // running max (scaled log2) and per-thread partial sums of rows 2t4, 2t4+1
+  uint32_t qb[8][2];  // Q^T B-fragments per k16 step of d
+
+  __device__ __forceinline__ void init(const __nv_bfloat16* q_rows, int G, int lane) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    m[0] = m[1] = -INFINITY;
+    l[0] = l[1] = 0.f;
+    const int gid = lane >> 2, t4 = lane & 3;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t b0 = 0, b1 = 0;
+      if (gid < G) {
+        b0 = __ldg(reinterpret_cast<const uint32_t*>(q_rows + gid * 128 + kk * 16 + 2 * t4));
+        b1 = __ldg(reinterpret_cast<const uint32_t*>(q_rows + gid * 128 + kk * 16 + 8 + 2 * t4));
+      }
+      qb[kk][0] = b0;
+      qb[kk][1] = b1;
+    }
+  }
+
+  // tokens [r0, r0+16) of the swizzled K/V tiles; valid(i) masks token i of the sub-block
+  __device__ __forceinline__ void step(uint32_t k_smem, uint32_t v_smem, uint32_t half, int r0, int lane,
+                                       float c, int n_valid) {
+    const int gid = lane >> 2, t4 = lane & 3, mi = lane >> 3;
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      const int tok = r0 + (mi & 1) * 8 + (lane & 7);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        uint32_t a[4];
+        ldsm_x4(k_smem + swz(tok, 2 * kk + (mi >> 1), half), a[0], a[1], a[2], a[3]);
+        mma_bf16(s, a, qb[kk][0], qb[kk][1]);
+      }
+    }
+    if (gid >= n_valid) s[0] = s[1] = -INFINITY;
+    if (gid + 8 >= n_valid) s[2] = s[3] = -INFINITY;
+    // per query row (2t4 + e): max over the 16 tokens (2 in-thread, 8 gid lanes)
+    float tmax[2] = {fmaxf(s[0], s[2]), fmaxf(s[1], s[3])};
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) tmax[e] = fmaxf(tmax[e], __shfl_xor_sync(0xffffffffu, tmax[e], off));
+    float mnew[2];
+    bool grow = false;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      mnew[e] = fmaxf(m[e], tmax[e] * c);
+      grow |= mnew[e] > m[e];
+    }
+    if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float f = (mnew[e] == -INFINITY || m[e] == mnew[e]) ? 1.f : fast_exp2(m[e] - mnew[e]);
+        l[e] *= f;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          o[jj][e] *= f;
+          o[jj][2 + e] *= f;
+        }
+        m[e] = mnew[e];
+      }
+    }
+    const float b0 = m[0] == -INFINITY ? 0.f : m[0], b1 = m[1] == -INFINITY ? 0.f : m[1];
+    const float p0 = fast_exp2(fmaf(s[0], c, -b0)), p1 = fast_exp2(fmaf(s[1], c, -b1));
+    const float p2 = fast_exp2(fmaf(s[2], c, -b0)), p3 = fast_exp2(fmaf(s[3], c, -b1));
+    l[0] += p0 + p2;
+    l[1] += p1 + p3;
+    uint32_t h01, l01, h23, l23;
+    split_bf16(p0, p1, h01, l01);  // token gid,   rows 2t4, 2t4+1
+    split_bf16(p2, p3, h23, l23);  // token gid+8
+    // B fragments of P^T (k = tokens, n = rows): 8x8 transposes of the two token halves
+    const uint32_t bh0 = movmatrix_trans(h01), bh1 = movmatrix_trans(h23);
+    const uint32_t bl0 = movmatrix_trans(l01), bl1 = movmatrix_trans(l23);
+    const int tok = r0 + (mi >> 1) * 8 + (lane & 7);
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      uint32_t a[4];
+      ldsm_x4_t(v_smem + swz(tok, 2 * jj + (mi & 1), half), a[0], a[1], a[2], a[3]);
+      mma_bf16(o[jj], a, bh0, bh1);
+    }
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      uint32_t a[4];
+      ldsm_x4_t(v_smem + swz(tok, 2 * jj + (mi & 1), half), a[0], a[1], a[2], a[3]);
+      mma_bf16(o[jj], a, bl0, bl1);
+    }
+  }
+
+  __device__ __forceinline__ void finalize_l() {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) l[e] += __shfl_xor_sync(0xffffffffu, l[e], off);
+  }
+};
+
 struct DCfg {
   static constexpr int kTile = 64;
-  static constexpr int kMaxTiles = 2;  // chunk <= 128 keys per CTA
-  static constexpr int kThreads = 128;
+  static constexpr int kMaxTiles = 3;   // resident tiles per round (192 keys)
+  static constexpr int kThreads = 256;
+  static constexpr int kWarps = kThreads / 32;
+  static constexpr int kMaxCS = 16;
   static constexpr int kHalf = kTile * 128;
   static constexpr int kTileBytes = 2 * kHalf;
   static constexpr int kOffV = kMaxTiles * kTileBytes;
   static constexpr int kOffQ = 2 * kMaxTiles * kTileBytes;
   static constexpr int kQHalf = 16 * 128;
-  static constexpr int kOffMisc = kOffQ + 2 * kQHalf;
-  static constexpr int kSmem = kOffMisc + 64 + 1024;
-  static constexpr int kMaxSplits = 192;
-  static_assert(4 * kWpFloats * 4 <= kOffQ && kMaxSplits * 16 * 8 <= kOffQ, "epilogue scratch must fit");
+  static constexpr int kOffPart = kOffQ + 2 * kQHalf;  // CTA partial: O[16][128], m[16], l[16]
+  static constexpr int kPartFloats = 8 * 128 + 16;  // CTA partial: O[8 rows][128], m[8], l[8]
+  static constexpr int kOffRow = kOffPart + kPartFloats * 4;  // int64 source rows of the round
+  static constexpr int kOffW = kOffRow + kMaxTiles * kTile * 8;  // merge weights [kMaxCS][16]
+  static constexpr int kSmem = kOffW + kMaxCS * 16 * 4 * 2 + 1024;
+  static constexpr int kWarpPart = 8 * 128 + 16;     // per-warp partial, same layout
+  static_assert(kWarps * kWarpPart * 4 <= kOffQ, "warp partials must fit in the tile buffers");
 };
+
+__device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
+  if (p.trace && threadIdx.x == 0) {
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (cta < 512) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.trace[cta * 8 + phase] = gt;
+    }
+  }
+}
 
 __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
-  int* misc = reinterpret_cast<int*>(smem + DCfg::kOffMisc);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* part = reinterpret_cast<float*>(smem + DCfg::kOffPart);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int CS = gridDim.x;
   const int seq = p.seq_ids[b];
   const int p0 = p.p0[b];
   const int j = p.step;
@@ -45,97 +171,223 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
   const int v_begin = split * p.chunk;
   const int v_end = min(m_total, v_begin + p.chunk);
   const int n = max(0, v_end - v_begin);
-  const int n_tiles = ceil_div(n, DCfg::kTile);
   const int Hq = p.Hkv * p.G;
   const int new_pos = p0 + j - 1;
+  dtrace(p, 0);
 
-  // Gather K/V rows of the virtual key list into swizzled smem tiles (zero-fill past the end).
-  for (int i = tid; i < n_tiles * DCfg::kTile * 16; i += DCfg::kThreads) {
-    const int r = i >> 4, ch = i & 15, tile = r >> 6, rr = r & 63;
-    const uint32_t off = tile * DCfg::kTileBytes + swz(rr, ch, DCfg::kHalf);
-    const int v = v_begin + r;
-    const __nv_bfloat16 *sk = p.cache.k, *sv = p.cache.v;
-    int bytes = 0;
-    if (v < v_end) {
-      const int pos = v < k ? __ldg(T + v) : p0 + (v - k);
-      if (p.k_new && pos == new_pos) {
+  // Gather rows [v_begin + r0, v_begin + r0 + rows) of the virtual key list into the tile buffers.
+  // Step 1 resolves every row's source (index load + block-table load, all independent across
+  // threads) into shared memory; step 2 issues the 16-byte cp.async copies without any dependent
+  // global load in the loop.  prefix_only: rows at positions < p0 (selected by T) — independent
+  // of the previous kernel; otherwise the tail rows, the new row and zero fill.
+  int64_t* src_row = reinterpret_cast<int64_t*>(smem + DCfg::kOffRow);  // -1: k_new row, -2: zero fill
+  auto resolve = [&](int r0, int rows, bool prefix_only) {
+    for (int r = tid; r < rows; r += DCfg::kThreads) {
+      const int v = v_begin + r0 + r;
+      if (v >= v_end) {
+        if (!prefix_only) src_row[r] = -2;
+        continue;
+      }
+      const bool is_tail = v >= k;
+      if (is_tail == prefix_only) continue;
+      const int pos = is_tail ? p0 + (v - k) : __ldg(T + v);
+      src_row[r] = (p.k_new && pos == new_pos) ? -1 : cache_row(p.cache, seq, p.layer, g, pos);
+    }
+  };
+  auto gather = [&](int r0, int rows, bool prefix_only) {
+    for (int i = tid; i < rows * 16; i += DCfg::kThreads) {
+      const int r = i >> 4, ch = i & 15;
+      const int v = v_begin + r0 + r;
+      const bool in = v < v_end;
+      if (in && ((v >= k) == prefix_only)) continue;
+      if (!in && prefix_only) continue;
+      const int tile = r >> 6, rr = r & 63;
+      const uint32_t off = tile * DCfg::kTileBytes + swz(rr, ch, DCfg::kHalf);
+      const int64_t row = src_row[r];
+      const __nv_bfloat16 *sk = p.cache.k, *sv = p.cache.v;
+      int bytes = 16;
+      if (row >= 0) {
+        sk += row * 128 + ch * 8;
+        sv += row * 128 + ch * 8;
+      } else if (row == -1) {
         sk = p.k_new + (static_cast<size_t>(b) * p.Hkv + g) * 128 + ch * 8;
         sv = p.v_new + (static_cast<size_t>(b) * p.Hkv + g) * 128 + ch * 8;
       } else {
-        const int64_t row = cache_row(p.cache, seq, p.layer, g, pos);
-        sk = p.cache.k + row * 128 + ch * 8;
-        sv = p.cache.v + row * 128 + ch * 8;
+        bytes = 0;  // zero-fill (keeps 0 * V finite)
       }
-      bytes = 16;
+      cp_async_16(smem + off, sk, bytes);
+      cp_async_16(smem + DCfg::kOffV + off, sv, bytes);
     }
-    cp_async_16(smem + off, sk, bytes);
-    cp_async_16(smem + DCfg::kOffV + off, sv, bytes);
-  }
-  cp_async_commit();
-  // Q rows of the G heads (one 16-row tile, zero-padded).
-  uint8_t* sq = smem + DCfg::kOffQ;
-  const __nv_bfloat16* qb = p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128;
-  for (int i = tid; i < 16 * 16; i += DCfg::kThreads) {
-    const int row = i >> 4, ch = i & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < p.G) v = __ldg(reinterpret_cast<const uint4*>(qb + row * 128 + ch * 8));
-    *reinterpret_cast<uint4*>(sq + swz(row, ch, DCfg::kQHalf)) = v;
-  }
-  // Fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45).
-  if (split == 0 && p.k_new && tid < 32) {
-    const int which = tid >> 4, ch = tid & 15;
-    const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128;
-    const int64_t row = cache_row(p.cache, seq, p.layer, g, new_pos);
-    __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + row * 128;
-    reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
-  }
-  cp_async_wait_all();
-  __syncthreads();
+  };
 
-  WarpAttn w;
-  w.init();
-  w.load_q(smem_u32(sq), DCfg::kQHalf, 0, lane);
-  const int t4 = lane & 3;
-  for (int t = 0; t < n_tiles; ++t) {
-    const uint32_t kt = smem_u32(smem + t * DCfg::kTileBytes);
-    const uint32_t vt = smem_u32(smem + DCfg::kOffV + t * DCfg::kTileBytes);
-    const int r0 = warp * 16;
-    if (t * DCfg::kTile + r0 >= n) break;
-    float s[2][4];
-    w.qk(kt, DCfg::kHalf, r0, lane, s);
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (t * DCfg::kTile + r0 + 8 * nt + 2 * t4 + (e & 1) >= n) s[nt][e] = -INFINITY;
-    w.softmax_pv(s, vt, DCfg::kHalf, r0, lane, p.scale_log2);
+  // selected prefix rows of round 0: independent of the previous kernel -> before the PDL wait
+  {
+    const int rows0 = (min(DCfg::kMaxTiles * DCfg::kTile, n) + 15) & ~15;
+    resolve(0, rows0, true);
+    __syncthreads();
+    gather(0, rows0, true);
+    cp_async_commit();
+  }
+  pdl_wait();  // previous layer complete: q, k_new and the tail rows are now valid
+  pdl_launch_dependents();
+  dtrace(p, 1);
+  DraftWarp w;
+  w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);  // (after the wait)
+  constexpr int kRoundRows = DCfg::kMaxTiles * DCfg::kTile;
+  for (int r0 = 0, round = 0; r0 < max(n, 1); r0 += kRoundRows, ++round) {
+    const int rows = min(kRoundRows, n - r0);
+    const int rows_pad = (rows + 15) & ~15;
+    if (round == 0) {
+      // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45)
+      if (split == 0 && p.k_new && tid < 32) {
+        const int which = tid >> 4, ch = tid & 15;
+        const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128;
+        const int64_t row = cache_row(p.cache, seq, p.layer, g, new_pos);
+        __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + row * 128;
+        reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
+      }
+      resolve(r0, rows_pad, false);  // tail rows, new row, zero fill
+      __syncthreads();
+      gather(r0, rows_pad, false);
+    } else {
+      __syncthreads();  // previous round's tiles fully consumed
+      resolve(r0, rows_pad, true);
+      resolve(r0, rows_pad, false);
+      __syncthreads();
+      gather(r0, rows_pad, true);
+      gather(r0, rows_pad, false);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    dtrace(p, 2);
+    const int n_sub = rows_pad >> 4;
+    for (int sb = warp; sb < n_sub; sb += DCfg::kWarps) {
+      const int tile = sb >> 2, r_in = (sb & 3) * 16;
+      w.step(smem_u32(smem + tile * DCfg::kTileBytes), smem_u32(smem + DCfg::kOffV + tile * DCfg::kTileBytes),
+             DCfg::kHalf, r_in, lane, p.scale_log2, min(16, n - (r0 + sb * 16)));
+    }
   }
   w.finalize_l();
+  dtrace(p, 3);
 
+  // in-CTA merge of the warps' partials (only the G real query rows) -> part (smem)
   __syncthreads();
   float* wps = reinterpret_cast<float*>(smem);
-  store_warp_partial(w, wps + warp * kWpFloats, lane);
+  {
+    float* wp = wps + warp * DCfg::kWarpPart;
+    const int gid = lane >> 2, t4 = lane & 3;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int row = 2 * t4 + e;
+      if (row < p.G) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          wp[row * 128 + 16 * jj + gid] = w.o[jj][e];
+          wp[row * 128 + 16 * jj + gid + 8] = w.o[jj][2 + e];
+        }
+        if (gid == 0) {
+          wp[1024 + row] = w.m[e];
+          wp[1024 + 8 + row] = w.l[e];
+        }
+      }
+    }
+  }
   __syncthreads();
-  const int unit = b * p.Hkv + g;
-  float* po = p.part_o + static_cast<size_t>(unit) * p.n_splits * 16 * 128;
-  float* pml = p.part_ml + static_cast<size_t>(unit) * p.n_splits * 16 * 2;
-  cta_partial_to_global<1, 4>(wps, po + static_cast<size_t>(split) * 16 * 128,
-                              pml + static_cast<size_t>(split) * 16 * 2, tid, DCfg::kThreads);
+  for (int i = tid; i < p.G * 128; i += DCfg::kThreads) {
+    const int row = i >> 7, col = i & 127;
+    float mstar = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < DCfg::kWarps; ++q) mstar = fmaxf(mstar, wps[q * DCfg::kWarpPart + 1024 + row]);
+    float acc = 0.f, lsum = 0.f;
+    if (mstar != -INFINITY) {
+#pragma unroll
+      for (int q = 0; q < DCfg::kWarps; ++q) {
+        const float* wp = wps + q * DCfg::kWarpPart;
+        const float mq = wp[1024 + row];
+        if (mq == -INFINITY) continue;
+        const float f = fast_exp2(mq - mstar);
+        acc += wp[row * 128 + col] * f;
+        lsum += wp[1024 + 8 + row] * f;
+      }
+    }
+    part[row * 128 + col] = acc;
+    if (col == 0) {
+      part[1024 + row] = mstar;
+      part[1024 + 8 + row] = lsum;
+    }
+  }
+  // cluster-wide merge over DSMEM: CTA `split` finalises a slice of the G x 128 outputs
+  cluster_sync_all();
+  const uint32_t part_addr = smem_u32(part);
+  const int n_out = p.G * 128;
+  const int per = (n_out + CS - 1) / CS;
   float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128;
-  combine_splits(po, pml, p.n_splits, 16, p.G, p.counters + unit, misc, wps, tid, DCfg::kThreads, 1,
-                 [&](int row) { return out_unit + static_cast<size_t>(row) * 128; });
+  float* wts = reinterpret_cast<float*>(smem + DCfg::kOffW);  // [s][16]: (m) then weight
+  float* lss = wts + DCfg::kMaxCS * 16;                      // [s][16]: l
+  if (tid < CS * p.G) {  // (m, l) of every (split, row) in one batch of remote loads
+    const int s2 = tid / p.G, row = tid % p.G;
+    const uint32_t base = mapa_shared(part_addr, s2);
+    wts[s2 * 16 + row] = ld_dsmem_f32(base + (1024 + row) * 4);
+    lss[s2 * 16 + row] = ld_dsmem_f32(base + (1024 + 8 + row) * 4);
+  }
+  __syncthreads();
+  if (tid < p.G) {  // merge weights w_s = 2^(m_s - m*) / L
+    float mstar = -INFINITY;
+    for (int s2 = 0; s2 < CS; ++s2) mstar = fmaxf(mstar, wts[s2 * 16 + tid]);
+    float lsum = 0.f;
+    for (int s2 = 0; s2 < CS; ++s2) {
+      const float ms = wts[s2 * 16 + tid];
+      const float f = ms == -INFINITY ? 0.f : fast_exp2(ms - mstar);
+      wts[s2 * 16 + tid] = f;
+      lsum += lss[s2 * 16 + tid] * f;
+    }
+    const float inv = 1.f / lsum;
+    for (int s2 = 0; s2 < CS; ++s2) wts[s2 * 16 + tid] *= inv;
+  }
+  __syncthreads();
+  for (int e = split * per + tid; e < min(n_out, (split + 1) * per); e += DCfg::kThreads) {
+    const int row = e >> 7, col = e & 127;
+    float os[DCfg::kMaxCS];
+#pragma unroll
+    for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2)
+      os[s2] = s2 < CS ? ld_dsmem_f32(mapa_shared(part_addr, s2) + (row * 128 + col) * 4) : 0.f;
+    float acc = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2)
+      if (s2 < CS) acc += os[s2] * wts[s2 * 16 + row];
+    out_unit[row * 128 + col] = acc;
+  }
+  cluster_sync_all();  // keep every CTA's partial alive until all remote reads are done
+  dtrace(p, 4);
 }
 
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg::kSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(p.n_splits, p.Hkv, p.B);
-  draft_kernel<<<grid, DCfg::kThreads, DCfg::kSmem, s>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);
+  cfg.blockDim = dim3(DCfg::kThreads);
+  cfg.dynamicSmemBytes = DCfg::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = p.n_splits;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = p.use_pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, draft_kernel, p);
 }
+
+int draft_max_splits() { return DCfg::kMaxCS; }
+int draft_round_rows() { return DCfg::kMaxTiles * DCfg::kTile; }
 
 }  // namespace sa

@@ -79,6 +79,8 @@ struct VerifyParams {
   float* part_o;   // [B*Hkv][n_splits][MT*16][128]
   float* part_ml;  // [B*Hkv][n_splits][MT*16][2]
   int* counters;   // [B*Hkv]
+  int* chunk_ctr;  // [B*Hkv] dynamic chunk claims (tcgen05 verify), re-armed by the merging CTA
+  unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production
 };
 
 struct DraftParams {
@@ -98,6 +100,8 @@ struct DraftParams {
   float* part_o;   // [B*Hkv][n_splits][16][128]
   float* part_ml;
   int* counters;
+  unsigned long long* trace;  // dev-only per-CTA phase timestamps; null in production
+  int use_pdl;  // launch with programmatic stream serialization (iteration graph only)
 };
 
 struct SelectParams {
@@ -117,6 +121,8 @@ struct SelectParams {
 cudaError_t launch_verify(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
 cudaError_t launch_verify_tc(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s);
+int draft_max_splits();
+int draft_round_rows();
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 size_t verify_smem_bytes(int MT);
 int verify_max_ctas_per_sm(int MT);

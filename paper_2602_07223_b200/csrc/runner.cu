@@ -7,6 +7,7 @@
 // graph and replayed.
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -36,7 +37,7 @@ struct sa_runner {
   // split-KV workspaces
   int64_t v_units_cap = 0, d_units_cap = 0;
   float *v_po = nullptr, *v_pml = nullptr, *d_po = nullptr, *d_pml = nullptr;
-  int *v_cnt = nullptr, *d_cnt = nullptr;
+  int *v_cnt = nullptr, *d_cnt = nullptr, *v_chunk = nullptr;
   // streams / graph
   cudaStream_t side = nullptr;
   cudaStream_t capture = nullptr;  // graphs are captured here (the caller's stream may be legacy)
@@ -87,7 +88,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   if (cfg->n_q_heads < 1 || cfg->n_q_heads % cache->n_kv_heads)
     return fail(SA_INVALID_ARGUMENT, "n_q_heads must be a positive multiple of n_kv_heads");
   const int G = cfg->n_q_heads / static_cast<int>(cache->n_kv_heads);
-  if (G > 16) return fail(SA_NOT_SUPPORTED, "GQA group size > 16");
+  if (G > 8) return fail(SA_NOT_SUPPORTED, "GQA group size > 8 (draft kernel n8 tile)");
   if (cfg->max_rows < 1 || mtiles_for(G, cfg->max_rows) > 4)
     return fail(SA_NOT_SUPPORTED, "G*(gamma+1)+2 must be <= 64");
   if (cfg->max_batch < 1 || cfg->max_batch > cache->max_seqs) return fail(SA_INVALID_ARGUMENT, "max_batch");
@@ -123,6 +124,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   alloc(reinterpret_cast<void**>(&r->v_po), sizeof(float) * r->v_units_cap * 64 * 128);
   alloc(reinterpret_cast<void**>(&r->v_pml), sizeof(float) * r->v_units_cap * 64 * 2);
   alloc(reinterpret_cast<void**>(&r->v_cnt), sizeof(int) * mb * H);
+  alloc(reinterpret_cast<void**>(&r->v_chunk), sizeof(int) * mb * H);
   alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
   alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
@@ -155,7 +157,7 @@ SA_API sa_status sa_runner_destroy(sa_runner* r) {
   if (r->capture) cudaStreamDestroy(r->capture);
   for (void* p : {static_cast<void*>(r->d_seq), static_cast<void*>(r->d_p0), static_cast<void*>(r->scores),
                   static_cast<void*>(r->idx), static_cast<void*>(r->kcnt), static_cast<void*>(r->keys),
-                  static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_cnt),
+                  static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_cnt), static_cast<void*>(r->v_chunk),
                   static_cast<void*>(r->d_po), static_cast<void*>(r->d_pml), static_cast<void*>(r->d_cnt)})
     cudaFree(p);
   delete r;
@@ -253,11 +255,35 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.counters = r->v_cnt;
     e = sa::launch_verify(p, r->cache->tmap_k, r->cache->tmap_v, s);
   } else {
-    p.n_splits = choose_splits(units, r->p_max, 128, 0, r->num_sms, r->v_units_cap, 128, &p.chunk);
+    // one CTA per SM over all units (dynamic chunk claiming balances inside a unit)
+    const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + 1) / 2);
+    p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, (r->num_sms + units - 1) / units),
+                                                     n_chunks, 128, r->v_units_cap / units}));
+    p.chunk = 0;
+    p.chunk_ctr = r->v_chunk;
     p.part_o = r->v_po;
     p.part_ml = r->v_pml;
     p.counters = r->v_cnt;
+    static unsigned long long* trace = [] {
+      unsigned long long* t = nullptr;
+      if (getenv("SA_TRACE")) {
+        cudaMalloc(&t, 3072 * 8);
+        cudaMemset(t, 0, 3072 * 8);
+      }
+      return t;
+    }();
+    p.trace = trace;
     e = sa::launch_verify_tc(p, r->cache->tmap_k128, r->cache->tmap_v128, s);
+    if (trace && getenv("SA_TRACE_DUMP")) {
+      cudaStreamSynchronize(s);
+      std::vector<unsigned long long> h(3072);
+      cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+      FILE* f = fopen(getenv("SA_TRACE_DUMP"), "wb");
+      if (f) {
+        fwrite(h.data(), 8, h.size(), f);
+        fclose(f);
+      }
+    }
   }
   if (e != cudaSuccess) return sa::cuda_fail(e, "verify launch");
   return SA_OK;
@@ -288,7 +314,7 @@ static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t
   return SA_OK;
 }
 
-static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s) {
+static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s, bool pdl = false) {
   if (!a || !a->q || !a->out) return fail(SA_INVALID_ARGUMENT, "draft: null argument");
   if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "draft: no batch bound");
   if (a->layer < 0 || a->layer >= r->cache->n_layers) return fail(SA_OUT_OF_RANGE, "draft: layer out of range");
@@ -319,11 +345,39 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.scale_log2 = a->scale * sa::kLog2e;
   p.out = a->out;
   const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
-  p.n_splits = choose_splits(units, r->k_cap + a->step, 64, 128, 3 * r->num_sms, r->d_units_cap, 192, &p.chunk);
+  {  // one cluster of CS CTAs per (sequence, KV head); >= 64 keys per CTA, CS <= 16
+    const int64_t m = r->k_cap + a->step;
+    int cs = static_cast<int>(std::min<int64_t>(sa::draft_max_splits(), std::max<int64_t>(1, (m + 63) / 64)));
+    if (cs > 8 && cs < 16) cs = 16;  // cluster sizes 1, 2, 4, 8, 16
+    else if (cs > 4 && cs < 8) cs = 8;
+    else if (cs == 3) cs = 4;
+    p.n_splits = cs;
+    p.chunk = static_cast<int>(((m + cs - 1) / cs + 15) / 16 * 16);
+  }
   p.part_o = r->d_po;
   p.part_ml = r->d_pml;
   p.counters = r->d_cnt;
+  static unsigned long long* dtr = [] {
+    unsigned long long* t = nullptr;
+    if (getenv("SA_TRACE")) {
+      cudaMalloc(&t, 512 * 8 * 8);
+      cudaMemset(t, 0, 512 * 8 * 8);
+    }
+    return t;
+  }();
+  p.trace = dtr;
+  p.use_pdl = pdl ? 1 : 0;
   cudaError_t e = sa::launch_draft(p, s);
+  if (dtr && getenv("SA_DTRACE_DUMP")) {
+    cudaStreamSynchronize(s);
+    std::vector<unsigned long long> h(512 * 8);
+    cudaMemcpy(h.data(), dtr, h.size() * 8, cudaMemcpyDeviceToHost);
+    FILE* f = fopen(getenv("SA_DTRACE_DUMP"), "wb");
+    if (f) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   if (e != cudaSuccess) return sa::cuda_fail(e, "draft launch");
   return SA_OK;
 }
@@ -396,7 +450,7 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
       d.v_new = vdn ? vdn + off * kd_l : nullptr;
       d.scale = a->scale;
       d.out = a->out_d + off * qd_l;
-      if (sa_status st = draft_impl(r, &d, main)) return st;
+      if (sa_status st = draft_impl(r, &d, main, /*pdl=*/j > 1 || l > 0)) return st;
     }
   }
   SA_CUDA_CHECK(cudaEventRecord(r->ev_join, r->side));

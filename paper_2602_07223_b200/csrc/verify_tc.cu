@@ -18,9 +18,10 @@
 // no cross-thread work; otherwise the warpgroup reduces the tile's row max, rescales its l partials
 // and O^T columns in TMEM, and continues (exact: every p uses the same reference as its O/l terms).
 //
-// Warp roles (352 threads): w0 K producer, w1 V producer (TMA, 128-token SWIZZLE_128B boxes, separate
-// rings so K is recycled right after QK^T), w2 MMA issuer (single elected thread; owns the TMEM
-// allocation), w3-6 softmax warpgroup 0, w7-10 softmax warpgroup 1.  The last split appends the
+// Warp roles (384 threads, setmaxnreg-rebalanced): w0 TMA producer (one thread, 128-token SWIZZLE_128B
+// boxes, separate K and V rings so K is recycled right after QK^T), w1 MMA issuer (single thread; owns
+// the TMEM allocation), w2-3 spare (warpgroup 0 drops to 72 registers), w4-7 softmax warpgroup 0,
+// w8-11 softmax warpgroup 1 (216 registers each).  The last split appends the
 // gamma+1 window rows to the cache (fused KvStore::append) and reads them back through TMA as part of
 // its final tile, masked causally inside the window (row t sees window keys j < t).
 #include "attn_core.cuh"
@@ -31,32 +32,63 @@ namespace sa {
 template <int N>
 struct TCfg {
   static constexpr int kTile = 128;
-  static constexpr int kSK = (N <= 32) ? 3 : 2;       // K ring stages
-  static constexpr int kSV = 2;                       // V ring stages
+  static constexpr int kSK = 2;                       // K ring stages (K is recycled right after QK^T)
+  static constexpr int kSV = (N <= 32) ? 3 : 2;       // V ring stages (V is held until PV retires)
+  static constexpr int kPrefetch = 4;                 // tiles prefetched into L2 ahead of the ring loads
   static constexpr int kHalf = kTile * 128;           // one 64-column half of a K or V tile (16 KB)
   static constexpr int kTileBytes = 2 * kHalf;         // K or V tile (32 KB)
   static constexpr int kQHalf = N * 128;
   static constexpr int kPAtoms = (N + 31) / 32;        // 32-row MN atoms of the SW64 P layout
   static constexpr int kPBytes = kPAtoms * kTile * 64; // hi (or lo) P plane
+  static constexpr int kNP = 2 * kPAtoms * 32;         // merged PV width: [P_hi atoms | P_lo atoms]
   static constexpr int kOffK = 0;
   static constexpr int kOffV = kOffK + kSK * kTileBytes;
   static constexpr int kOffQ = kOffV + kSV * kTileBytes;
   static constexpr int kOffP = kOffQ + 2 * kQHalf;     // [wg][hi, lo]
   static constexpr int kOffBar = kOffP + 4 * kPBytes;
-  static constexpr int kNumBars = 2 * kSK + 2 * kSV + 10;
+  static constexpr int kPosRing = 8;                  // published tile positions (consumer-visible)
+  static constexpr int kChunkTiles = 2;               // tiles per dynamically claimed chunk
+  static constexpr int kNumBars = 2 * kSK + 2 * kSV + 10 + kPosRing;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
-  // misc: tmem slot, flag | mref[2][64] fac[2][64] ltot[2][64] wsc[64] lim[64] | red[2][4][64]
-  static constexpr int kMiscBytes = 16 + (2 + 2 + 2 + 1 + 1) * 64 * 4 + 2 * 4 * 64 * 4;
+  // misc: tmem slot, flag, ntiles[2] | mref[2][64] fac[2][64] ltot[2][64] wsc[64] lim[64] | red[2][4][64]
+  //       | tile_pos[kPosRing] | producer ring pring[16]
+  static constexpr int kMiscBytes = 16 + (2 + 2 + 2 + 1 + 1) * 64 * 4 + 2 * 4 * 64 * 4 + kPosRing * 4 + 16 * 4;
   static constexpr int kSmem = kOffMisc + kMiscBytes + 1024;
-  static constexpr int kThreads = 352;
-  static constexpr uint32_t kTmemCols = (4 * N <= 128) ? 128 : 256;
+  static constexpr int kThreads = 384;
+  // TMEM columns: S[2] (N each) then O[2] (kNP each: O_hi | O_lo)
+  static constexpr int kOCol = 2 * N;
+  static constexpr uint32_t kTmemCols = (2 * N + 2 * kNP <= 128) ? 128 : (2 * N + 2 * kNP <= 256) ? 256 : 512;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
-constexpr float kLazyMaxThresh = 8.0f;  // log2 units: p <= 2^8 before a forced max update
+constexpr float kLazyMaxThresh = 8.0f;
+
+// Butterfly all-reduce of N independent values across the warp, level-outer so the N shuffles of
+// each level pipeline instead of forming N serial 5-deep chains.
+template <int N>
+__device__ __forceinline__ void warp_allreduce_max(float (&x)[N]) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int m = 0; m < N; ++m) x[m] = fmaxf(x[m], __shfl_xor_sync(0xffffffffu, x[m], off));
+}
+template <int N>
+__device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int m = 0; m < N; ++m) x[m] += __shfl_xor_sync(0xffffffffu, x[m], off);
+}
+
+// dev-only pipeline trace: ev[e][t] = clock64 of event e at tile t for CTA (0,0,0)
+#define SA_TRACE(e, t)                                                                          \
+  do {                                                                                          \
+    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < 64)            \
+      p.trace[(e) * 64 + (t)] = clock64();                                                      \
+  } while (0)  // log2 units: p <= 2^8 before a forced max update
 
 template <int N>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(384, 1)
     verify_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                      const VerifyParams p) {
   using C = TCfg<N>;
@@ -73,6 +105,7 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 2;
   uint64_t* pv_done = p_empty + 2;
+  uint64_t* pos_bar = pv_done + 2;  // [kPosRing]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   int* flag = reinterpret_cast<int*>(smem + C::kOffMisc + 4);
   float* mref_all = reinterpret_cast<float*>(smem + C::kOffMisc + 16);  // [2][64]
@@ -81,24 +114,26 @@ __global__ void __launch_bounds__(352, 1)
   float* wsc = ltot + 128;                                               // [64] score weights 0/1
   int* lim = reinterpret_cast<int*>(wsc + 64);                           // [64]
   float* red_all = reinterpret_cast<float*>(lim + 64);                   // [2][4][64]
+  int* tile_pos = reinterpret_cast<int*>(red_all + 512);                 // [kPosRing]
+  int* pring = tile_pos + C::kPosRing;                                   // [16] producer-private
+  int* ntiles_wg = flag + 1;                                             // [2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int seq = p.seq_ids[b];
   const int p0 = p.p0[b];
   const int R = p.R, M = p.M, Hq = p.Hkv * p.G;
+  // Work split: full prefix tiles [0, n_pref*128) are shared by the unit's CTAs through chunks of
+  // kChunkTiles tiles — chunk `split` first, then chunks claimed from an atomic counter (dynamic
+  // balancing: attention is permutation-invariant and the score byproduct is position-indexed).
+  // The window tile(s) [n_pref*128, p0+R) (prefix tail + the gamma+1 window rows) belong to the
+  // last split, which also appends the window rows.
   const bool last = split == p.n_splits - 1;
-  int lo = split * p.chunk, hi;
-  if (!last) {
-    hi = min(lo + p.chunk, p0);
-  } else {
-    lo = min(lo, p0);
-    hi = p0 + R;
-  }
-  const int tile0 = lo & ~(C::kTile - 1);
-  const int n_tiles = hi > lo ? (hi - tile0 + C::kTile - 1) / C::kTile : 0;
-  const int pre_hi = min(hi, p0);  // end of this CTA's prefix columns (score byproduct range)
-
+  const int n_pref = p0 / C::kTile;
+  const int win_lo = n_pref * C::kTile;
+  const int n_win = (p0 + R - win_lo + C::kTile - 1) / C::kTile;
+  const int n_chunks = (n_pref + C::kChunkTiles - 1) / C::kChunkTiles;
+  const int unit = b * p.Hkv + g;
   // ------------------------------------------------------------------ prologue (all threads)
   if (tid == 0) {
     for (int s = 0; s < C::kSK; ++s) {
@@ -109,6 +144,7 @@ __global__ void __launch_bounds__(352, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
+    for (int i = 0; i < C::kPosRing; ++i) mbar_init(&pos_bar[i], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 128);
@@ -144,62 +180,123 @@ __global__ void __launch_bounds__(352, 1)
     fence_proxy_async();  // generic-proxy global writes -> async-proxy (TMA) reads
   }
   fence_proxy_async_smem();  // Q tile: generic smem writes -> tensor-core reads
-  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (tid == 0) SA_TRACE(11, 0);
+  const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (p.trace && tid == 0 && cta_lin < 1024) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[1024 + 2 * cta_lin] = gt;
+  }
   const uint32_t tmem = *tmem_slot;
 
-  if (warp <= 1) {
-    // ---------------------------------------------------------------- TMA producers (K: w0, V: w1)
-    if (lane == 0 && n_tiles > 0) {
-      const CUtensorMap* map = warp == 0 ? &tmk : &tmv;
-      const int S = warp == 0 ? C::kSK : C::kSV;
-      uint64_t* full = warp == 0 ? k_full : v_full;
-      uint64_t* empty = warp == 0 ? k_empty : v_empty;
-      uint8_t* ring = smem + (warp == 0 ? C::kOffK : C::kOffV);
-      tma_prefetch_desc(map);
+  if (warp < 4) {
+  setmaxnreg_dec<72>();  // warpgroup 0: producer / MMA issuer / spare
+  if (warp == 0) {
+    // ---------------------------------------------------------------- TMA producer (one thread)
+    // K and V rings are refilled independently (K frees right after QK^T, V after PV): the thread
+    // polls both empty barriers without blocking and issues whichever stage is free.
+    if (lane == 0) {
+      tma_prefetch_desc(&tmk);
+      tma_prefetch_desc(&tmv);
       const uint64_t pol = policy_evict_first();
-      for (int t = 0; t < n_tiles; ++t) {
-        const int st = t % S;
-        if (t >= S) mbar_wait(&empty[st], ((t / S) & 1) ^ 1);
-        const int row = static_cast<int>(cache_row(p.cache, seq, p.layer, g, tile0 + t * C::kTile));
-        uint8_t* dst = ring + st * C::kTileBytes;
-        mbar_expect_tx(&full[st], C::kTileBytes);
-        tma_load_2d(dst, map, &full[st], 0, row, pol);
-        tma_load_2d(dst + C::kHalf, map, &full[st], 64, row, pol);
+      // tile stream of this CTA: window tiles (last split), then its chunks; pring holds positions
+      int q_end = 0, cur_chunk = -1, cur_tile = 0, claims = 0;
+      bool exhausted = false;
+      if (last)
+        for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 15] = win_lo + w2 * C::kTile;
+      auto fill = [&](int upto) {
+        while (q_end < upto && !exhausted) {
+          if (cur_chunk < 0 || cur_tile == min(C::kChunkTiles, n_pref - cur_chunk * C::kChunkTiles)) {
+            cur_chunk = claims++ == 0 ? split : p.n_splits + atomicAdd(p.chunk_ctr + unit, 1);
+            if (cur_chunk >= n_chunks) {
+              exhausted = true;
+              break;
+            }
+            cur_tile = 0;
+          }
+          pring[q_end++ & 15] = (cur_chunk * C::kChunkTiles + cur_tile++) * C::kTile;
+        }
+      };
+      auto row_of = [&](int pos) { return static_cast<int>(cache_row(p.cache, seq, p.layer, g, pos)); };
+      int nk = 0, nv = 0, npf = 0;
+      while (true) {
+        fill(nk + 1 + C::kPrefetch);
+        for (; npf < min(q_end, nv + C::kSV + C::kPrefetch) && nk >= 1; ++npf) {  // L2 prefetch
+          const int row = row_of(pring[npf & 15]);
+          tma_prefetch_l2_2d(&tmk, 0, row);
+          tma_prefetch_l2_2d(&tmk, 64, row);
+          tma_prefetch_l2_2d(&tmv, 0, row);
+          tma_prefetch_l2_2d(&tmv, 64, row);
+        }
+        if (nk < q_end && (nk < C::kSK || mbar_test(&k_empty[nk % C::kSK], ((nk / C::kSK) & 1) ^ 1))) {
+          const int st = nk % C::kSK, pos = pring[nk & 15];
+          tile_pos[nk % C::kPosRing] = pos;  // publish before the loads (mbarrier arrive = release)
+          mbar_arrive(&pos_bar[nk % C::kPosRing]);
+          const int row = row_of(pos);
+          uint8_t* dst = smem + C::kOffK + st * C::kTileBytes;
+          mbar_expect_tx(&k_full[st], C::kTileBytes);
+          tma_load_2d(dst, &tmk, &k_full[st], 0, row, pol);
+          tma_load_2d(dst + C::kHalf, &tmk, &k_full[st], 64, row, pol);
+          SA_TRACE(0, nk);
+          ++nk;
+        }
+        if (nv < nk && (nv < C::kSV || mbar_test(&v_empty[nv % C::kSV], ((nv / C::kSV) & 1) ^ 1))) {
+          const int st = nv % C::kSV;
+          const int row = row_of(pring[nv & 15]);
+          uint8_t* dst = smem + C::kOffV + st * C::kTileBytes;
+          mbar_expect_tx(&v_full[st], C::kTileBytes);
+          tma_load_2d(dst, &tmv, &v_full[st], 0, row, pol);
+          tma_load_2d(dst + C::kHalf, &tmv, &v_full[st], 64, row, pol);
+          SA_TRACE(1, nv);
+          ++nv;
+        }
+        if (exhausted && nk == q_end && nv == nk) break;
+      }
+      // end of stream for both softmax warpgroups and the MMA issuer
+      for (int e = 0; e < 2; ++e) {
+        tile_pos[(nk + e) % C::kPosRing] = -1;
+        mbar_arrive(&pos_bar[(nk + e) % C::kPosRing]);
       }
     }
-  } else if (warp == 2) {
+  } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (one thread)
-    if (lane == 0 && n_tiles > 0) {
+    if (lane == 0) {
       constexpr uint32_t idesc_qk = umma_idesc_bf16(N, 0, 0);
-      constexpr uint32_t idesc_pv = umma_idesc_bf16(N, 1, 1);
+      constexpr uint32_t idesc_pv = umma_idesc_bf16(C::kNP, 1, 1);
       const uint32_t q_base = smem_u32(sq);
       const uint32_t p_base = smem_u32(smem + C::kOffP);
       auto issue_pv = [&](int u) {
         const int wg = u & 1, sv = u % C::kSV;
         mbar_wait(&v_full[sv], (u / C::kSV) & 1);
+        SA_TRACE(5, u);
         mbar_wait(&p_full[wg], (u >> 1) & 1);
+        SA_TRACE(6, u);
         tc_fence_after();
         const uint32_t v_base = smem_u32(smem + C::kOffV + sv * C::kTileBytes);
-        const uint32_t p_hi = p_base + wg * 2 * C::kPBytes, p_lo = p_hi + C::kPBytes;
-        const uint32_t o_tm = tmem + 2 * N + wg * N;
+        const uint32_t p_pl = p_base + wg * 2 * C::kPBytes;
+        const uint32_t o_tm = tmem + C::kOCol + wg * C::kNP;
 #pragma unroll
-        for (int kt = 0; kt < 8; ++kt) {  // 16 tokens per MMA
+        for (int kt = 0; kt < 8; ++kt) {  // 16 tokens per MMA; one MMA covers P_hi and P_lo (N' = kNP)
           const uint64_t a = umma_desc(v_base + kt * 2048, C::kHalf, 1024, kLayoutSW128);
-          const uint64_t bh = umma_desc(p_hi + kt * 1024, C::kTile * 64, 512, kLayoutSW64);
-          const uint64_t bl = umma_desc(p_lo + kt * 1024, C::kTile * 64, 512, kLayoutSW64);
-          umma_bf16(o_tm, a, bh, idesc_pv, ((u >> 1) > 0 || kt > 0) ? 1u : 0u);
-          umma_bf16(o_tm, a, bl, idesc_pv, 1u);
+          const uint64_t bp = umma_desc(p_pl + kt * 1024, C::kTile * 64, 512, kLayoutSW64);
+          umma_bf16(o_tm, a, bp, idesc_pv, ((u >> 1) > 0 || kt > 0) ? 1u : 0u);
         }
         umma_commit(&v_empty[sv]);
         umma_commit(&p_empty[wg]);
         umma_commit(&pv_done[wg]);
+        SA_TRACE(3, u);
       };
-      for (int t = 0; t < n_tiles; ++t) {
+      int t = 0;
+      for (;; ++t) {
+        mbar_wait(&pos_bar[t % C::kPosRing], (t / C::kPosRing) & 1);
+        if (tile_pos[t % C::kPosRing] < 0) break;
         const int sk = t % C::kSK;
         mbar_wait(&k_full[sk], (t / C::kSK) & 1);
+        SA_TRACE(4, t);
         if (t >= 2) mbar_wait(&s_empty[t & 1], ((t >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(smem + C::kOffK + sk * C::kTileBytes);
@@ -211,16 +308,19 @@ __global__ void __launch_bounds__(352, 1)
         }
         umma_commit(&s_full[t & 1]);
         umma_commit(&k_empty[sk]);
+        SA_TRACE(2, t);
         if (t >= 1) issue_pv(t - 1);
       }
-      issue_pv(n_tiles - 1);
+      if (t >= 1) issue_pv(t - 1);
     }
+  }
   } else {
+    setmaxnreg_inc<216>();  // warpgroups 1-2: softmax
     // ---------------------------------------------------------------- softmax warpgroups
-    const int wg = (warp - 3) >> 2;     // 0: even tiles, 1: odd tiles
+    const int wg = (warp - 4) >> 2;     // 0: even tiles, 1: odd tiles
     const int q4 = warp & 3;            // TMEM lane quarter this warp may access
     const int tk = q4 * 32 + lane;      // token within the tile (S) / d (O)
-    const int ts = (warp - 3) * 32 + lane - wg * 128;  // 0..127 within the warpgroup
+    const int ts = tid - 128 - wg * 128;  // 0..127 within the warpgroup
     const int bar_wg = 2 + wg;
     const uint32_t lane_off = static_cast<uint32_t>(q4 * 32) << 16;
     const float c = p.scale_log2;
@@ -230,31 +330,35 @@ __global__ void __launch_bounds__(352, 1)
     float* score_out = p.scores ? p.scores + (static_cast<size_t>(b) * p.Hkv + g) * p.ld_scores : nullptr;
     uint8_t* p_hi = smem + C::kOffP + wg * 2 * C::kPBytes;
     const uint32_t s_tm = tmem + lane_off + wg * N;
-    const uint32_t o_tm = tmem + lane_off + 2 * N + wg * N;
+    const uint32_t o_tm = tmem + lane_off + C::kOCol + wg * C::kNP;  // O_hi at +0, O_lo at +kNP/2
     float l[N];
 #pragma unroll
     for (int m = 0; m < N; ++m) l[m] = 0.f;
 
     int i = 0;
-    for (int t = wg; t < n_tiles; t += 2, ++i) {
+    for (int t = wg;; t += 2, ++i) {
+      mbar_wait(&pos_bar[t % C::kPosRing], (t / C::kPosRing) & 1);
+      const int tstart = tile_pos[t % C::kPosRing];
+      if (tstart < 0) break;
       mbar_wait(&s_full[wg], i & 1);
+      if (ts == 0) SA_TRACE(7, t);
       tc_fence_after();
       float s[N];
       tmem_ld_n<N>(s_tm, s);
       tc_wait_ld();
       tc_fence_before();
       mbar_arrive(&s_empty[wg]);
-      const int tstart = tile0 + t * C::kTile;
+      if (ts == 0) SA_TRACE(12, t);
       const int pos = tstart + tk;
-      const bool full = tstart >= lo && tstart + C::kTile <= pre_hi;  // every row sees every token
-      const bool in_range = pos >= lo && pos < hi;
-      if (score_out && pos >= lo && pos < pre_hi) {  // fused Collect-k column sum (raw logits)
+      const bool full = tstart + C::kTile <= p0;  // chunk tiles: every row sees every token
+      const bool in_range = pos < p0 + R;         // window tiles: positions past the window masked
+      if (score_out && pos < p0) {  // fused Collect-k column sum (raw logits)
         float sc = 0.f;
 #pragma unroll
         for (int m = 0; m < N; ++m) sc = fmaf(wsc[m], s[m], sc);
         score_out[pos] = sc;
       }
-      if (p.logits && pos >= lo && pos < pre_hi) {  // debug / variant path: raw prefix logits
+      if (p.logits && pos < p0) {  // debug / variant path: raw prefix logits
 #pragma unroll
         for (int m = 0; m < N; ++m) {
           if (m >= M) continue;
@@ -264,24 +368,37 @@ __global__ void __launch_bounds__(352, 1)
           p.logits[((static_cast<size_t>(b) * Hq + g * p.G + m / R) * p.n_collect + ci) * p.ld_logits + pos] = s[m];
         }
       }
-      // pass 1: does any logit exceed the lazy reference by more than 2^8?
+      // pass 1: does any logit exceed the lazy reference by more than 2^8?  (mref held in registers:
+      // no shared-memory reads between the P stores below)
+      float mr[N];
+#pragma unroll
+      for (int m = 0; m < N; m += 4) *reinterpret_cast<float4*>(&mr[m]) = *reinterpret_cast<const float4*>(&mref[m]);
       bool exceed = false;
       if (full) {
 #pragma unroll
-        for (int m = 0; m < N; ++m) exceed |= fmaf(s[m], c, -mref[m]) > kLazyMaxThresh;
+        for (int m = 0; m < N; ++m) exceed |= fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
       } else {
 #pragma unroll
         for (int m = 0; m < N; ++m)
-          exceed |= (in_range && pos <= lim[m]) && fmaf(s[m], c, -mref[m]) > kLazyMaxThresh;
+          exceed |= (in_range && pos <= lim[m]) && fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
       }
-      if (named_bar_or(bar_wg, 128, exceed)) {
+      if (ts == 0) SA_TRACE(13, t);
+      const bool any_exceed = named_bar_or(bar_wg, 128, exceed);
+      if (ts == 0) SA_TRACE(14, t);
+      if (any_exceed) {
         // slow path: exact row max of this tile, rescale l partials and this warpgroup's O^T
+        float x[N];
 #pragma unroll
-        for (int m = 0; m < N; ++m) {
-          float x = (full || (in_range && pos <= lim[m])) ? s[m] * c : -INFINITY;
+        for (int m = 0; m < N; ++m) x[m] = s[m] * c;
+        if (!full) {
 #pragma unroll
-          for (int off = 16; off > 0; off >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, off));
-          if (lane == 0) red[q4 * 64 + m] = x;
+          for (int m = 0; m < N; ++m) x[m] = (in_range && pos <= lim[m]) ? x[m] : -INFINITY;
+        }
+        warp_allreduce_max<N>(x);
+        if (lane == 0) {
+#pragma unroll
+          for (int m = 0; m < N; m += 4)
+            *reinterpret_cast<float4*>(&red[q4 * 64 + m]) = make_float4(x[m], x[m + 1], x[m + 2], x[m + 3]);
         }
         named_bar_sync(bar_wg, 128);
         if (ts < N) {
@@ -293,21 +410,39 @@ __global__ void __launch_bounds__(352, 1)
         }
         named_bar_sync(bar_wg, 128);
 #pragma unroll
-        for (int m = 0; m < N; ++m) l[m] *= fac[m];
+        for (int m = 0; m < N; ++m) {
+          l[m] *= fac[m];
+          mr[m] = mref[m];
+        }
         if (i > 0) {  // O^T of this warpgroup is final through its previous tile once that PV is done
           mbar_wait(&pv_done[wg], (i - 1) & 1);
           tc_fence_after();
-          float v[N];
-          tmem_ld_n<N>(o_tm, v);
-          tc_wait_ld();
 #pragma unroll
-          for (int m = 0; m < N; ++m) v[m] *= fac[m];
-          tmem_st_n<N>(o_tm, v);
+          for (int half = 0; half < 2; ++half) {
+            float v[N];
+            tmem_ld_n<N>(o_tm + half * (C::kNP / 2), v);
+            tc_wait_ld();
+#pragma unroll
+            for (int m = 0; m < N; ++m) v[m] *= fac[m];
+            tmem_st_n<N>(o_tm + half * (C::kNP / 2), v);
+          }
           tc_wait_st();
         }
       }
+      // pass 2a: p = 2^(s*c - mref) in place, l += p (independent per row: full ILP)
+      if (full) {
+#pragma unroll
+        for (int m = 0; m < N; ++m) s[m] = fast_exp2(fmaf(s[m], c, -mr[m]));
+      } else {
+#pragma unroll
+        for (int m = 0; m < N; ++m) s[m] = (in_range && pos <= lim[m]) ? fast_exp2(fmaf(s[m], c, -mr[m])) : 0.f;
+      }
+#pragma unroll
+      for (int m = 0; m < N; ++m) l[m] += s[m];
+      if (ts == 0) SA_TRACE(8, t);
       if (i > 0) mbar_wait(&p_empty[wg], (i - 1) & 1);  // previous PV finished reading this P plane
-      // pass 2: p = 2^(s*c - mref), l += p, P^T -> smem as bf16 hi + lo (MN-major SWIZZLE_64B)
+      if (ts == 0) SA_TRACE(9, t);
+      // pass 2b: P^T -> smem as bf16 hi + lo planes (MN-major SWIZZLE_64B, 32-row atoms)
 #pragma unroll
       for (int a = 0; a < C::kPAtoms; ++a)
 #pragma unroll
@@ -315,19 +450,8 @@ __global__ void __launch_bounds__(352, 1)
           uint32_t hw[4], lw[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float x[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int m = 32 * a + 8 * ch + 2 * e + u;
-              if (m < N) {
-                const bool valid = full || (in_range && pos <= lim[m]);
-                x[u] = valid ? fast_exp2(fmaf(s[m], c, -mref[m])) : 0.f;
-                l[m] += x[u];
-              } else {
-                x[u] = 0.f;
-              }
-            }
-            split_bf16(x[0], x[1], hw[e], lw[e]);
+            const int m = 32 * a + 8 * ch + 2 * e;
+            split_bf16(m < N ? s[m] : 0.f, m + 1 < N ? s[m + 1] : 0.f, hw[e], lw[e]);
           }
           const uint32_t off = a * (C::kTile * 64) + tk * 64 + ((ch ^ ((tk >> 1) & 3)) << 4);
           *reinterpret_cast<uint4*>(p_hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -336,34 +460,41 @@ __global__ void __launch_bounds__(352, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&p_full[wg]);
+      if (ts == 0) SA_TRACE(10, t);
     }
 
     // ---------------------------------------------------------------- epilogue
     const int my_tiles = i;  // tiles this warpgroup processed
+    if (ts == 0) ntiles_wg[wg] = my_tiles;
     if (my_tiles > 0) {
       mbar_wait(&pv_done[wg], (my_tiles - 1) & 1);
       tc_fence_after();
     }
+    warp_allreduce_sum<N>(l);
+    if (lane == 0) {
 #pragma unroll
-    for (int m = 0; m < N; ++m) {
-      float x = l[m];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      if (lane == 0) red[q4 * 64 + m] = x;
+      for (int m = 0; m < N; m += 4)
+        *reinterpret_cast<float4*>(&red[q4 * 64 + m]) = make_float4(l[m], l[m + 1], l[m + 2], l[m + 3]);
     }
     named_bar_sync(bar_wg, 128);
     if (ts < N) ltot[wg * 64 + ts] = red[ts] + red[64 + ts] + red[128 + ts] + red[192 + ts];
     named_bar_sync(1, 256);  // both warpgroups' (mref, ltot) final
-    const int unit = b * p.Hkv + g;
     float* po = p.part_o + static_cast<size_t>(unit) * p.n_splits * N * 128;
     float* pml = p.part_ml + static_cast<size_t>(unit) * p.n_splits * N * 2;
     float* my_o = po + static_cast<size_t>(split) * N * 128;
-    const bool has0 = n_tiles > 0, has1 = n_tiles > 1;
+    const bool has0 = ntiles_wg[0] > 0, has1 = ntiles_wg[1] > 0;
     // merge the two warpgroups' O^T: warpgroup 0 takes even 16-column chunks, warpgroup 1 odd ones
     for (int c16 = wg; c16 < N / 16; c16 += 2) {
-      float o0[16], o1[16];
-      if (has0) tmem_ld16(tmem + lane_off + 2 * N + 16 * c16, o0);
-      if (has1) tmem_ld16(tmem + lane_off + 3 * N + 16 * c16, o1);
+      float o0[16], o1[16], t0[16], t1[16];
+      const uint32_t base = tmem + lane_off + C::kOCol + 16 * c16;
+      if (has0) {
+        tmem_ld16(base, o0);
+        tmem_ld16(base + C::kNP / 2, t0);
+      }
+      if (has1) {
+        tmem_ld16(base + C::kNP, o1);
+        tmem_ld16(base + C::kNP + C::kNP / 2, t1);
+      }
       tc_wait_ld();
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -371,8 +502,8 @@ __global__ void __launch_bounds__(352, 1)
         const float m0 = mref_all[m], m1 = mref_all[64 + m];
         const float ms = fmaxf(m0, m1);
         float acc = 0.f;
-        if (has0 && m0 != -INFINITY) acc += o0[j] * fast_exp2(m0 - ms);
-        if (has1 && m1 != -INFINITY) acc += o1[j] * fast_exp2(m1 - ms);
+        if (has0 && m0 != -INFINITY) acc += (o0[j] + t0[j]) * fast_exp2(m0 - ms);
+        if (has1 && m1 != -INFINITY) acc += (o1[j] + t1[j]) * fast_exp2(m1 - ms);
         my_o[m * 128 + tk] = acc;
       }
     }
@@ -382,16 +513,22 @@ __global__ void __launch_bounds__(352, 1)
       float lsum = 0.f;
       if (m0 != -INFINITY) lsum += ltot[ts] * fast_exp2(m0 - ms);
       if (m1 != -INFINITY) lsum += ltot[64 + ts] * fast_exp2(m1 - ms);
-      pml[(split * N + ts) * 2] = ms;
+      pml[(split * N + ts) * 2] = (has0 || has1) ? ms : -INFINITY;
       pml[(split * N + ts) * 2 + 1] = lsum;
     }
     tc_fence_before();
     float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
     combine_splits(po, pml, p.n_splits, N, M, p.counters + unit, flag, reinterpret_cast<float*>(smem),
                    wg * 128 + ts, 256, 1, [&](int row) { return out_unit + static_cast<size_t>(row) * 128; });
+    if (wg == 0 && ts == 0 && *flag == p.n_splits - 1) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
   }
   __syncthreads();
-  if (warp == 2) {
+  if (p.trace && tid == 0 && cta_lin < 1024) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[1024 + 2 * cta_lin + 1] = gt;
+  }
+  if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
   }
