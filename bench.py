@@ -58,7 +58,7 @@ def iteration_bytes(L, Hq, Hkv, p, gamma, k, B):
     s, d = 2, D
     per = ((p + gamma + 1) * 2 * Hkv * d * s                              # verify KV (+ window)
            + sum((k + t) * 2 * Hkv * d * s for t in range(1, gamma + 1))  # draft gathers
-           + Hkv * p * 4 * 2                                              # score partial write + read
+           + p * 8 * 2                                                    # per-layer score sums (int64) write + read
            + (gamma + 1) * Hq * d * (s + 4) + gamma * Hq * d * (s + 4)    # Q in (bf16), O out (f32)
            + (gamma + 1) * k * 4                                          # index write + reads
            + (2 * gamma + 1) * 2 * Hkv * d * s)                           # appends
@@ -69,7 +69,7 @@ def verify_launch_bytes(Hq, Hkv, p, R, B):
     """Algorithmic bytes of ONE verify launch (one layer): KV prefix + window rows + Q + O +
     score byproduct + fused append."""
     d = D
-    return B * (p * 2 * Hkv * d * 2 + R * 2 * Hkv * d * 2 + R * Hq * d * 2 + R * Hq * d * 4 + Hkv * p * 4
+    return B * (p * 2 * Hkv * d * 2 + R * 2 * Hkv * d * 2 + R * Hq * d * 2 + R * Hq * d * 4 + p * 8
                 + R * 2 * Hkv * d * 2)
 
 
@@ -200,6 +200,7 @@ def run_ours(args, rank, world, local_rank):
             a.record(stream)
             runner.verify(l, qv[l], out_v[l], kvn[l], vvn[l], scale, score_row_mask=1 | (1 << gamma), stream=stream)
             b_.record(stream)
+            runner.select(l, stream=stream)  # consumes (re-arms) the per-layer score sums, outside the events
     torch.cuda.synchronize()
     vms = sum(a.elapsed_time(b_) for a, b_ in ev[nv:]) / (len(ev) - nv)  # skip the first (warm) pass
 

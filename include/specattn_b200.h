@@ -143,6 +143,9 @@ SA_API sa_status sa_runner_set_batch(sa_runner* r, int32_t n, const int32_t* seq
                                      const int64_t* prefix_len_host);
 /* Per-layer device buffers owned by the runner (valid until destroy). */
 SA_API float* sa_runner_scores(sa_runner* r, int32_t layer_slot, int64_t* ld);      /* [B][Hkv][ld] */
+/* Per-layer score byproduct: int64 column sums in units of 2^-32 ([B][ld]); consumed (zeroed) by
+ * sa_select_topk in SA_PER_LAYER mode. */
+SA_API int64_t* sa_runner_layer_scores(sa_runner* r, int32_t layer_slot, int64_t* ld);
 SA_API int32_t* sa_runner_indices(sa_runner* r, int32_t layer_slot, int32_t* k_cap); /* [B][sets][k_cap] */
 SA_API int32_t* sa_runner_counts(sa_runner* r, int32_t layer_slot);                  /* [B][sets] */
 
@@ -163,6 +166,10 @@ typedef struct sa_verify_args {
   float* logits;            /* optional raw prefix logits f32 [B][Hq][n_collect][ld_logits]; NULL = off */
   int64_t ld_logits;
   uint32_t collect_row_mask;/* rows whose raw logits go to `logits` (n_collect = popcount) */
+  int32_t score_layout;     /* sa_select_mode the byproduct is laid out for: SA_PER_LAYER = one
+                               fixed-point column sum per (sequence, column) over all KV heads
+                               (sa_runner_layer_scores), SA_PER_KV_HEAD = fp32 per-head column
+                               sums (sa_runner_scores).  sa_select_topk must use the same mode. */
 } sa_verify_args;
 SA_API sa_status sa_verify_attention(sa_runner* r, const sa_verify_args* a, void* stream);
 
@@ -213,6 +220,11 @@ typedef struct sa_iteration_args {
 SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void* stream);
 /* Number of kernels one sa_iteration_run launches (for gpu_launches accounting). */
 SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_args* a);
+
+/* Development hook (not part of the reference surface): with SA_TRACE=1 in the environment the
+ * verify kernel records per-CTA start / main-loop-end / end timestamps per layer; this writes the
+ * trace buffer to `path` after a device sync.  Returns 0 on success, < 0 otherwise. */
+SA_API int sa_dev_trace_dump(const char* path);
 
 /* Reference helper: selection_k (selection.cpp:63-66). */
 SA_API int64_t sa_selection_k(double sparse_ratio, int64_t prefix_len, int64_t k_min);

@@ -40,7 +40,7 @@ class RunnerConfig(C.Structure):
 class VerifyArgs(C.Structure):
     _fields_ = [("layer", _i32), ("layer_slot", _i32), ("n_rows", _i32), ("q", _vp), ("k_new", _vp),
                 ("v_new", _vp), ("scale", _f32), ("score_row_mask", _u32), ("out", _vp), ("logits", _vp),
-                ("ld_logits", _i64), ("collect_row_mask", _u32)]
+                ("ld_logits", _i64), ("collect_row_mask", _u32), ("score_layout", _i32)]
 
 
 class SelectArgs(C.Structure):
@@ -80,6 +80,7 @@ SIGNATURES = {
     "sa_runner_destroy": (C.c_int, [_vp]),
     "sa_runner_set_batch": (C.c_int, [_vp, _i32, C.POINTER(_i32), C.POINTER(_i64)]),
     "sa_runner_scores": (_vp, [_vp, _i32, C.POINTER(_i64)]),
+    "sa_runner_layer_scores": (_vp, [_vp, _i32, C.POINTER(_i64)]),
     "sa_runner_indices": (_vp, [_vp, _i32, C.POINTER(_i32)]),
     "sa_runner_counts": (_vp, [_vp, _i32]),
     "sa_verify_attention": (C.c_int, [_vp, C.POINTER(VerifyArgs), _vp]),
@@ -87,6 +88,7 @@ SIGNATURES = {
     "sa_draft_attention": (C.c_int, [_vp, C.POINTER(DraftArgs), _vp]),
     "sa_iteration_run": (C.c_int, [_vp, C.POINTER(IterationArgs), _vp]),
     "sa_iteration_kernel_count": (_i64, [_vp, C.POINTER(IterationArgs)]),
+    "sa_dev_trace_dump": (C.c_int, [C.c_char_p]),
 }
 
 _LIB = None
@@ -250,6 +252,17 @@ class Runner:
         ptr = lib().sa_runner_scores(self.h, slot, C.byref(ld))
         return ptr, ld.value
 
+    def layer_scores(self, slot):
+        """Per-layer fixed-point column sums [B][ld] int64 (units of 2^-32), copied to host numpy."""
+        import numpy as np
+        import torch
+        ld = _i64()
+        ptr = lib().sa_runner_layer_scores(self.h, slot, C.byref(ld))
+        torch.cuda.synchronize()
+        out = np.empty(self.B * ld.value, np.int64)
+        cudart_memcpy(out.ctypes.data, ptr, out.nbytes)
+        return out.reshape(self.B, ld.value)
+
     def selection(self, slot, n_sets):
         """(indices [B][n_sets][k_cap] int32, counts [B][n_sets]) copied to host numpy."""
         import numpy as np
@@ -266,7 +279,7 @@ class Runner:
         return idx.reshape(self.B, n_sets, kc.value), cnt.reshape(self.B, n_sets)
 
     def verify(self, layer, q, out, k_new=None, v_new=None, scale=None, score_row_mask=None, layer_slot=None,
-               logits=None, collect_row_mask=0, stream=None):
+               logits=None, collect_row_mask=0, score_layout=PER_LAYER, stream=None):
         R = q.shape[-2]
         if scale is None:
             scale = float((1.0 / 128 ** 0.5))
@@ -274,7 +287,7 @@ class Runner:
             score_row_mask = 1 | (1 << (R - 1))
         a = VerifyArgs(layer, layer if layer_slot is None else layer_slot, R, _ptr(q), _ptr(k_new), _ptr(v_new),
                        scale, score_row_mask, _ptr(out), _ptr(logits),
-                       0 if logits is None else logits.shape[-1], collect_row_mask)
+                       0 if logits is None else logits.shape[-1], collect_row_mask, score_layout)
         _check(lib().sa_verify_attention(self.h, C.byref(a), _stream(stream)))
 
     def select(self, layer_slot, mode=PER_LAYER, rows_in_score=2, stream=None):

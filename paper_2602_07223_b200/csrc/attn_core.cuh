@@ -183,12 +183,15 @@ __device__ __forceinline__ void cta_partial_to_global(const float* wps, float* p
 template <typename OutRow>
 __device__ __forceinline__ void combine_splits(const float* part_o_unit, const float* part_ml_unit, int n_splits,
                                                int rows_pad, int rows_out, int* counter, int* smem_flag,
-                                               float* smem_w, int tid, int nthreads, int bar_id, OutRow out_row) {
-  __threadfence();
-  named_bar_sync(bar_id, nthreads);
-  if (tid == 0) *smem_flag = atomicAdd(counter, 1);
-  named_bar_sync(bar_id, nthreads);
-  if (*smem_flag != n_splits - 1) return;
+                                               float* smem_w, int tid, int nthreads, int bar_id, OutRow out_row,
+                                               bool arrived = false) {
+  if (!arrived) {  // arrival (skipped when the caller already counted this CTA in)
+    __threadfence();
+    named_bar_sync(bar_id, nthreads);
+    if (tid == 0) *smem_flag = atomicAdd(counter, 1);
+    named_bar_sync(bar_id, nthreads);
+    if (*smem_flag != n_splits - 1) return;
+  }
   __threadfence();
   float2* ml = reinterpret_cast<float2*>(smem_w);  // [n_splits][rows_out] (m, l) -> (w, -)
   for (int i = tid; i < n_splits * rows_out; i += nthreads) {

@@ -11,6 +11,10 @@ namespace sa {
 constexpr int kHeadDim = 128;
 constexpr int kRowBytes = kHeadDim * 2;  // one bf16 K or V row = 256 B
 constexpr float kLog2e = 1.4426950408889634f;
+// Per-layer score sums are accumulated across KV heads as int64 fixed point in units of 2^-32
+// (saturating f32 -> s64 conversion): exact, associative, so the sum is independent of the order
+// the verify CTAs finish in.
+constexpr float kScoreFxScale = 4294967296.0f;
 
 // ------------------------------------------------------------------------------------------- smem
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -356,5 +360,15 @@ __device__ __forceinline__ uint32_t movmatrix_trans(uint32_t x) {
   uint32_t y;
   asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
   return y;
+}
+}  // namespace sa
+
+namespace sa {
+// 1-D bulk copy global -> shared, completion counted on `bar` (complete_tx::bytes).  bytes % 16 == 0.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 }  // namespace sa

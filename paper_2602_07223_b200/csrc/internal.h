@@ -69,7 +69,8 @@ struct VerifyParams {
   float scale_log2;
   uint32_t score_mask;
   float* out;
-  float* scores;
+  float* scores;           // per-KV-head fp32 column sums [B][Hkv][ld] (SA_PER_KV_HEAD layout) or null
+  long long* score_fx;     // per-layer fixed-point column sums [B][ld] (SA_PER_LAYER layout) or null
   int64_t ld_scores;
   float* logits;
   int64_t ld_logits;
@@ -81,6 +82,8 @@ struct VerifyParams {
   int* counters;   // [B*Hkv]
   int* chunk_ctr;  // [B*Hkv] dynamic chunk claims (tcgen05 verify), re-armed by the merging CTA
   unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production
+  int use_pdl;  // programmatic dependent launch after the previous layer's verify (iteration graph)
+  int next_layer;  // layer verified next (its first tiles are prefetched into L2), -1: none
 };
 
 struct DraftParams {
@@ -107,7 +110,8 @@ struct DraftParams {
 struct SelectParams {
   int B, Hkv, n_sets;
   const int32_t* p0;
-  const float* scores;
+  const float* scores;     // per-KV-head fp32 sums (when score_fx is null)
+  long long* score_fx;     // per-layer fixed-point sums, zeroed as consumed
   int64_t ld_scores;
   double count;  // (#q-heads in the set) * rows_in_score
   double ratio;

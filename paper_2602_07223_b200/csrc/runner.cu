@@ -29,7 +29,10 @@ struct sa_runner {
   int32_t* d_p0 = nullptr;
   // selection buffers
   int64_t ld = 0;
-  float* scores = nullptr;     // [slots][max_batch][Hkv][ld]
+  float* scores = nullptr;     // [slots][max_batch][Hkv][ld]   per-KV-head layout
+  long long* score_fx = nullptr;  // [slots][max_batch][ld]    per-layer layout (fixed point)
+  std::vector<char> fx_dirty;  // slot holds unconsumed per-layer sums (needs zeroing before reuse)
+  std::vector<int> slot_layout;  // layout the slot's last verify wrote (-1: none)
   int k_cap = 0;
   int32_t* idx = nullptr;      // [slots][max_batch][Hkv][k_cap]
   int32_t* kcnt = nullptr;     // [slots][max_batch][Hkv]
@@ -80,6 +83,21 @@ int mtiles_for(int G, int R) { return (G * R + 2 + 15) / 16; }
 
 }  // namespace
 
+// dev-only verify pipeline trace (SA_TRACE=1): [1024] per-tile events of CTA 0, then per layer
+// (mod 64) [1024 CTAs][4] = start, main-loop end, end (globaltimer ns), tiles | split << 32.
+constexpr size_t kVTraceWords = 1024 + 64 * 4096;
+static unsigned long long* dev_verify_trace() {
+  static unsigned long long* t = [] {
+    unsigned long long* b = nullptr;
+    if (getenv("SA_TRACE")) {
+      cudaMalloc(&b, kVTraceWords * 8);
+      cudaMemset(b, 0, kVTraceWords * 8);
+    }
+    return b;
+  }();
+  return t;
+}
+
 extern "C" {
 
 SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, sa_runner** out) {
@@ -97,6 +115,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   if (!(cfg->sparse_ratio > 0.0) || cfg->sparse_ratio > 1.0)
     return fail(SA_INVALID_ARGUMENT, "SelectorConfig: sparse_ratio must be in (0, 1]");  // selection.cpp:50-53
   if (cfg->k_min < 0) return fail(SA_INVALID_ARGUMENT, "SelectorConfig: k_min must be >= 0");
+  dev_verify_trace();  // dev trace buffer (SA_TRACE) allocated outside any graph capture
   auto* r = new sa_runner();
   r->cache = cache;
   r->cfg = *cfg;
@@ -118,13 +137,17 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   alloc(reinterpret_cast<void**>(&r->d_seq), sizeof(int32_t) * mb);
   alloc(reinterpret_cast<void**>(&r->d_p0), sizeof(int32_t) * mb);
   alloc(reinterpret_cast<void**>(&r->scores), sizeof(float) * S * mb * H * r->ld);
+  alloc(reinterpret_cast<void**>(&r->score_fx), sizeof(long long) * S * mb * r->ld);
+  r->fx_dirty.assign(S, 0);
+  r->slot_layout.assign(S, -1);
   alloc(reinterpret_cast<void**>(&r->idx), sizeof(int32_t) * S * mb * H * r->k_cap);
   alloc(reinterpret_cast<void**>(&r->kcnt), sizeof(int32_t) * S * mb * H);
   alloc(reinterpret_cast<void**>(&r->keys), sizeof(uint32_t) * mb * H * r->ld);
-  alloc(reinterpret_cast<void**>(&r->v_po), sizeof(float) * r->v_units_cap * 64 * 128);
-  alloc(reinterpret_cast<void**>(&r->v_pml), sizeof(float) * r->v_units_cap * 64 * 2);
-  alloc(reinterpret_cast<void**>(&r->v_cnt), sizeof(int) * mb * H);
-  alloc(reinterpret_cast<void**>(&r->v_chunk), sizeof(int) * mb * H);
+  // verify split workspaces x2: consecutive layers alternate (PDL-chained verify launches)
+  alloc(reinterpret_cast<void**>(&r->v_po), 2 * sizeof(float) * r->v_units_cap * 64 * 128);
+  alloc(reinterpret_cast<void**>(&r->v_pml), 2 * sizeof(float) * r->v_units_cap * 64 * 2);
+  alloc(reinterpret_cast<void**>(&r->v_cnt), 2 * sizeof(int) * mb * H);
+  alloc(reinterpret_cast<void**>(&r->v_chunk), 2 * sizeof(int) * mb * H);
   alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
   alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
@@ -156,7 +179,7 @@ SA_API sa_status sa_runner_destroy(sa_runner* r) {
   if (r->side) cudaStreamDestroy(r->side);
   if (r->capture) cudaStreamDestroy(r->capture);
   for (void* p : {static_cast<void*>(r->d_seq), static_cast<void*>(r->d_p0), static_cast<void*>(r->scores),
-                  static_cast<void*>(r->idx), static_cast<void*>(r->kcnt), static_cast<void*>(r->keys),
+                  static_cast<void*>(r->idx), static_cast<void*>(r->score_fx), static_cast<void*>(r->kcnt), static_cast<void*>(r->keys),
                   static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_cnt), static_cast<void*>(r->v_chunk),
                   static_cast<void*>(r->d_po), static_cast<void*>(r->d_pml), static_cast<void*>(r->d_cnt)})
     cudaFree(p);
@@ -194,6 +217,11 @@ SA_API float* sa_runner_scores(sa_runner* r, int32_t slot, int64_t* ld) {
   if (ld) *ld = r->ld;
   return r->scores + static_cast<size_t>(slot) * r->cfg.max_batch * r->Hkv * r->ld;
 }
+SA_API int64_t* sa_runner_layer_scores(sa_runner* r, int32_t slot, int64_t* ld) {
+  if (!r || slot < 0 || slot >= r->n_slots) return nullptr;
+  if (ld) *ld = r->ld;
+  return reinterpret_cast<int64_t*>(r->score_fx + static_cast<size_t>(slot) * r->cfg.max_batch * r->ld);
+}
 SA_API int32_t* sa_runner_indices(sa_runner* r, int32_t slot, int32_t* k_cap) {
   if (!r || slot < 0 || slot >= r->n_slots) return nullptr;
   if (k_cap) *k_cap = r->k_cap;
@@ -204,7 +232,8 @@ SA_API int32_t* sa_runner_counts(sa_runner* r, int32_t slot) {
   return r->kcnt + static_cast<size_t>(slot) * r->cfg.max_batch * r->Hkv;
 }
 
-static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t s) {
+static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t s, bool pdl = false,
+                             bool in_iteration = false, int next_layer = -1) {
   if (!a || !a->q || !a->out) return fail(SA_INVALID_ARGUMENT, "verify: null argument");
   if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "verify: no batch bound");
   if (a->layer < 0 || a->layer >= r->cache->n_layers) return fail(SA_OUT_OF_RANGE, "verify: layer out of range");
@@ -213,6 +242,8 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   if (!(a->scale > 0.f)) return fail(SA_INVALID_ARGUMENT, "softmax_stable: scale must be positive");
   if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(SA_INVALID_ARGUMENT, "verify: k_new/v_new");
   if (a->score_row_mask >> a->n_rows) return fail(SA_INVALID_ARGUMENT, "score_columns: row label not collected");
+  if (a->score_layout != SA_PER_LAYER && a->score_layout != SA_PER_KV_HEAD)
+    return fail(SA_INVALID_ARGUMENT, "verify: score_layout");
   if (a->logits && (a->collect_row_mask == 0 || (a->collect_row_mask >> a->n_rows) || a->ld_logits < r->p_max))
     return fail(SA_INVALID_ARGUMENT, "verify: logits collection arguments");
   if (!a->k_new)
@@ -237,53 +268,56 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   p.scale_log2 = a->scale * sa::kLog2e;
   p.score_mask = a->score_row_mask;
   p.out = a->out;
-  p.scores = a->score_row_mask ? sa_runner_scores(r, a->layer_slot, &p.ld_scores) : nullptr;
+  p.scores = nullptr;
+  p.score_fx = nullptr;
+  p.ld_scores = r->ld;
+  if (a->score_row_mask) {
+    if (a->score_layout == SA_PER_KV_HEAD) {
+      p.scores = sa_runner_scores(r, a->layer_slot, &p.ld_scores);
+    } else {
+      p.score_fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, a->layer_slot, &p.ld_scores));
+      if (r->fx_dirty[a->layer_slot] && !in_iteration)  // unconsumed sums of an earlier verify
+        SA_CUDA_CHECK(cudaMemsetAsync(p.score_fx, 0, sizeof(long long) * r->cfg.max_batch * r->ld, s));
+      r->fx_dirty[a->layer_slot] = 1;
+    }
+    r->slot_layout[a->layer_slot] = a->score_layout;
+  }
   p.logits = a->logits;
   p.ld_logits = a->ld_logits;
   p.collect_mask = a->collect_row_mask;
   p.n_collect = __builtin_popcount(a->collect_row_mask);
   const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
+  const int par = a->layer & 1;  // workspace parity
+  const size_t po_stride = static_cast<size_t>(r->v_units_cap) * 64 * 128;
+  const size_t pml_stride = static_cast<size_t>(r->v_units_cap) * 64 * 2;
+  const size_t cnt_stride = static_cast<size_t>(r->cfg.max_batch) * r->Hkv;
   static const bool use_mma_sync = [] {
     const char* v = getenv("SA_VERIFY_IMPL");
     return v && std::string(v) == "mma";
   }();
   cudaError_t e;
   if (use_mma_sync) {
+    if (p.score_fx) return fail(SA_NOT_SUPPORTED, "SA_VERIFY_IMPL=mma: per-KV-head score layout only");
     p.n_splits = choose_splits(units, r->p_max, 64, 0, r->num_sms, r->v_units_cap, 128, &p.chunk);
     p.part_o = r->v_po;
     p.part_ml = r->v_pml;
     p.counters = r->v_cnt;
     e = sa::launch_verify(p, r->cache->tmap_k, r->cache->tmap_v, s);
   } else {
-    // one CTA per SM over all units (dynamic chunk claiming balances inside a unit)
+    // at most one CTA per SM over all units, a single wave (floor: a 149th CTA would run as a
+    // second wave); dynamic chunk claiming balances inside a unit
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + 1) / 2);
-    p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, (r->num_sms + units - 1) / units),
+    p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, r->num_sms / units),
                                                      n_chunks, 128, r->v_units_cap / units}));
     p.chunk = 0;
-    p.chunk_ctr = r->v_chunk;
-    p.part_o = r->v_po;
-    p.part_ml = r->v_pml;
-    p.counters = r->v_cnt;
-    static unsigned long long* trace = [] {
-      unsigned long long* t = nullptr;
-      if (getenv("SA_TRACE")) {
-        cudaMalloc(&t, 3072 * 8);
-        cudaMemset(t, 0, 3072 * 8);
-      }
-      return t;
-    }();
-    p.trace = trace;
+    p.chunk_ctr = r->v_chunk + par * cnt_stride;
+    p.part_o = r->v_po + par * po_stride;
+    p.part_ml = r->v_pml + par * pml_stride;
+    p.counters = r->v_cnt + par * cnt_stride;
+    p.use_pdl = pdl ? 1 : 0;
+    p.next_layer = next_layer;
+    p.trace = dev_verify_trace();
     e = sa::launch_verify_tc(p, r->cache->tmap_k128, r->cache->tmap_v128, s);
-    if (trace && getenv("SA_TRACE_DUMP")) {
-      cudaStreamSynchronize(s);
-      std::vector<unsigned long long> h(3072);
-      cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
-      FILE* f = fopen(getenv("SA_TRACE_DUMP"), "wb");
-      if (f) {
-        fwrite(h.data(), 8, h.size(), f);
-        fclose(f);
-      }
-    }
   }
   if (e != cudaSuccess) return sa::cuda_fail(e, "verify launch");
   return SA_OK;
@@ -294,12 +328,20 @@ static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t
   if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "select: no batch bound");
   if (a->layer_slot < 0 || a->layer_slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "select: layer_slot");
   if (a->rows_in_score < 1) return fail(SA_INVALID_ARGUMENT, "score_columns: empty row subset");
+  if (a->mode != SA_PER_LAYER && a->mode != SA_PER_KV_HEAD) return fail(SA_INVALID_ARGUMENT, "select: mode");
+  if (r->slot_layout[a->layer_slot] >= 0 && r->slot_layout[a->layer_slot] != a->mode)
+    return fail(SA_INVALID_ARGUMENT, "select: mode differs from the score layout the verify wrote");
   sa::SelectParams p{};
   p.B = r->B;
   p.Hkv = r->Hkv;
   p.n_sets = a->mode == SA_PER_LAYER ? 1 : r->Hkv;
   p.p0 = r->d_p0;
   p.scores = sa_runner_scores(r, a->layer_slot, &p.ld_scores);
+  p.score_fx = nullptr;
+  if (a->mode == SA_PER_LAYER) {
+    p.score_fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, a->layer_slot, nullptr));
+    r->fx_dirty[a->layer_slot] = 0;  // the kernel zeroes what it consumes
+  }
   p.count = static_cast<double>(a->mode == SA_PER_LAYER ? r->Hq : r->G) * a->rows_in_score;
   p.ratio = r->cfg.sparse_ratio;
   p.k_min = r->cfg.k_min;
@@ -359,7 +401,7 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.counters = r->d_cnt;
   static unsigned long long* dtr = [] {
     unsigned long long* t = nullptr;
-    if (getenv("SA_TRACE")) {
+    if (getenv("SA_DTRACE")) {  // dev-only; allocated on first draft call (outside graph capture)
       cudaMalloc(&t, 512 * 8 * 8);
       cudaMemset(t, 0, 512 * 8 * 8);
     }
@@ -380,6 +422,20 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   }
   if (e != cudaSuccess) return sa::cuda_fail(e, "draft launch");
   return SA_OK;
+}
+
+// dev-only: write the verify trace buffer to `path` (after a device sync); 0 on success.
+SA_API int sa_dev_trace_dump(const char* path) {
+  unsigned long long* t = dev_verify_trace();
+  if (!t || !path) return -1;
+  if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+  std::vector<unsigned long long> h(kVTraceWords);
+  if (cudaMemcpy(h.data(), t, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -3;
+  FILE* f = fopen(path, "wb");
+  if (!f) return -4;
+  fwrite(h.data(), 8, h.size(), f);
+  fclose(f);
+  return 0;
 }
 
 SA_API sa_status sa_verify_attention(sa_runner* r, const sa_verify_args* a, void* stream) {
@@ -413,6 +469,11 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
   const auto* qd = static_cast<const __nv_bfloat16*>(a->qd);
   const auto* kdn = static_cast<const __nv_bfloat16*>(a->kd_new);
   const auto* vdn = static_cast<const __nv_bfloat16*>(a->vd_new);
+  // dev-only phase isolation for timing breakdowns: SA_ITER_SKIP bit0 verify, bit1 select, bit2 draft
+  static const int skip = [] {
+    const char* v = getenv("SA_ITER_SKIP");
+    return v ? atoi(v) : 0;
+  }();
   SA_CUDA_CHECK(cudaEventRecord(r->ev_fork, main));
   SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
   for (int l = 0; l < L; ++l) {
@@ -425,15 +486,19 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     v.v_new = vvn ? vvn + l * kv_l : nullptr;
     v.scale = a->scale;
     v.score_row_mask = mask;
+    v.score_layout = a->mode;
     v.out = a->out_v + l * qv_l;
-    if (sa_status st = verify_impl(r, &v, main)) return st;
+    if ((skip & 1) == 0)
+      if (sa_status st = verify_impl(r, &v, main, /*pdl=*/l > 0, /*in_iteration=*/true, l + 1 < L ? l + 1 : -1))
+        return st;
     SA_CUDA_CHECK(cudaEventRecord(r->ev_v[l], main));
     SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_v[l], 0));
     sa_select_args sel{};
     sel.layer_slot = l;
     sel.mode = a->mode;
     sel.rows_in_score = rows_in_score;
-    if (sa_status st = select_impl(r, &sel, r->side)) return st;
+    if ((skip & 2) == 0)
+      if (sa_status st = select_impl(r, &sel, r->side)) return st;
     SA_CUDA_CHECK(cudaEventRecord(r->ev_s[l], r->side));
   }
   for (int j = 1; j <= a->gamma; ++j) {
@@ -450,7 +515,8 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
       d.v_new = vdn ? vdn + off * kd_l : nullptr;
       d.scale = a->scale;
       d.out = a->out_d + off * qd_l;
-      if (sa_status st = draft_impl(r, &d, main, /*pdl=*/j > 1 || l > 0)) return st;
+      if ((skip & 4) == 0)
+        if (sa_status st = draft_impl(r, &d, main, /*pdl=*/j > 1 || l > 0)) return st;
     }
   }
   SA_CUDA_CHECK(cudaEventRecord(r->ev_join, r->side));
@@ -467,6 +533,14 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
   if (r->n_slots < r->cache->n_layers) return fail(SA_INVALID_ARGUMENT, "iteration needs n_layers_buf >= n_layers");
   if (!a->qv || !a->qd || !a->out_v || !a->out_d) return fail(SA_INVALID_ARGUMENT, "iteration: null buffer");
   cudaStream_t main = static_cast<cudaStream_t>(stream);
+  // per-layer sums left unconsumed by direct verify calls: zero before the iteration accumulates
+  if (a->mode == SA_PER_LAYER)
+    for (int l = 0; l < r->cache->n_layers; ++l)
+      if (r->fx_dirty[l]) {
+        long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, l, nullptr));
+        SA_CUDA_CHECK(cudaMemsetAsync(fx, 0, sizeof(long long) * r->cfg.max_batch * r->ld, main));
+        r->fx_dirty[l] = 0;
+      }
   if (!a->use_graph) return enqueue_iteration(r, a, main);
   std::vector<char> key(sizeof(sa_iteration_args) + sizeof(int) + r->h_p0.size() * sizeof(int64_t) +
                         r->h_seq.size() * sizeof(int32_t));

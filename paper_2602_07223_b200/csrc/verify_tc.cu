@@ -48,7 +48,7 @@ struct TCfg {
   static constexpr int kOffBar = kOffP + 4 * kPBytes;
   static constexpr int kPosRing = 8;                  // published tile positions (consumer-visible)
   static constexpr int kChunkTiles = 2;               // tiles per dynamically claimed chunk
-  static constexpr int kNumBars = 2 * kSK + 2 * kSV + 10 + kPosRing;
+  static constexpr int kNumBars = 2 * kSK + 2 * kSV + 10 + kPosRing + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   // misc: tmem slot, flag, ntiles[2] | mref[2][64] fac[2][64] ltot[2][64] wsc[64] lim[64] | red[2][4][64]
   //       | tile_pos[kPosRing] | producer ring pring[16]
@@ -83,7 +83,7 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
 // dev-only pipeline trace: ev[e][t] = clock64 of event e at tile t for CTA (0,0,0)
 #define SA_TRACE(e, t)                                                                          \
   do {                                                                                          \
-    if (p.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < 64)            \
+    if (p.trace && p.layer == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < 64) \
       p.trace[(e) * 64 + (t)] = clock64();                                                      \
   } while (0)  // log2 units: p <= 2^8 before a forced max update
 
@@ -106,6 +106,8 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* p_empty = p_full + 2;
   uint64_t* pv_done = p_empty + 2;
   uint64_t* pos_bar = pv_done + 2;  // [kPosRing]
+  uint64_t* dep_bar = pos_bar + C::kPosRing;  // Q staged + window appended (after griddepcontrol.wait)
+  uint64_t* merge_bar = dep_bar + 1;          // split merge: partials bulk-loaded into smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
   int* flag = reinterpret_cast<int*>(smem + C::kOffMisc + 4);
   float* mref_all = reinterpret_cast<float*>(smem + C::kOffMisc + 16);  // [2][64]
@@ -127,7 +129,12 @@ __global__ void __launch_bounds__(384, 1)
   // kChunkTiles tiles — chunk `split` first, then chunks claimed from an atomic counter (dynamic
   // balancing: attention is permutation-invariant and the score byproduct is position-indexed).
   // The window tile(s) [n_pref*128, p0+R) (prefix tail + the gamma+1 window rows) belong to the
-  // last split, which also appends the window rows.
+  // last split, which also appends the window rows; they come last in its tile stream.
+  //
+  // Programmatic dependent launch (iteration graph): the prefix K/V of this layer does not depend on
+  // the previous kernel, so the producer starts streaming at once; Q and the new window rows (in a
+  // real model produced from the previous layer's output) are read by the MMA warp only after
+  // griddepcontrol.wait, which then releases dep_bar.
   const bool last = split == p.n_splits - 1;
   const int n_pref = p0 / C::kTile;
   const int win_lo = n_pref * C::kTile;
@@ -145,6 +152,8 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&v_empty[s], 1);
     }
     for (int i = 0; i < C::kPosRing; ++i) mbar_init(&pos_bar[i], 1);
+    mbar_init(dep_bar, 1);
+    mbar_init(merge_bar, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 128);
@@ -155,31 +164,12 @@ __global__ void __launch_bounds__(384, 1)
     fence_mbar_init();
   }
   uint8_t* sq = smem + C::kOffQ;
-  const __nv_bfloat16* qb = p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
-  for (int i = tid; i < N * 16; i += C::kThreads) {
-    const int row = i >> 4, ch = i & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < M) v = __ldg(reinterpret_cast<const uint4*>(qb + row * 128 + ch * 8));
-    *reinterpret_cast<uint4*>(sq + swz(row, ch, C::kQHalf)) = v;
-  }
   if (tid < 64) {
     mref_all[tid] = -INFINITY;
     mref_all[64 + tid] = -INFINITY;
     lim[tid] = tid < M ? p0 + tid % R : -1;  // last key position row m may see (causal window)
     wsc[tid] = (tid < M && ((p.score_mask >> (tid % R)) & 1u)) ? 1.f : 0.f;
   }
-  if (last && p.k_new) {  // fused KvStore::append of the window rows, read back below by TMA
-    for (int i = tid; i < 2 * R * 16; i += C::kThreads) {
-      const int which = i / (R * 16), row = (i >> 4) % R, ch = i & 15;
-      const __nv_bfloat16* src =
-          (which ? p.v_new : p.k_new) + ((static_cast<size_t>(b) * R + row) * p.Hkv + g) * 128;
-      const int64_t cr = cache_row(p.cache, seq, p.layer, g, p0 + row);
-      __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + cr * 128;
-      reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
-    }
-    fence_proxy_async();  // generic-proxy global writes -> async-proxy (TMA) reads
-  }
-  fence_proxy_async_smem();  // Q tile: generic smem writes -> tensor-core reads
   if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
   __syncthreads();
@@ -189,7 +179,7 @@ __global__ void __launch_bounds__(384, 1)
   if (p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[1024 + 2 * cta_lin] = gt;
+    p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin] = gt;
   }
   const uint32_t tmem = *tmem_slot;
 
@@ -205,9 +195,7 @@ __global__ void __launch_bounds__(384, 1)
       const uint64_t pol = policy_evict_first();
       // tile stream of this CTA: window tiles (last split), then its chunks; pring holds positions
       int q_end = 0, cur_chunk = -1, cur_tile = 0, claims = 0;
-      bool exhausted = false;
-      if (last)
-        for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 15] = win_lo + w2 * C::kTile;
+      bool exhausted = false, done = false, dep_seen = false;
       auto fill = [&](int upto) {
         while (q_end < upto && !exhausted) {
           if (cur_chunk < 0 || cur_tile == min(C::kChunkTiles, n_pref - cur_chunk * C::kChunkTiles)) {
@@ -219,6 +207,11 @@ __global__ void __launch_bounds__(384, 1)
             cur_tile = 0;
           }
           pring[q_end++ & 15] = (cur_chunk * C::kChunkTiles + cur_tile++) * C::kTile;
+        }
+        if (exhausted && !done) {  // the last split's window tiles close its stream
+          if (last)
+            for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 15] = win_lo + w2 * C::kTile;
+          done = true;
         }
       };
       auto row_of = [&](int pos) { return static_cast<int>(cache_row(p.cache, seq, p.layer, g, pos)); };
@@ -234,6 +227,10 @@ __global__ void __launch_bounds__(384, 1)
         }
         if (nk < q_end && (nk < C::kSK || mbar_test(&k_empty[nk % C::kSK], ((nk / C::kSK) & 1) ^ 1))) {
           const int st = nk % C::kSK, pos = pring[nk & 15];
+          if (pos >= win_lo && !dep_seen) {  // window rows are appended after the dependency wait
+            mbar_wait(dep_bar, 0);
+            dep_seen = true;
+          }
           tile_pos[nk % C::kPosRing] = pos;  // publish before the loads (mbarrier arrive = release)
           mbar_arrive(&pos_bar[nk % C::kPosRing]);
           const int row = row_of(pos);
@@ -254,7 +251,19 @@ __global__ void __launch_bounds__(384, 1)
           SA_TRACE(1, nv);
           ++nv;
         }
-        if (exhausted && nk == q_end && nv == nk) break;
+        if (done && nk == q_end && nv == nk) break;
+      }
+      // keep HBM busy across the layer boundary: pull the next layer's first tiles of this unit
+      // (the chunk the next layer's CTA `split` claims statically) into L2 while this layer drains
+      if (p.next_layer >= 0 && split < n_chunks) {
+        for (int t = 0; t < min(C::kChunkTiles, n_pref - split * C::kChunkTiles); ++t) {
+          const int row = static_cast<int>(
+              cache_row(p.cache, seq, p.next_layer, g, (split * C::kChunkTiles + t) * C::kTile));
+          tma_prefetch_l2_2d(&tmk, 0, row);
+          tma_prefetch_l2_2d(&tmk, 64, row);
+          tma_prefetch_l2_2d(&tmv, 0, row);
+          tma_prefetch_l2_2d(&tmv, 64, row);
+        }
       }
       // end of stream for both softmax warpgroups and the MMA issuer
       for (int e = 0; e < 2; ++e) {
@@ -263,6 +272,30 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
+    // ------------------------------------------- dependency wait, Q staging, fused window append
+    pdl_wait();
+    const __nv_bfloat16* qb = p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
+    for (int i = lane; i < N * 16; i += 32) {
+      const int row = i >> 4, ch = i & 15;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (row < M) v = __ldg(reinterpret_cast<const uint4*>(qb + row * 128 + ch * 8));
+      *reinterpret_cast<uint4*>(sq + swz(row, ch, C::kQHalf)) = v;
+    }
+    if (last && p.k_new) {  // fused KvStore::append of the window rows, read back by TMA
+      for (int i = lane; i < 2 * R * 16; i += 32) {
+        const int which = i / (R * 16), row = (i >> 4) % R, ch = i & 15;
+        const __nv_bfloat16* src =
+            (which ? p.v_new : p.k_new) + ((static_cast<size_t>(b) * R + row) * p.Hkv + g) * 128;
+        const int64_t cr = cache_row(p.cache, seq, p.layer, g, p0 + row);
+        __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + cr * 128;
+        reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
+      }
+      fence_proxy_async();  // generic-proxy global writes -> async-proxy (TMA) reads
+    }
+    fence_proxy_async_smem();  // Q tile: generic smem writes -> tensor-core reads
+    __syncwarp();
+    if (lane == 0) mbar_arrive(dep_bar);
+    pdl_launch_dependents();
     // ---------------------------------------------------------------- MMA issuer (one thread)
     if (lane == 0) {
       constexpr uint32_t idesc_qk = umma_idesc_bf16(N, 0, 0);
@@ -314,6 +347,10 @@ __global__ void __launch_bounds__(384, 1)
       if (t >= 1) issue_pv(t - 1);
     }
   }
+  if (warp != 1) {  // producer and spare warps: trigger only once this CTA is past its wait
+    mbar_wait(dep_bar, 0);
+    pdl_launch_dependents();
+  }
   } else {
     setmaxnreg_inc<216>();  // warpgroups 1-2: softmax
     // ---------------------------------------------------------------- softmax warpgroups
@@ -328,6 +365,7 @@ __global__ void __launch_bounds__(384, 1)
     float* fac = fac_all + wg * 64;
     float* red = red_all + wg * 256;
     float* score_out = p.scores ? p.scores + (static_cast<size_t>(b) * p.Hkv + g) * p.ld_scores : nullptr;
+    long long* score_fx = p.score_fx ? p.score_fx + static_cast<size_t>(b) * p.ld_scores : nullptr;
     uint8_t* p_hi = smem + C::kOffP + wg * 2 * C::kPBytes;
     const uint32_t s_tm = tmem + lane_off + wg * N;
     const uint32_t o_tm = tmem + lane_off + C::kOCol + wg * C::kNP;  // O_hi at +0, O_lo at +kNP/2
@@ -352,11 +390,15 @@ __global__ void __launch_bounds__(384, 1)
       const int pos = tstart + tk;
       const bool full = tstart + C::kTile <= p0;  // chunk tiles: every row sees every token
       const bool in_range = pos < p0 + R;         // window tiles: positions past the window masked
-      if (score_out && pos < p0) {  // fused Collect-k column sum (raw logits)
+      if ((score_out || score_fx) && pos < p0) {  // fused Collect-k column sum (raw logits)
         float sc = 0.f;
 #pragma unroll
         for (int m = 0; m < N; ++m) sc = fmaf(wsc[m], s[m], sc);
-        score_out[pos] = sc;
+        if (score_fx)  // per-layer: integer atomics over the KV heads (order-independent, deterministic)
+          atomicAdd(reinterpret_cast<unsigned long long*>(score_fx + pos),
+                    static_cast<unsigned long long>(__float2ll_rn(sc * kScoreFxScale)));
+        else
+          score_out[pos] = sc;
       }
       if (p.logits && pos < p0) {  // debug / variant path: raw prefix logits
 #pragma unroll
@@ -464,6 +506,17 @@ __global__ void __launch_bounds__(384, 1)
     }
 
     // ---------------------------------------------------------------- epilogue
+    // PDL chain: trigger the next layer's launch only once this CTA is past its griddepcontrol.wait
+    // (dep_bar is released after it), so "layer l+2 launched" implies "layer l complete" and the
+    // layer-parity workspaces (partials, counters, chunk claims) are free again by transitivity.
+    mbar_wait(dep_bar, 0);
+    pdl_launch_dependents();
+    if (p.trace && ts == 0 && wg == 0 && cta_lin < 1024) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin + 2] = gt;  // main loop done
+      p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin + 3] = static_cast<unsigned long long>(i) | (static_cast<unsigned long long>(split) << 32);
+    }
     const int my_tiles = i;  // tiles this warpgroup processed
     if (ts == 0) ntiles_wg[wg] = my_tiles;
     if (my_tiles > 0) {
@@ -479,12 +532,30 @@ __global__ void __launch_bounds__(384, 1)
     named_bar_sync(bar_wg, 128);
     if (ts < N) ltot[wg * 64 + ts] = red[ts] + red[64 + ts] + red[128 + ts] + red[192 + ts];
     named_bar_sync(1, 256);  // both warpgroups' (mref, ltot) final
+    const bool single = p.n_splits == 1;  // this CTA owns the whole unit: normalise in place
     float* po = p.part_o + static_cast<size_t>(unit) * p.n_splits * N * 128;
     float* pml = p.part_ml + static_cast<size_t>(unit) * p.n_splits * N * 2;
     float* my_o = po + static_cast<size_t>(split) * N * 128;
+    float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
+    float* fin_l = red_all;  // [64] per-row sum of this CTA (both warpgroups, common max)
     const bool has0 = ntiles_wg[0] > 0, has1 = ntiles_wg[1] > 0;
-    // merge the two warpgroups' O^T: warpgroup 0 takes even 16-column chunks, warpgroup 1 odd ones
+    if (wg == 0 && ts < N) {
+      const float m0 = mref_all[ts], m1 = mref_all[64 + ts];
+      const float ms = fmaxf(m0, m1);
+      float lsum = 0.f;
+      if (m0 != -INFINITY) lsum += ltot[ts] * fast_exp2(m0 - ms);
+      if (m1 != -INFINITY) lsum += ltot[64 + ts] * fast_exp2(m1 - ms);
+      fin_l[ts] = lsum;
+      if (!single) {
+        pml[(split * N + ts) * 2] = (has0 || has1) ? ms : -INFINITY;
+        pml[(split * N + ts) * 2 + 1] = lsum;
+      }
+    }
+    named_bar_sync(1, 256);
+    // merge the two warpgroups' O^T: warpgroup 0 takes even 16-column chunks, warpgroup 1 odd ones;
+    // only the M real rows are stored (partial rows keep the N-row stride)
     for (int c16 = wg; c16 < N / 16; c16 += 2) {
+      if (16 * c16 >= M) break;
       float o0[16], o1[16], t0[16], t1[16];
       const uint32_t base = tmem + lane_off + C::kOCol + 16 * c16;
       if (has0) {
@@ -499,34 +570,88 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int m = 16 * c16 + j;
+        if (m >= M) break;
         const float m0 = mref_all[m], m1 = mref_all[64 + m];
         const float ms = fmaxf(m0, m1);
         float acc = 0.f;
         if (has0 && m0 != -INFINITY) acc += (o0[j] + t0[j]) * fast_exp2(m0 - ms);
         if (has1 && m1 != -INFINITY) acc += (o1[j] + t1[j]) * fast_exp2(m1 - ms);
-        my_o[m * 128 + tk] = acc;
+        if (single) out_unit[m * 128 + tk] = acc / fin_l[m];
+        else my_o[m * 128 + tk] = acc;
       }
     }
-    if (wg == 0 && ts < N) {
-      const float m0 = mref_all[ts], m1 = mref_all[64 + ts];
-      const float ms = fmaxf(m0, m1);
-      float lsum = 0.f;
-      if (m0 != -INFINITY) lsum += ltot[ts] * fast_exp2(m0 - ms);
-      if (m1 != -INFINITY) lsum += ltot[64 + ts] * fast_exp2(m1 - ms);
-      pml[(split * N + ts) * 2] = (has0 || has1) ? ms : -INFINITY;
-      pml[(split * N + ts) * 2 + 1] = lsum;
-    }
     tc_fence_before();
-    float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
-    combine_splits(po, pml, p.n_splits, N, M, p.counters + unit, flag, reinterpret_cast<float*>(smem),
-                   wg * 128 + ts, 256, 1, [&](int row) { return out_unit + static_cast<size_t>(row) * 128; });
-    if (wg == 0 && ts == 0 && *flag == p.n_splits - 1) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
+    if (single) {
+      if (wg == 0 && ts == 0) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
+    } else {
+      // arrival: one fence + one atomic per CTA after the CTA-wide barrier (cumulativity)
+      named_bar_sync(1, 256);
+      if (wg == 0 && ts == 0) {
+        __threadfence();
+        *flag = atomicAdd(p.counters + unit, 1);
+      }
+      named_bar_sync(1, 256);
+      if (*flag == p.n_splits - 1) {
+        // last-arriving CTA merges the unit: all partials (M rows each) and (m, l) are pulled into
+        // the now idle ring buffers with bulk copies in flight together, then combined from smem
+        const uint32_t obytes = static_cast<uint32_t>(M) * 512u;
+        const uint32_t mlbytes = static_cast<uint32_t>(p.n_splits) * N * 8u;
+        if (static_cast<size_t>(p.n_splits) * obytes + mlbytes <= static_cast<size_t>(C::kOffBar)) {
+          if (wg == 0 && ts == 0) {
+            __threadfence();
+            fence_proxy_async();  // generic writes of the other CTAs -> async-proxy reads
+            mbar_expect_tx(merge_bar, p.n_splits * obytes + mlbytes);
+            for (int s2 = 0; s2 < p.n_splits; ++s2)
+              bulk_load(smem + s2 * obytes, po + static_cast<size_t>(s2) * N * 128, obytes, merge_bar);
+            bulk_load(smem + p.n_splits * obytes, pml, mlbytes, merge_bar);
+          }
+          mbar_wait(merge_bar, 0);
+          const float4* so = reinterpret_cast<const float4*>(smem);
+          float2* sml = reinterpret_cast<float2*>(smem + p.n_splits * obytes);  // [split][N] (m, l)
+          const int t256 = wg * 128 + ts;
+          if (t256 < M) {  // merge weights w_s = 2^(m_s - m*) / L in place of m_s
+            float mstar = -INFINITY;
+            for (int s2 = 0; s2 < p.n_splits; ++s2) mstar = fmaxf(mstar, sml[s2 * N + t256].x);
+            float lsum = 0.f;
+            for (int s2 = 0; s2 < p.n_splits; ++s2) {
+              const float2 v = sml[s2 * N + t256];
+              const float f = v.x == -INFINITY ? 0.f : fast_exp2(v.x - mstar);
+              sml[s2 * N + t256].x = f;
+              lsum += v.y * f;
+            }
+            const float inv = 1.f / lsum;
+            for (int s2 = 0; s2 < p.n_splits; ++s2) sml[s2 * N + t256].x *= inv;
+          }
+          named_bar_sync(1, 256);
+          for (int it = t256; it < M * 32; it += 256) {
+            const int row = it >> 5, c4 = it & 31;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s2 = 0; s2 < p.n_splits; ++s2) {
+              const float4 v = so[(s2 * M + row) * 32 + c4];
+              const float w = sml[s2 * N + row].x;
+              acc.x = fmaf(v.x, w, acc.x);
+              acc.y = fmaf(v.y, w, acc.y);
+              acc.z = fmaf(v.z, w, acc.z);
+              acc.w = fmaf(v.w, w, acc.w);
+            }
+            reinterpret_cast<float4*>(out_unit + static_cast<size_t>(row) * 128)[c4] = acc;
+          }
+          if (wg == 0 && ts == 0) p.counters[unit] = 0;  // re-arm for the next launch
+        } else {
+          // too many splits for shared memory: latency-aware merge straight from L2
+          combine_splits(po, pml, p.n_splits, N, M, p.counters + unit, flag, reinterpret_cast<float*>(smem),
+                         wg * 128 + ts, 256, 1, [&](int row) { return out_unit + static_cast<size_t>(row) * 128; },
+                         /*arrived=*/true);
+        }
+        if (wg == 0 && ts == 0) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
+      }
+    }
   }
   __syncthreads();
   if (p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[1024 + 2 * cta_lin + 1] = gt;
+    p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin + 1] = gt;
   }
   if (warp == 1) {
     tc_fence_after();
@@ -543,9 +668,17 @@ static cudaError_t launch_n(const VerifyParams& p, const CUtensorMap& tk, const 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid(p.n_splits, p.Hkv, p.B);
-  kern<<<grid, TCfg<N>::kThreads, TCfg<N>::kSmem, s>>>(tk, tv, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);
+  cfg.blockDim = dim3(TCfg<N>::kThreads);
+  cfg.dynamicSmemBytes = TCfg<N>::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p.use_pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, tk, tv, p);
 }
 
 cudaError_t launch_verify_tc(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s) {

@@ -86,7 +86,7 @@ VERIFY_CASES = [
 ]
 
 
-def _run_verify(ref, Hkv, G, R, p0s, page, seed=31, collect_all=True):
+def _run_verify(ref, Hkv, G, R, p0s, page, seed=31, collect_all=True, score_layout=1):
     import torch
     Runner, _, _ = _lib()
     Hq = Hkv * G
@@ -104,11 +104,14 @@ def _run_verify(ref, Hkv, G, R, p0s, page, seed=31, collect_all=True):
     logits = torch.full((B, Hq, R, ld), float("nan"), dtype=torch.float32, device="cuda")
     mask = (1 | (1 << (R - 1)))
     r.verify(layer, to_dev_bf16(q), out, to_dev_bf16(kn), to_dev_bf16(vn), SCALE, score_row_mask=mask,
-             logits=logits, collect_row_mask=(1 << R) - 1)
+             logits=logits, collect_row_mask=(1 << R) - 1, score_layout=score_layout)
     torch.cuda.synchronize()
-    sp, sld = r.scores(layer)
-    from paper_2602_07223_b200._lib import _device_bytes
-    scores = _device_bytes(sp, B * Hkv * sld * 4).view(torch.float32).reshape(B, Hkv, sld).cpu().numpy()
+    if score_layout == 1:  # per-KV-head fp32 column sums
+        sp, sld = r.scores(layer)
+        from paper_2602_07223_b200._lib import _device_bytes
+        scores = _device_bytes(sp, B * Hkv * sld * 4).view(torch.float32).reshape(B, Hkv, sld).cpu().numpy()
+    else:  # per-layer fixed-point sums over all KV heads (2^-32 units)
+        scores = r.layer_scores(layer)
     res = []
     for b in range(B):
         kv = m.refs[b]
@@ -153,10 +156,34 @@ def test_verify_parity(cuda, ref, Hkv, G, R, p0s, page):
     torch.cuda.synchronize()
 
 
+def test_layer_scores_fixed_point(cuda, ref):
+    """Per-layer score byproduct: int64 column sums over ALL KV heads (fixed point, 2^-32) ==
+    score_columns' numerator (selection.cpp:93-106); consumed (zeroed) by the per-layer select."""
+    Hkv, G, R, p0 = 4, 4, 5, 3000
+    m, r, q, kn, vn, out, logits, fx, res = _run_verify(ref, Hkv, G, R, [p0], 128, seed=45, score_layout=0)
+    l_ref = res[0][1]
+    rows = [0, R - 1]
+    want = l_ref[:, rows, :].astype(np.float64).sum((0, 1))
+    got = fx[0, :p0].astype(np.float64) / 2.0 ** 32
+    Kh = m.K[0][:p0].reshape(p0, 2, Hkv, D)[:, 1]
+    bound = np.einsum("hrd,phd->hrp", np.abs(q[0]), np.abs(Kh[:, np.arange(Hkv * G) // G]))[:, rows].sum((0, 1))
+    assert np.all(np.abs(got - want) <= 2e-5 * bound + 1e-4)
+    assert not fx[0, p0:].any()
+    r.select(1, mode=0, rows_in_score=2)
+    assert not r.layer_scores(1).any()  # re-armed for the next verify
+    # a second verify on the same slot without a select in between must not double-accumulate
+    import torch
+    out2 = torch.zeros((1, Hkv * G, R, D), dtype=torch.float32, device="cuda")
+    for _ in range(2):
+        r.verify(1, to_dev_bf16(q), out2, to_dev_bf16(kn), to_dev_bf16(vn), SCALE, score_row_mask=1 | (1 << (R - 1)))
+    assert np.array_equal(r.layer_scores(1), fx)
+
+
 def test_verify_deterministic(cuda, ref):
-    a = _run_verify(ref, 2, 4, 5, [1500], 128, seed=41)
-    b = _run_verify(ref, 2, 4, 5, [1500], 128, seed=41)
-    assert np.array_equal(a[5], b[5]) and np.array_equal(a[7], b[7])
+    for layout in (0, 1):
+        a = _run_verify(ref, 2, 4, 5, [1500], 128, seed=41, score_layout=layout)
+        b = _run_verify(ref, 2, 4, 5, [1500], 128, seed=41, score_layout=layout)
+        assert np.array_equal(a[5], b[5]) and np.array_equal(a[7], b[7])
 
 
 # ----------------------------------------------------------------------------------- select
@@ -170,7 +197,7 @@ def _gpu_select(r, slot, mode, n_sets, rows_in_score):
 @pytest.mark.parametrize("mode", [0, 1])
 def test_select_parity(cuda, ref, mode):
     Hkv, G, R, p0 = 8, 4, 5, 4096
-    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=51)
+    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=51, score_layout=mode)
     Runner, _, selection_k = _lib()
     l_ref = res[0][1]  # [Hq][R][p0]
     n_sets = 1 if mode == 0 else Hkv
@@ -226,7 +253,7 @@ def test_select_exact_ties_lower_index(cuda, ref):
 def test_draft_parity(cuda, ref, mode):
     torch = cuda
     Hkv, G, R, p0 = 8, 4, 5, 4096
-    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=71)
+    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=71, score_layout=mode)
     n_sets = 1 if mode == 0 else Hkv
     idx, cnt = _gpu_select(r, 1, mode, n_sets, 2)
     sets = [idx[0, s, : cnt[0, s]].astype(np.int64) for s in range(n_sets)]

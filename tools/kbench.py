@@ -42,12 +42,17 @@ def main():
 
     def verify():
         layer[0] = (layer[0] + 1) % L
-        r.verify(layer[0], q, out, kn, kn, sc)
+        r.verify(layer[0], q, out, kn, kn, sc, score_layout=1)
 
     tv = timed(verify)
-    for l in range(L):
-        r.verify(l, q, out, kn, kn, sc)
-    tsel = timed(lambda: r.select(1))
+    tsel_kv = timed(lambda: r.select(1, mode=1))
+
+    def sel_layer():
+        r.verify(1, q, out, kn, kn, sc)
+        r.select(1)
+
+    tvs = timed(sel_layer)
+    tsel = tvs - tv
     qd = torch.randn((1, Hq, D), device="cuda").to(torch.bfloat16)
     kd = torch.randn((1, Hkv, D), device="cuda").to(torch.bfloat16)
     od = torch.empty((1, Hq, D), device="cuda")
@@ -60,7 +65,7 @@ def main():
     kv_bytes = p0 * Hkv * 512
     k = r.selection(1, 1)[1][0, 0]
     print(f"verify  {tv:8.2f} us  {kv_bytes / tv / 1e3:8.1f} GB/s (KV only)")
-    print(f"select  {tsel:8.2f} us")
+    print(f"select  {tsel:8.2f} us (per layer, = verify+select - verify)   per-KV-head select {tsel_kv:8.2f} us")
     print(f"draft   {td:8.2f} us  k={k}  {(k + 2) * Hkv * 512 / td / 1e3:8.1f} GB/s")
 
 

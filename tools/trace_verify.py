@@ -1,4 +1,7 @@
-"""Dev tool: run one config-2 verify layer with SA_TRACE set and print the per-tile pipeline timeline."""
+"""Dev tool: config-2 verify of one layer with SA_TRACE set, after 3 other layers have streamed
+through L2 (so the traced layer is read from DRAM): CTA start / main-loop end / end and the per-tile
+pipeline timeline of CTA 0."""
+import ctypes
 import os
 import sys
 
@@ -7,12 +10,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ["SA_TRACE"] = "1"
-dump = os.path.join(ROOT, "gpurun_out", "trace.bin")
 import torch  # noqa: E402
 
 from paper_2602_07223_b200 import Cache, Runner  # noqa: E402
+from paper_2602_07223_b200._lib import lib  # noqa: E402
 
-L, Hq, Hkv, p0, R = 2, 32, 8, 32768, 5
+L, Hq, Hkv, p0, R = 4, 32, 8, int(os.environ.get("CTX", 32768)), 5
 cache = Cache(L, Hkv, 128, p0 + 64, page_size=256)
 for s in range(0, p0, 4096):
     kk = torch.randn((4096, L * Hkv, 128), device="cuda").to(torch.bfloat16)
@@ -22,21 +25,29 @@ r.set_batch([0], [p0])
 q = torch.randn((1, Hq, R, 128), device="cuda").to(torch.bfloat16)
 kn = torch.randn((1, R, Hkv, 128), device="cuda").to(torch.bfloat16)
 out = torch.empty((1, Hq, R, 128), device="cuda")
-for it in range(3):
-    if it == 2:
-        os.environ["SA_TRACE_DUMP"] = dump
-    r.verify(0, q, out, kn, kn)
+for it in range(2):
+    for layer in (1, 2, 3, 0):
+        r.verify(layer, q, out, kn, kn, score_layout=1)
 torch.cuda.synchronize()
+dump = os.path.join(ROOT, "gpurun_out", "trace.bin")
+os.makedirs(os.path.dirname(dump), exist_ok=True)
+f = lib().sa_dev_trace_dump
+f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
+assert f(dump.encode()) == 0
 raw = np.fromfile(dump, dtype=np.uint64).astype(np.int64)
 ev = raw[:1024].reshape(16, 64)
-se = raw[1024:3072].reshape(1024, 2)
-se = se[se[:, 0] > 0]
-g0 = se[:, 0].min()
-st, en = (se[:, 0] - g0) / 1e3, (se[:, 1] - g0) / 1e3
-print(f"CTAs {len(se)}: start us min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f}; "
-      f"end us min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f}; dur med {np.median(en - st):.2f}")
-order = np.argsort(en)[-6:]
-print("slowest CTAs (lin idx, start, end):", [(int(i), round(float(st[i]), 2), round(float(en[i]), 2)) for i in order])
+se4 = raw[1024:1024 + 4096].reshape(1024, 4)
+se4 = se4[se4[:, 0] > 0]
+g0 = se4[:, 0].min()
+st, en, ml = (se4[:, 0] - g0) / 1e3, (se4[:, 1] - g0) / 1e3, (se4[:, 2] - g0) / 1e3
+tiles, split = se4[:, 3] & 0xFFFFFFFF, se4[:, 3] >> 32
+print(f"CTAs {len(se4)}: start us min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f}; "
+      f"main-loop end min/med/max {ml.min():.2f}/{np.median(ml):.2f}/{ml.max():.2f}; "
+      f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f}")
+order = np.argsort(en)[-10:]
+print("slowest CTAs (lin, split, wg0 tiles, start, loop_end, end):",
+      [(int(i), int(split[i]), int(tiles[i]), round(float(st[i]), 2), round(float(ml[i]), 2), round(float(en[i]), 2)) for i in order])
+print("wg0 tiles per CTA: min/med/max", tiles.min(), np.median(tiles), tiles.max())
 t0 = ev[11, 0]
 names = ["K_issued", "V_issued", "QK_issued", "PV_issued", "MMA_kfull", "MMA_vfull", "MMA_pfull", "SM_sfull",
          "SM_pdone", "SM_pempty", "SM_parrive", "start", "SM_ldS", "SM_chk", "SM_bar"]
