@@ -263,6 +263,14 @@ class Runner:
         cudart_memcpy(out.ctypes.data, ptr, out.nbytes)
         return out.reshape(self.B, ld.value)
 
+    def layer_scores_tensor(self, slot):
+        """The per-layer int64 score sums of `slot` as a torch tensor ALIASING device memory ([B][ld]);
+        used for the KV-head-sharded exchange (shard.exchange_layer_scores) between verify and select."""
+        import torch
+        ld = _i64()
+        ptr = lib().sa_runner_layer_scores(self.h, slot, C.byref(ld))
+        return _device_bytes(ptr, self.B * ld.value * 8).view(torch.int64).reshape(self.B, ld.value)
+
     def selection(self, slot, n_sets):
         """(indices [B][n_sets][k_cap] int32, counts [B][n_sets]) copied to host numpy."""
         import numpy as np

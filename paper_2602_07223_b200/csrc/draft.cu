@@ -132,15 +132,19 @@ struct DCfg {
   static constexpr int kHalf = kTile * 128;
   static constexpr int kTileBytes = 2 * kHalf;
   static constexpr int kOffV = kMaxTiles * kTileBytes;
-  static constexpr int kOffQ = 2 * kMaxTiles * kTileBytes;
-  static constexpr int kQHalf = 16 * 128;
-  static constexpr int kOffPart = kOffQ + 2 * kQHalf;  // CTA partial: O[16][128], m[16], l[16]
   static constexpr int kPartFloats = 8 * 128 + 16;  // CTA partial: O[8 rows][128], m[8], l[8]
-  static constexpr int kOffRow = kOffPart + kPartFloats * 4;  // int64 source rows of the round
-  static constexpr int kOffW = kOffRow + kMaxTiles * kTile * 8;  // merge weights [kMaxCS][16]
-  static constexpr int kSmem = kOffW + kMaxCS * 16 * 4 * 2 + 1024;
+  static constexpr int kOffPart = 2 * kMaxTiles * kTileBytes;
+  static constexpr int kOffRow = kOffPart + kPartFloats * 4;      // int64 source rows of the round
+  static constexpr int kOffRecv = kOffRow + kMaxTiles * kTile * 8;  // merge inbox [kMaxCS][kRecvFloats]
+  static constexpr int kRecvFloats = 8 * 128 / 1 + 16;            // worst case (CS = 1) slice + (m, l)
+  static constexpr int kRecvPerSender = 64 + 16;                  // CS = 16, G = 8: 64-float slice + (m, l)
+  static constexpr int kRecvBytes = kMaxCS * kRecvPerSender * 4 > kRecvFloats * 4 ? kMaxCS * kRecvPerSender * 4
+                                                                                  : kRecvFloats * 4;
+  static constexpr int kOffBar = kOffRecv + kRecvBytes;
+  static constexpr int kSmem = kOffBar + 16 + 1024;
   static constexpr int kWarpPart = 8 * 128 + 16;     // per-warp partial, same layout
-  static_assert(kWarps * kWarpPart * 4 <= kOffQ, "warp partials must fit in the tile buffers");
+  static_assert(kWarps * kWarpPart * 4 <= kOffPart, "warp partials must fit in the tile buffers");
+  static_assert(kSmem <= 113 * 1024, "two CTAs per SM: the next PDL launch co-resides");
 };
 
 __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
@@ -149,15 +153,31 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
     if (cta < 512) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      p.trace[cta * 8 + phase] = gt;
+      const size_t launch = static_cast<size_t>((p.step - 1) & 7) * 64 + (p.layer & 63);
+      p.trace[(launch * 512 + cta) * 8 + phase] = gt;
     }
   }
 }
 
+// Grid (CS, Hkv, B) in clusters of CS CTAs: CTA `split` of a (sequence, KV head) owns rows
+// [split*chunk, (split+1)*chunk) of the virtual key list T[0..k) ++ [p0, p0+step).
+//
+// Before griddepcontrol.wait (overlapping the previous launch, two CTAs per SM): every row that
+// already exists — the selected prefix rows and the tail rows appended by earlier draft steps —
+// is resolved (index + block-table loads) and gathered into shared memory with 16-byte cp.async.
+// After the wait: the query and this step's new row (produced by the previous layer in a real
+// model), the fused append, then the mma.sync flash step over the resident rows.
+//
+// Merge without a global round trip and without a second cluster barrier: CTA r owns output slice r
+// of the G x 128 outputs; every CTA pushes its partial slices and (m, l) into the owners' inboxes
+// with st.async (remote shared-memory stores completing as transaction bytes on the owner's
+// mbarrier), and each owner combines its slice once its inbox is full.
 __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* part = reinterpret_cast<float*>(smem + DCfg::kOffPart);
+  float* inbox = reinterpret_cast<float*>(smem + DCfg::kOffRecv);
+  uint64_t* inbox_bar = reinterpret_cast<uint64_t*>(smem + DCfg::kOffBar);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int CS = gridDim.x;
@@ -173,34 +193,44 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
   const int n = max(0, v_end - v_begin);
   const int Hq = p.Hkv * p.G;
   const int new_pos = p0 + j - 1;
+  const int new_v = k + j - 1;  // virtual index of this step's new row
+  // rows written by earlier draft steps of this layer come from launches >= 2 back in the PDL
+  // chain, complete once this grid runs (every earlier CTA passed its own wait before triggering)
+  const bool old_tail_ready = p.cache.n_layers >= 2;
+  // output slices: CTA r owns outputs [r*per, min(G*128, (r+1)*per)), per a multiple of 4
+  const int n_out = p.G * 128;
+  const int per = ((n_out + CS - 1) / CS + 3) & ~3;
+  const int my_lo = min(n_out, split * per), my_hi = min(n_out, my_lo + per);
+  const int rstride = per + 16;  // inbox floats per sender
   dtrace(p, 0);
+  if (tid == 0) {
+    mbar_init(inbox_bar, 1);
+    fence_mbar_init();
+  }
+  cluster_arrive_release();  // inbox barriers initialised (waited on just before the pushes)
 
-  // Gather rows [v_begin + r0, v_begin + r0 + rows) of the virtual key list into the tile buffers.
-  // Step 1 resolves every row's source (index load + block-table load, all independent across
-  // threads) into shared memory; step 2 issues the 16-byte cp.async copies without any dependent
-  // global load in the loop.  prefix_only: rows at positions < p0 (selected by T) — independent
-  // of the previous kernel; otherwise the tail rows, the new row and zero fill.
-  int64_t* src_row = reinterpret_cast<int64_t*>(smem + DCfg::kOffRow);  // -1: k_new row, -2: zero fill
-  auto resolve = [&](int r0, int rows, bool prefix_only) {
+  int64_t* src_row = reinterpret_cast<int64_t*>(smem + DCfg::kOffRow);  // -1: new row (k_new), -2: zero fill
+  // pre: true -> rows that exist before this launch (gathered ahead of the dependency wait)
+  auto is_pre = [&](int v) { return v < k || (v != new_v && old_tail_ready); };
+  auto resolve = [&](int r0, int rows, bool pre_pass) {
     for (int r = tid; r < rows; r += DCfg::kThreads) {
       const int v = v_begin + r0 + r;
       if (v >= v_end) {
-        if (!prefix_only) src_row[r] = -2;
+        if (!pre_pass) src_row[r] = -2;
         continue;
       }
+      if (is_pre(v) != pre_pass) continue;
       const bool is_tail = v >= k;
-      if (is_tail == prefix_only) continue;
       const int pos = is_tail ? p0 + (v - k) : __ldg(T + v);
       src_row[r] = (p.k_new && pos == new_pos) ? -1 : cache_row(p.cache, seq, p.layer, g, pos);
     }
   };
-  auto gather = [&](int r0, int rows, bool prefix_only) {
+  auto gather = [&](int r0, int rows, bool pre_pass) {
     for (int i = tid; i < rows * 16; i += DCfg::kThreads) {
       const int r = i >> 4, ch = i & 15;
       const int v = v_begin + r0 + r;
       const bool in = v < v_end;
-      if (in && ((v >= k) == prefix_only)) continue;
-      if (!in && prefix_only) continue;
+      if (in ? (is_pre(v) != pre_pass) : pre_pass) continue;
       const int tile = r >> 6, rr = r & 63;
       const uint32_t off = tile * DCfg::kTileBytes + swz(rr, ch, DCfg::kHalf);
       const int64_t row = src_row[r];
@@ -220,33 +250,33 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
     }
   };
 
-  // selected prefix rows of round 0: independent of the previous kernel -> before the PDL wait
-  {
-    const int rows0 = (min(DCfg::kMaxTiles * DCfg::kTile, n) + 15) & ~15;
+  constexpr int kRoundRows = DCfg::kMaxTiles * DCfg::kTile;
+  {  // round 0, pre-existing rows: independent of the previous kernel
+    const int rows0 = (min(kRoundRows, n) + 15) & ~15;
     resolve(0, rows0, true);
     __syncthreads();
     gather(0, rows0, true);
     cp_async_commit();
   }
-  pdl_wait();  // previous layer complete: q, k_new and the tail rows are now valid
+  pdl_wait();  // previous layer complete: q and this step's new row are valid
   pdl_launch_dependents();
   dtrace(p, 1);
   DraftWarp w;
-  w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);  // (after the wait)
-  constexpr int kRoundRows = DCfg::kMaxTiles * DCfg::kTile;
+  w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
+  // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45)
+  if (split == 0 && p.k_new && tid < 32) {
+    const int which = tid >> 4, ch = tid & 15;
+    const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128;
+    const int64_t row = cache_row(p.cache, seq, p.layer, g, new_pos);
+    __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + row * 128;
+    reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
+  }
   for (int r0 = 0, round = 0; r0 < max(n, 1); r0 += kRoundRows, ++round) {
     const int rows = min(kRoundRows, n - r0);
     const int rows_pad = (rows + 15) & ~15;
     if (round == 0) {
-      // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45)
-      if (split == 0 && p.k_new && tid < 32) {
-        const int which = tid >> 4, ch = tid & 15;
-        const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128;
-        const int64_t row = cache_row(p.cache, seq, p.layer, g, new_pos);
-        __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + row * 128;
-        reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
-      }
-      resolve(r0, rows_pad, false);  // tail rows, new row, zero fill
+      __syncthreads();                // src_row of the pre pass consumed by every thread
+      resolve(r0, rows_pad, false);   // new row, not-yet-ready tail rows, zero fill
       __syncthreads();
       gather(r0, rows_pad, false);
     } else {
@@ -294,7 +324,7 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
     }
   }
   __syncthreads();
-  for (int i = tid; i < p.G * 128; i += DCfg::kThreads) {
+  for (int i = tid; i < n_out; i += DCfg::kThreads) {
     const int row = i >> 7, col = i & 127;
     float mstar = -INFINITY;
 #pragma unroll
@@ -317,48 +347,44 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
       part[1024 + 8 + row] = lsum;
     }
   }
-  // cluster-wide merge over DSMEM: CTA `split` finalises a slice of the G x 128 outputs
-  cluster_sync_all();
-  const uint32_t part_addr = smem_u32(part);
-  const int n_out = p.G * 128;
-  const int per = (n_out + CS - 1) / CS;
+  __syncthreads();
+
+  // push: partial slices -> their owners' inboxes, (m, l) -> every owner
+  cluster_wait_acquire();  // every owner's inbox barrier is initialised
+  if (tid == 0) {
+    const int my_vals = my_hi - my_lo;
+    mbar_arrive_expect_tx(inbox_bar, static_cast<uint32_t>(CS) * (my_vals + 16) * 4u);
+  }
+  const uint32_t inbox_addr = smem_u32(inbox), bar_addr = smem_u32(inbox_bar);
+  for (int q4 = tid; q4 < n_out / 4; q4 += DCfg::kThreads) {
+    const int e = q4 * 4, owner = e / per;
+    const float4 v = *reinterpret_cast<const float4*>(part + e);
+    st_async_v4(mapa_shared(inbox_addr + (split * rstride + (e - owner * per)) * 4, owner), v,
+                mapa_shared(bar_addr, owner));
+  }
+  for (int t = tid; t < CS * 4; t += DCfg::kThreads) {
+    const int owner = t >> 2, q = t & 3;
+    const float4 v = *reinterpret_cast<const float4*>(part + 1024 + 4 * q);  // m[0..7], l[0..7]
+    st_async_v4(mapa_shared(inbox_addr + (split * rstride + per + 4 * q) * 4, owner), v,
+                mapa_shared(bar_addr, owner));
+  }
+  // combine my slice once every sender's contribution has landed
+  mbar_wait_cluster(inbox_bar, 0);
   float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128;
-  float* wts = reinterpret_cast<float*>(smem + DCfg::kOffW);  // [s][16]: (m) then weight
-  float* lss = wts + DCfg::kMaxCS * 16;                      // [s][16]: l
-  if (tid < CS * p.G) {  // (m, l) of every (split, row) in one batch of remote loads
-    const int s2 = tid / p.G, row = tid % p.G;
-    const uint32_t base = mapa_shared(part_addr, s2);
-    wts[s2 * 16 + row] = ld_dsmem_f32(base + (1024 + row) * 4);
-    lss[s2 * 16 + row] = ld_dsmem_f32(base + (1024 + 8 + row) * 4);
-  }
-  __syncthreads();
-  if (tid < p.G) {  // merge weights w_s = 2^(m_s - m*) / L
+  for (int e = my_lo + tid; e < my_hi; e += DCfg::kThreads) {
+    const int row = e >> 7, off = e - my_lo;
     float mstar = -INFINITY;
-    for (int s2 = 0; s2 < CS; ++s2) mstar = fmaxf(mstar, wts[s2 * 16 + tid]);
-    float lsum = 0.f;
+    for (int s2 = 0; s2 < CS; ++s2) mstar = fmaxf(mstar, inbox[s2 * rstride + per + row]);
+    float acc = 0.f, lsum = 0.f;
     for (int s2 = 0; s2 < CS; ++s2) {
-      const float ms = wts[s2 * 16 + tid];
-      const float f = ms == -INFINITY ? 0.f : fast_exp2(ms - mstar);
-      wts[s2 * 16 + tid] = f;
-      lsum += lss[s2 * 16 + tid] * f;
+      const float ms = inbox[s2 * rstride + per + row];
+      if (ms == -INFINITY) continue;
+      const float f = fast_exp2(ms - mstar);
+      acc += inbox[s2 * rstride + off] * f;
+      lsum += inbox[s2 * rstride + per + 8 + row] * f;
     }
-    const float inv = 1.f / lsum;
-    for (int s2 = 0; s2 < CS; ++s2) wts[s2 * 16 + tid] *= inv;
+    out_unit[e] = acc / lsum;
   }
-  __syncthreads();
-  for (int e = split * per + tid; e < min(n_out, (split + 1) * per); e += DCfg::kThreads) {
-    const int row = e >> 7, col = e & 127;
-    float os[DCfg::kMaxCS];
-#pragma unroll
-    for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2)
-      os[s2] = s2 < CS ? ld_dsmem_f32(mapa_shared(part_addr, s2) + (row * 128 + col) * 4) : 0.f;
-    float acc = 0.f;
-#pragma unroll
-    for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2)
-      if (s2 < CS) acc += os[s2] * wts[s2 * 16 + row];
-    out_unit[row * 128 + col] = acc;
-  }
-  cluster_sync_all();  // keep every CTA's partial alive until all remote reads are done
   dtrace(p, 4);
 }
 

@@ -84,14 +84,29 @@ int mtiles_for(int G, int R) { return (G * R + 2 + 15) / 16; }
 }  // namespace
 
 // dev-only verify pipeline trace (SA_TRACE=1): [1024] per-tile events of CTA 0, then per layer
-// (mod 64) [1024 CTAs][4] = start, main-loop end, end (globaltimer ns), tiles | split << 32.
-constexpr size_t kVTraceWords = 1024 + 64 * 4096;
+// (mod 64) [1024 CTAs][8] = start, end, main-loop end, tiles | split << 32, last PV done,
+// partial stored, arrival counted, merge inputs landed (globaltimer ns).
+constexpr size_t kVTraceWords = 1024 + 64 * 8192;
 static unsigned long long* dev_verify_trace() {
   static unsigned long long* t = [] {
     unsigned long long* b = nullptr;
     if (getenv("SA_TRACE")) {
       cudaMalloc(&b, kVTraceWords * 8);
       cudaMemset(b, 0, kVTraceWords * 8);
+    }
+    return b;
+  }();
+  return t;
+}
+
+// dev-only draft trace (SA_TRACE=1): [(step-1) mod 8][layer mod 64][512 CTAs][8 phases] globaltimer ns.
+constexpr size_t kDTraceWords = static_cast<size_t>(8) * 64 * 512 * 8;
+static unsigned long long* dev_draft_trace() {
+  static unsigned long long* t = [] {
+    unsigned long long* b = nullptr;
+    if (getenv("SA_TRACE")) {
+      cudaMalloc(&b, kDTraceWords * 8);
+      cudaMemset(b, 0, kDTraceWords * 8);
     }
     return b;
   }();
@@ -115,7 +130,8 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   if (!(cfg->sparse_ratio > 0.0) || cfg->sparse_ratio > 1.0)
     return fail(SA_INVALID_ARGUMENT, "SelectorConfig: sparse_ratio must be in (0, 1]");  // selection.cpp:50-53
   if (cfg->k_min < 0) return fail(SA_INVALID_ARGUMENT, "SelectorConfig: k_min must be >= 0");
-  dev_verify_trace();  // dev trace buffer (SA_TRACE) allocated outside any graph capture
+  dev_verify_trace();  // dev trace buffers (SA_TRACE) allocated outside any graph capture
+  dev_draft_trace();
   auto* r = new sa_runner();
   r->cache = cache;
   r->cfg = *cfg;
@@ -399,27 +415,9 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.part_o = r->d_po;
   p.part_ml = r->d_pml;
   p.counters = r->d_cnt;
-  static unsigned long long* dtr = [] {
-    unsigned long long* t = nullptr;
-    if (getenv("SA_DTRACE")) {  // dev-only; allocated on first draft call (outside graph capture)
-      cudaMalloc(&t, 512 * 8 * 8);
-      cudaMemset(t, 0, 512 * 8 * 8);
-    }
-    return t;
-  }();
-  p.trace = dtr;
+  p.trace = dev_draft_trace();
   p.use_pdl = pdl ? 1 : 0;
   cudaError_t e = sa::launch_draft(p, s);
-  if (dtr && getenv("SA_DTRACE_DUMP")) {
-    cudaStreamSynchronize(s);
-    std::vector<unsigned long long> h(512 * 8);
-    cudaMemcpy(h.data(), dtr, h.size() * 8, cudaMemcpyDeviceToHost);
-    FILE* f = fopen(getenv("SA_DTRACE_DUMP"), "wb");
-    if (f) {
-      fwrite(h.data(), 8, h.size(), f);
-      fclose(f);
-    }
-  }
   if (e != cudaSuccess) return sa::cuda_fail(e, "draft launch");
   return SA_OK;
 }
@@ -429,8 +427,10 @@ SA_API int sa_dev_trace_dump(const char* path) {
   unsigned long long* t = dev_verify_trace();
   if (!t || !path) return -1;
   if (cudaDeviceSynchronize() != cudaSuccess) return -2;
-  std::vector<unsigned long long> h(kVTraceWords);
-  if (cudaMemcpy(h.data(), t, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -3;
+  std::vector<unsigned long long> h(kVTraceWords + kDTraceWords);
+  if (cudaMemcpy(h.data(), t, kVTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -3;
+  if (cudaMemcpy(h.data() + kVTraceWords, dev_draft_trace(), kDTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -3;
   FILE* f = fopen(path, "wb");
   if (!f) return -4;
   fwrite(h.data(), 8, h.size(), f);

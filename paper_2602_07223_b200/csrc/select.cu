@@ -194,20 +194,81 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
   }
   // Selected: (key >> shift) > T, plus the `rem` lowest-index keys with (key >> shift) == T; never
   // a -inf key (selection.cpp:153).  k == 0 selects nothing.
-  const long long take_eq = rem;
+  const long long take_eq_ll = rem;
 
-  // ---- output: warp w owns [w*R, min(n, (w+1)*R)), R a multiple of 32
-  const int R = ((n + kSelWarps * 32 - 1) / (kSelWarps * 32)) * 32;
-  const int w_lo = warp * R, w_hi = min(n, w_lo + R);
-  int gt = 0, eq = 0;
-  for (int base = w_lo; base < w_hi; base += 32) {
-    const int i = base + lane;
-    const uint32_t u = i < w_hi ? keys[i] : 0u;
-    const uint32_t d = u >> shift;
-    const bool ok = i < w_hi && u != kKeyNegInf;
-    gt += __popc(__ballot_sync(0xffffffffu, ok && d > T));
-    eq += __popc(__ballot_sync(0xffffffffu, ok && d == T));
+  // ---- output, common case: every key of the threshold bin is taken (no tie straddles the
+  // boundary), so the selection is the predicate (key >> shift) >= T: ballot stream compaction,
+  // warp w owning the contiguous range [w*R1, (w+1)*R1), 32 keys per step.
+  if (static_cast<long long>(sh.bin_count) == take_eq_ll) {
+    const int R1 = ((n + kSelThreads - 1) / kSelThreads) * 32;
+    const int lo = warp * R1, hi = min(n, lo + R1);
+    int cnt = 0;
+    for (int base = lo; base < hi; base += 32) {
+      const int i = base + lane;
+      const uint32_t u = i < hi ? keys[i] : kKeyNegInf;
+      cnt += __popc(__ballot_sync(0xffffffffu, u != kKeyNegInf && (u >> shift) >= T));
+    }
+    if (lane == 0) sh.wgt[warp] = cnt;
+    __syncthreads();
+    if (warp == 0) {
+      const int c = sh.wgt[lane];
+      int ci = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, ci, off);
+        if (lane >= off) ci += t;
+      }
+      sh.wgt[lane] = ci - c;
+      if (lane == 31) p.k_out[b * p.n_sets + set] = ci;
+    }
+    __syncthreads();
+    int32_t* out = p.idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
+    int run = sh.wgt[warp];
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = lo; base < hi; base += 32) {
+      const int i = base + lane;
+      const uint32_t u = i < hi ? keys[i] : kKeyNegInf;
+      const bool sel = u != kKeyNegInf && (u >> shift) >= T;
+      const unsigned bs = __ballot_sync(0xffffffffu, sel);
+      if (sel) out[run + __popc(bs & lt)] = i;
+      run += __popc(bs);
+    }
+    return;
   }
+
+  // ---- output, general case (ties straddle the boundary: the lowest-index equal keys win):
+  // warp w owns [w*R, min(n, (w+1)*R)), R a multiple of 128; lane l takes keys
+  // [base + 4l, base + 4l + 4) of each 128-key step, so (lane, element) order is index order.
+  const int R = ((n + kSelWarps * 128 - 1) / (kSelWarps * 128)) * 128;
+  const int w_lo = warp * R, w_hi = min(n, w_lo + R);
+  const int take_eq = static_cast<int>(take_eq_ll);
+  auto classify = [&](int i0, int& cg, int& ce, uint32_t (&u)[4]) {
+    if (i0 + 3 < w_hi) {
+      const uint4 v = reinterpret_cast<const uint4*>(keys)[i0 >> 2];
+      u[0] = v.x, u[1] = v.y, u[2] = v.z, u[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) u[e] = i0 + e < w_hi ? keys[i0 + e] : kKeyNegInf;
+    }
+    cg = ce = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t d = u[e] >> shift;
+      const bool ok = u[e] != kKeyNegInf;
+      cg += ok && d > T;
+      ce += ok && d == T;
+    }
+  };
+  int gt = 0, eq = 0;
+  for (int base = w_lo; base < w_hi; base += 128) {
+    uint32_t u[4];
+    int cg, ce;
+    classify(base + 4 * lane, cg, ce, u);
+    gt += cg;
+    eq += ce;
+  }
+  gt = __reduce_add_sync(0xffffffffu, gt);
+  eq = __reduce_add_sync(0xffffffffu, eq);
   if (lane == 0) {
     sh.wgt[warp] = gt;
     sh.weq[warp] = eq;
@@ -226,29 +287,39 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
     }
     sh.wgt[lane] = gi - g;
     sh.weq[lane] = ei - e;
-    if (lane == 31) {
-      const long long tot = gi + min(static_cast<long long>(ei), take_eq);
-      p.k_out[b * p.n_sets + set] = static_cast<int>(tot);
-    }
+    if (lane == 31) p.k_out[b * p.n_sets + set] = gi + min(ei, take_eq);
   }
   __syncthreads();
   int32_t* out = p.idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
   int gt_run = sh.wgt[warp], eq_run = sh.weq[warp];
-  const unsigned lt = (1u << lane) - 1u;
-  for (int base = w_lo; base < w_hi; base += 32) {
-    const int i = base + lane;
-    const uint32_t u = i < w_hi ? keys[i] : 0u;
-    const uint32_t d = u >> shift;
-    const bool ok = i < w_hi && u != kKeyNegInf;
-    const bool is_gt = ok && d > T, is_eq = ok && d == T;
-    const unsigned bg = __ballot_sync(0xffffffffu, is_gt), be = __ballot_sync(0xffffffffu, is_eq);
-    const int eq_rank = eq_run + __popc(be & lt);
-    const bool sel = is_gt || (is_eq && eq_rank < take_eq);
-    // selected before this key = gt before + min(eq before, take_eq)
-    const long long before = gt_run + __popc(bg & lt) + min(static_cast<long long>(eq_rank), take_eq);
-    if (sel) out[before] = i;
-    gt_run += __popc(bg);
-    eq_run += __popc(be);
+  for (int base = w_lo; base < w_hi; base += 128) {
+    const int i0 = base + 4 * lane;
+    uint32_t u[4];
+    int cg, ce;
+    classify(i0, cg, ce, u);
+    // warp-exclusive scan of the packed (gt | eq << 16) counts
+    const int packed = cg | (ce << 16);
+    int incl = packed;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += t;
+    }
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - packed;
+    int g_before = gt_run + (excl & 0xFFFF), e_before = eq_run + (excl >> 16);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t d = u[e] >> shift;
+      const bool ok = u[e] != kKeyNegInf;
+      const bool is_gt = ok && d > T, is_eq = ok && d == T;
+      // selected before this key = gt before + min(eq before, take_eq)
+      if (is_gt || (is_eq && e_before < take_eq)) out[g_before + min(e_before, take_eq)] = i0 + e;
+      g_before += is_gt;
+      e_before += is_eq;
+    }
+    gt_run += tot & 0xFFFF;
+    eq_run += tot >> 16;
   }
 }
 

@@ -80,6 +80,16 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
     for (int m = 0; m < N; ++m) x[m] += __shfl_xor_sync(0xffffffffu, x[m], off);
 }
 
+// dev-only per-CTA phase timestamps (globaltimer ns): slot k of CTA `cta_lin` in layer p.layer
+#define SA_TSTAMP(k)                                                                            \
+  do {                                                                                          \
+    if (p.trace && cta_lin < 1024) {                                                            \
+      unsigned long long gt_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                                   \
+      p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + (k)] = gt_;                          \
+    }                                                                                           \
+  } while (0)
+
 // dev-only pipeline trace: ev[e][t] = clock64 of event e at tile t for CTA (0,0,0)
 #define SA_TRACE(e, t)                                                                          \
   do {                                                                                          \
@@ -179,7 +189,7 @@ __global__ void __launch_bounds__(384, 1)
   if (p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin] = gt;
+    p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin] = gt;
   }
   const uint32_t tmem = *tmem_slot;
 
@@ -195,10 +205,14 @@ __global__ void __launch_bounds__(384, 1)
       const uint64_t pol = policy_evict_first();
       // tile stream of this CTA: window tiles (last split), then its chunks; pring holds positions
       int q_end = 0, cur_chunk = -1, cur_tile = 0, claims = 0;
-      bool exhausted = false, done = false, dep_seen = false;
+      bool exhausted = false, done = false, dep_seen = false, win_added = false;
       auto fill = [&](int upto) {
         while (q_end < upto && !exhausted) {
           if (cur_chunk < 0 || cur_tile == min(C::kChunkTiles, n_pref - cur_chunk * C::kChunkTiles)) {
+            if (last && claims == 1 && !win_added) {  // window tiles go right after the first chunk
+              for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 15] = win_lo + w2 * C::kTile;
+              win_added = true;
+            }
             cur_chunk = claims++ == 0 ? split : p.n_splits + atomicAdd(p.chunk_ctr + unit, 1);
             if (cur_chunk >= n_chunks) {
               exhausted = true;
@@ -208,8 +222,8 @@ __global__ void __launch_bounds__(384, 1)
           }
           pring[q_end++ & 15] = (cur_chunk * C::kChunkTiles + cur_tile++) * C::kTile;
         }
-        if (exhausted && !done) {  // the last split's window tiles close its stream
-          if (last)
+        if (exhausted && !done) {  // (short prefixes: the window tiles close the stream)
+          if (last && !win_added)
             for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 15] = win_lo + w2 * C::kTile;
           done = true;
         }
@@ -514,8 +528,8 @@ __global__ void __launch_bounds__(384, 1)
     if (p.trace && ts == 0 && wg == 0 && cta_lin < 1024) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin + 2] = gt;  // main loop done
-      p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin + 3] = static_cast<unsigned long long>(i) | (static_cast<unsigned long long>(split) << 32);
+      p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + 2] = gt;  // main loop done
+      p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + 3] = static_cast<unsigned long long>(i) | (static_cast<unsigned long long>(split) << 32);
     }
     const int my_tiles = i;  // tiles this warpgroup processed
     if (ts == 0) ntiles_wg[wg] = my_tiles;
@@ -523,6 +537,7 @@ __global__ void __launch_bounds__(384, 1)
       mbar_wait(&pv_done[wg], (my_tiles - 1) & 1);
       tc_fence_after();
     }
+    if (wg == 0 && ts == 0) SA_TSTAMP(4);
     warp_allreduce_sum<N>(l);
     if (lane == 0) {
 #pragma unroll
@@ -587,8 +602,11 @@ __global__ void __launch_bounds__(384, 1)
       // arrival: one fence + one atomic per CTA after the CTA-wide barrier (cumulativity)
       named_bar_sync(1, 256);
       if (wg == 0 && ts == 0) {
-        __threadfence();
-        *flag = atomicAdd(p.counters + unit, 1);
+        SA_TSTAMP(5);
+        int old;  // release: this CTA's partial stores (ordered by the barrier) before the count
+        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + unit) : "memory");
+        *flag = old;
+        SA_TSTAMP(6);
       }
       named_bar_sync(1, 256);
       if (*flag == p.n_splits - 1) {
@@ -598,14 +616,14 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t mlbytes = static_cast<uint32_t>(p.n_splits) * N * 8u;
         if (static_cast<size_t>(p.n_splits) * obytes + mlbytes <= static_cast<size_t>(C::kOffBar)) {
           if (wg == 0 && ts == 0) {
-            __threadfence();
-            fence_proxy_async();  // generic writes of the other CTAs -> async-proxy reads
+            fence_proxy_async();  // generic writes of the other CTAs (acquired above) -> async-proxy reads
             mbar_expect_tx(merge_bar, p.n_splits * obytes + mlbytes);
             for (int s2 = 0; s2 < p.n_splits; ++s2)
               bulk_load(smem + s2 * obytes, po + static_cast<size_t>(s2) * N * 128, obytes, merge_bar);
             bulk_load(smem + p.n_splits * obytes, pml, mlbytes, merge_bar);
           }
           mbar_wait(merge_bar, 0);
+          if (wg == 0 && ts == 0) SA_TSTAMP(7);
           const float4* so = reinterpret_cast<const float4*>(smem);
           float2* sml = reinterpret_cast<float2*>(smem + p.n_splits * obytes);  // [split][N] (m, l)
           const int t256 = wg * 128 + ts;
@@ -651,7 +669,7 @@ __global__ void __launch_bounds__(384, 1)
   if (p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[1024 + (p.layer & 63) * 4096 + 4 * cta_lin + 1] = gt;
+    p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + 1] = gt;
   }
   if (warp == 1) {
     tc_fence_after();

@@ -59,3 +59,32 @@ def test_cubin_is_sm100a():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def _build_mirror_test(tmp_path):
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2602_07223_b200", "lib")
+    exe = str(tmp_path / "test_mirror")
+    cmd = ["g++", "-std=c++17", "-O1", "-I" + os.path.join(root, "include"), "-I/usr/local/cuda/include",
+           os.path.join(root, "tests", "cpp", "test_mirror.cpp"), "-o", exe, "-L" + libdir, "-lspecattn_b200",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + libdir, "-Wl,-rpath,/usr/local/cuda/lib64"]
+    subprocess.run(cmd, check=True)
+    return exe
+
+
+def test_cpp_host_mirror_cpu(tmp_path):
+    """include/specattn_b200.hpp: reference-shaped C++ calls rethrow the reference exception types."""
+    import subprocess
+    out = subprocess.run([_build_mirror_test(tmp_path), "cpu"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert "mirror cpu ok" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_host_mirror_gpu(tmp_path):
+    """KvStore append / truncate / gather / length_error through the C++ mirror on the device."""
+    import subprocess
+    out = subprocess.run([_build_mirror_test(tmp_path), "gpu"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert "mirror gpu ok" in out.stdout

@@ -327,3 +327,47 @@ def test_iteration_parity(cuda, ref, strategy, mode, use_graph):
         for layer in range(L):
             o_ref = kv.draft_layer(layer, Hq, qd[j - 1, layer, 0], sets_by_layer[layer], p0, j, SCALE, threads=8)
             assert rel_err_rows(od[j - 1, layer, 0], o_ref) < 2e-4, (j, layer)
+
+
+# ----------------------------------------------------------------------------------- sharding
+
+def test_head_sharded_layer_scores_sum_exactly(cuda):
+    """KV-head sharding with real kernels on one GPU: two half-head caches (the two
+    ranks' shards) produce per-layer fixed-point sums whose integer sum is bit-identical to the
+    full cache's, and selecting on the exchanged sums gives the full cache's selection exactly."""
+    torch = cuda
+    from paper_2602_07223_b200 import Cache, Runner
+    L, Hkv, G, R, p0 = 1, 4, 4, 5, 2500
+    Hq = Hkv * G
+    K = normal_bf16(95, 1, (p0, L * Hkv, D))
+    V = normal_bf16(95, 2, (p0, L * Hkv, D))
+    q = normal_bf16(95, 3, (1, Hq, R, D))
+    kn, vn = normal_bf16(95, 4, (1, R, Hkv, D)), normal_bf16(95, 5, (1, R, Hkv, D))
+
+    def run(heads):
+        c = Cache(L, len(heads), D, p0 + 64, page_size=128)
+        c.append(torch.from_numpy(np.ascontiguousarray(K[:, heads])).cuda(),
+                 torch.from_numpy(np.ascontiguousarray(V[:, heads])).cuda())
+        r = Runner(c, len(heads) * G, max_rows=R, max_prefix=p0)
+        r.set_batch([0], [p0])
+        qh = np.ascontiguousarray(q[:, heads[0] * G:(heads[-1] + 1) * G])
+        out = torch.zeros((1, len(heads) * G, R, D), dtype=torch.float32, device="cuda")
+        r.verify(0, to_dev_bf16(qh), out, to_dev_bf16(np.ascontiguousarray(kn[:, :, heads])),
+                 to_dev_bf16(np.ascontiguousarray(vn[:, :, heads])), SCALE)
+        torch.cuda.synchronize()
+        return c, r
+
+    full = run([0, 1, 2, 3])
+    a, b = run([0, 1]), run([2, 3])
+    fx_full = full[1].layer_scores(0)
+    fx_a, fx_b = a[1].layer_scores(0), b[1].layer_scores(0)
+    assert np.array_equal(fx_full, fx_a + fx_b)
+    # the exchange (what shard.exchange_layer_scores' all-reduce does), in place on shard a's buffer
+    ta = a[1].layer_scores_tensor(0)
+    ta += torch.from_numpy(fx_b).cuda()
+    torch.cuda.synchronize()
+    full[1].select(0)
+    a[1].select(0)
+    i_full, c_full = full[1].selection(0, 1)
+    i_a, c_a = a[1].selection(0, 1)
+    assert c_full[0, 0] == c_a[0, 0] and np.array_equal(i_full[0, 0, :c_full[0, 0]], i_a[0, 0, :c_a[0, 0]])

@@ -1,4 +1,8 @@
-"""Dev tool: per-CTA phase timestamps of one draft launch (config-2 shapes)."""
+"""Dev tool: draft-phase CTA timeline inside the config-2 iteration graph (SA_TRACE=1).
+  SA_ITER_SKIP=3 python tools/trace_draft.py     # drafts only (selections from an earlier run)
+Per draft launch (step, layer): first CTA start, median start, median 'loaded' (after the PDL wait),
+median 'computed', max end (us relative to the first draft start)."""
+import ctypes
 import math
 import os
 import sys
@@ -10,34 +14,71 @@ sys.path.insert(0, ROOT)
 os.environ["SA_TRACE"] = "1"
 import torch  # noqa: E402
 
-from paper_2602_07223_b200 import Cache, Runner  # noqa: E402
+from paper_2602_07223_b200 import COLLECT2, Cache, Runner  # noqa: E402
+from paper_2602_07223_b200._lib import lib  # noqa: E402
 
-L, Hq, Hkv, p0, R, D = 2, 32, 8, 32768, 5, 128
-cache = Cache(L, Hkv, D, p0 + 64)
-for s in range(0, p0, 4096):
-    kk = torch.randn((4096, L * Hkv, D), device="cuda").to(torch.bfloat16)
+L = int(os.environ.get("LAYERS", 32))
+Hq, Hkv, p0, gamma, D = 32, 8, int(os.environ.get("CTX", 32768)), 4, 128
+R = gamma + 1
+cache = Cache(L, Hkv, D, p0 + R + 64, page_size=256)
+for s in range(0, p0, 2048):
+    kk = torch.randn((2048, L * Hkv, D), device="cuda").to(torch.bfloat16)
     cache.append(kk, kk)
 r = Runner(cache, Hq, max_rows=R, max_prefix=p0)
 r.set_batch([0], [p0])
-q = torch.randn((1, Hq, R, D), device="cuda").to(torch.bfloat16)
-kn = torch.randn((1, R, Hkv, D), device="cuda").to(torch.bfloat16)
-out = torch.empty((1, Hq, R, D), device="cuda")
-for l in range(L):
-    r.verify(l, q, out, kn, kn, 1 / math.sqrt(D))
+
+
+def rnd(*s):
+    return torch.randn(s, device="cuda").to(torch.bfloat16)
+
+
+qv, kvn, vvn = rnd(L, 1, Hq, R, D), rnd(L, 1, R, Hkv, D), rnd(L, 1, R, Hkv, D)
+qd, kdn, vdn = rnd(gamma, L, 1, Hq, D), rnd(gamma, L, 1, Hkv, D), rnd(gamma, L, 1, Hkv, D)
+out_v = torch.empty((L, 1, Hq, R, D), device="cuda")
+out_d = torch.empty((gamma, L, 1, Hq, D), device="cuda")
+for l in range(L):  # selections for every layer (the drafts-only graph reuses them)
+    r.verify(l, qv[l], out_v[l], kvn[l], vvn[l])
     r.select(l)
-qd = torch.randn((1, Hq, D), device="cuda").to(torch.bfloat16)
-od = torch.empty((1, Hq, D), device="cuda")
-for it in range(4):
-    if it == 3:
-        os.environ["SA_DTRACE_DUMP"] = os.path.join(ROOT, "gpurun_out", "dtrace.bin")
-    r.draft(it % L, 2, qd, od, kn[:, 0].contiguous(), kn[:, 0].contiguous())
+st = torch.cuda.Stream()
+args = r.iteration_args(gamma, qv, kvn, vvn, qd, kdn, vdn, out_v, out_d, strategy=COLLECT2, mode=0,
+                        scale=1 / math.sqrt(D), use_graph=True)
+with torch.cuda.stream(st):
+    for _ in range(4):
+        r.iteration(args, stream=st)
 torch.cuda.synchronize()
-tr = np.fromfile(os.path.join(ROOT, "gpurun_out", "dtrace.bin"), dtype=np.uint64).astype(np.int64).reshape(512, 8)
-tr = tr[tr[:, 0] > 0]
-g0 = tr[:, 0].min()
-ph = ["start", "loaded", "computed", "partial", "end"]
-print("CTAs", len(tr))
-for i, name in enumerate(ph):
-    v = (tr[:, i] - g0) / 1e3
-    v = v[tr[:, i] > 0]
-    print(f"{name:10s} min {v.min():7.2f} med {np.median(v):7.2f} max {v.max():7.2f} us")
+path = os.path.join(ROOT, "gpurun_out", "trace_draft.bin")
+f = lib().sa_dev_trace_dump
+f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
+assert f(path.encode()) == 0
+raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
+dr = raw[1024 + 64 * 8192:].reshape(8, 64, 512, 8)
+t0 = None
+prev = None
+print(f"{'step':>4s} {'layer':>5s} {'start':>7s} {'st_max':>7s} | after wait med/max | gathered med/max | computed med/max | end med/max | dt")
+for j in range(gamma):
+    for l in range(L):
+        blk = dr[j, l]
+        blk = blk[blk[:, 0] > 0]
+        if not len(blk):
+            continue
+        if t0 is None:
+            t0 = blk[:, 0].min()
+        v = lambda k: (blk[:, k] - t0) / 1e3  # noqa: E731
+        s0, en = v(0), v(4)
+        dt = 0.0 if prev is None else en.max() - prev
+        prev = en.max()
+        if l < 3 or l == L - 1:
+            print(f"{j + 1:4d} {l:5d} {s0.min():7.2f} {s0.max():7.2f} | {np.median(v(1)):7.2f} {v(1).max():7.2f} | "
+                  f"{np.median(v(2)):7.2f} {v(2).max():7.2f} | {np.median(v(3)):7.2f} {v(3).max():7.2f} | "
+                  f"{np.median(en):7.2f} {en.max():7.2f} | {dt:5.2f}")
+
+# verify phase on the same clock (globaltimer): last layer's end vs the first draft's start
+vt = raw[1024:1024 + 64 * 8192].reshape(64, 1024, 8)
+v_st = [vt[l][vt[l][:, 0] > 0][:, 0].min() for l in range(L) if (vt[l][:, 0] > 0).any()]
+v_en = [vt[l][vt[l][:, 0] > 0][:, 1].max() for l in range(L) if (vt[l][:, 0] > 0).any()]
+if v_st:
+    d_first = dr[0, 0][dr[0, 0][:, 0] > 0][:, 0].min()
+    d_last = max(dr[gamma - 1, l][dr[gamma - 1, l][:, 4] > 0][:, 4].max() for l in range(L) if (dr[gamma - 1, l][:, 4] > 0).any())
+    print(f"verify layer0 start -> last verify end {(max(v_en) - min(v_st)) / 1e3:.1f} us; last verify end -> first "
+          f"draft start {(d_first - max(v_en)) / 1e3:.1f} us; drafts {(d_last - d_first) / 1e3:.1f} us; "
+          f"total {(d_last - min(v_st)) / 1e3:.1f} us")

@@ -51,10 +51,10 @@ f.argtypes = [ctypes.c_char_p]
 assert f(path.encode()) == 0
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 t0 = None
-print(f"{'layer':>5s} {'start':>8s} {'loop_med':>8s} {'loop_max':>8s} {'end_med':>8s} {'end_max':>8s} {'dt':>7s}")
+print(f"{'layer':>5s} {'start':>8s} {'st_med':>8s} {'loop_med':>8s} {'loop_max':>8s} {'end_med':>8s} {'end_max':>8s} {'dt':>7s}")
 prev = None
 for l in range(min(L, 64)):
-    blk = raw[1024 + l * 4096: 1024 + (l + 1) * 4096].reshape(1024, 4)
+    blk = raw[1024 + l * 8192: 1024 + (l + 1) * 8192].reshape(1024, 8)
     blk = blk[blk[:, 0] > 0]
     if not len(blk):
         continue
@@ -63,4 +63,4 @@ for l in range(min(L, 64)):
     s0, ml, en = (blk[:, 0] - t0) / 1e3, (blk[:, 2] - t0) / 1e3, (blk[:, 1] - t0) / 1e3
     dt = s0.min() - prev if prev is not None else 0.0
     prev = s0.min()
-    print(f"{l:5d} {s0.min():8.2f} {np.median(ml):8.2f} {ml.max():8.2f} {np.median(en):8.2f} {en.max():8.2f} {dt:7.2f}")
+    print(f"{l:5d} {s0.min():8.2f} {np.median(s0):8.2f} {np.median(ml):8.2f} {ml.max():8.2f} {np.median(en):8.2f} {en.max():8.2f} {dt:7.2f}")

@@ -36,15 +36,24 @@ f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
 assert f(dump.encode()) == 0
 raw = np.fromfile(dump, dtype=np.uint64).astype(np.int64)
 ev = raw[:1024].reshape(16, 64)
-se4 = raw[1024:1024 + 4096].reshape(1024, 4)
-se4 = se4[se4[:, 0] > 0]
-g0 = se4[:, 0].min()
-st, en, ml = (se4[:, 0] - g0) / 1e3, (se4[:, 1] - g0) / 1e3, (se4[:, 2] - g0) / 1e3
-tiles, split = se4[:, 3] & 0xFFFFFFFF, se4[:, 3] >> 32
-print(f"CTAs {len(se4)}: start us min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f}; "
+se = raw[1024:1024 + 8192].reshape(1024, 8)
+se = se[se[:, 0] > 0]
+g0 = se[:, 0].min()
+rel = lambda k: (se[:, k] - g0) / 1e3  # noqa: E731
+st, en, ml, pv, sto, cnt, mrg = rel(0), rel(1), rel(2), rel(4), rel(5), rel(6), rel(7)
+tiles, split = se[:, 3] & 0xFFFFFFFF, se[:, 3] >> 32
+print(f"CTAs {len(se)}: start us min/med/max {st.min():.2f}/{np.median(st):.2f}/{st.max():.2f}; "
       f"main-loop end min/med/max {ml.min():.2f}/{np.median(ml):.2f}/{ml.max():.2f}; "
       f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f}")
-order = np.argsort(en)[-10:]
+has = se[:, 5] > 0
+print(f"epilogue medians (us): loop_end->pv_done {np.median(pv - ml):.2f}  pv_done->partial_stored "
+      f"{np.median((sto - pv)[has]):.2f}  stored->counted {np.median((cnt - sto)[has]):.2f}  counted->end(non-merger) "
+      f"{np.median((en - cnt)[has]):.2f}")
+mg = se[:, 7] > 0
+if mg.any():
+    print(f"mergers {mg.sum()}: counted->inputs_landed med {np.median((mrg - cnt)[mg]):.2f}  landed->end med "
+          f"{np.median((en - mrg)[mg]):.2f}  merger end max {en[mg].max():.2f}")
+order = np.argsort(en)[-8:]
 print("slowest CTAs (lin, split, wg0 tiles, start, loop_end, end):",
       [(int(i), int(split[i]), int(tiles[i]), round(float(st[i]), 2), round(float(ml[i]), 2), round(float(en[i]), 2)) for i in order])
 print("wg0 tiles per CTA: min/med/max", tiles.min(), np.median(tiles), tiles.max())
