@@ -15,6 +15,8 @@
 // the previous layer's kernel; the query, the tail rows and this step's new row (which a real model
 // produces in the previous layer) are read after it.
 #include "attn_core.cuh"
+#include <algorithm>
+
 #include "internal.h"
 
 namespace sa {
@@ -47,28 +49,44 @@ struct DraftWarp {
     }
   }
 
-  // tokens [r0, r0+16) of the swizzled K/V tiles; valid(i) masks token i of the sub-block
-  __device__ __forceinline__ void step(uint32_t k_smem, uint32_t v_smem, uint32_t half, int r0, int lane,
-                                       float c, int n_valid) {
-    const int gid = lane >> 2, t4 = lane & 3, mi = lane >> 3;
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
-    {
-      const int tok = r0 + (mi & 1) * 8 + (lane & 7);
+  // NB sub-blocks of 16 tokens each (sub-block i: tokens [r0[i], r0[i]+16) of the swizzled K/V tile
+  // at k_smem[i] / v_smem[i], the first n_valid[i] valid) in ONE online-softmax step: the QK^T
+  // chains of the sub-blocks are independent (ILP), one row-max reduction and one rescale cover them.
+  template <int NB>
+  __device__ __forceinline__ void step(const uint32_t (&k_smem)[NB], const uint32_t (&v_smem)[NB], uint32_t half,
+                                       const int (&r0)[NB], int lane, float c, const int (&n_valid)[NB]) {
+    const int gid = lane >> 2, mi = lane >> 3;
+    float s[NB][4];
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        uint32_t a[4];
-        ldsm_x4(k_smem + swz(tok, 2 * kk + (mi >> 1), half), a[0], a[1], a[2], a[3]);
-        mma_bf16(s, a, qb[kk][0], qb[kk][1]);
+    for (int bi = 0; bi < NB; ++bi) {
+      const int tok = r0[bi] + (mi & 1) * 8 + (lane & 7);
+      float s2[4] = {0.f, 0.f, 0.f, 0.f};  // two accumulator chains halve the dependent mma depth
+      s[bi][0] = s[bi][1] = s[bi][2] = s[bi][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 2) {
+        uint32_t a[4], a2[4];
+        ldsm_x4(k_smem[bi] + swz(tok, 2 * kk + (mi >> 1), half), a[0], a[1], a[2], a[3]);
+        ldsm_x4(k_smem[bi] + swz(tok, 2 * (kk + 1) + (mi >> 1), half), a2[0], a2[1], a2[2], a2[3]);
+        mma_bf16(s[bi], a, qb[kk][0], qb[kk][1]);
+        mma_bf16(s2, a2, qb[kk + 1][0], qb[kk + 1][1]);
       }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[bi][i] += s2[i];
+      if (gid >= n_valid[bi]) s[bi][0] = s[bi][1] = -INFINITY;
+      if (gid + 8 >= n_valid[bi]) s[bi][2] = s[bi][3] = -INFINITY;
     }
-    if (gid >= n_valid) s[0] = s[1] = -INFINITY;
-    if (gid + 8 >= n_valid) s[2] = s[3] = -INFINITY;
-    // per query row (2t4 + e): max over the 16 tokens (2 in-thread, 8 gid lanes)
-    float tmax[2] = {fmaxf(s[0], s[2]), fmaxf(s[1], s[3])};
+    // per query row (2t4 + e): max over the NB x 16 tokens (in-thread, then 8 gid lanes)
+    float tmax[2] = {fmaxf(s[0][0], s[0][2]), fmaxf(s[0][1], s[0][3])};
 #pragma unroll
-    for (int e = 0; e < 2; ++e)
+    for (int bi = 1; bi < NB; ++bi) {
+      tmax[0] = fmaxf(tmax[0], fmaxf(s[bi][0], s[bi][2]));
+      tmax[1] = fmaxf(tmax[1], fmaxf(s[bi][1], s[bi][3]));
+    }
 #pragma unroll
-      for (int off = 4; off < 32; off <<= 1) tmax[e] = fmaxf(tmax[e], __shfl_xor_sync(0xffffffffu, tmax[e], off));
+    for (int off = 4; off < 32; off <<= 1) {
+      tmax[0] = fmaxf(tmax[0], __shfl_xor_sync(0xffffffffu, tmax[0], off));
+      tmax[1] = fmaxf(tmax[1], __shfl_xor_sync(0xffffffffu, tmax[1], off));
+    }
     float mnew[2];
     bool grow = false;
 #pragma unroll
@@ -90,28 +108,26 @@ struct DraftWarp {
       }
     }
     const float b0 = m[0] == -INFINITY ? 0.f : m[0], b1 = m[1] == -INFINITY ? 0.f : m[1];
-    const float p0 = fast_exp2(fmaf(s[0], c, -b0)), p1 = fast_exp2(fmaf(s[1], c, -b1));
-    const float p2 = fast_exp2(fmaf(s[2], c, -b0)), p3 = fast_exp2(fmaf(s[3], c, -b1));
-    l[0] += p0 + p2;
-    l[1] += p1 + p3;
-    uint32_t h01, l01, h23, l23;
-    split_bf16(p0, p1, h01, l01);  // token gid,   rows 2t4, 2t4+1
-    split_bf16(p2, p3, h23, l23);  // token gid+8
-    // B fragments of P^T (k = tokens, n = rows): 8x8 transposes of the two token halves
-    const uint32_t bh0 = movmatrix_trans(h01), bh1 = movmatrix_trans(h23);
-    const uint32_t bl0 = movmatrix_trans(l01), bl1 = movmatrix_trans(l23);
-    const int tok = r0 + (mi >> 1) * 8 + (lane & 7);
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      uint32_t a[4];
-      ldsm_x4_t(v_smem + swz(tok, 2 * jj + (mi & 1), half), a[0], a[1], a[2], a[3]);
-      mma_bf16(o[jj], a, bh0, bh1);
-    }
+    for (int bi = 0; bi < NB; ++bi) {
+      const float p0 = fast_exp2(fmaf(s[bi][0], c, -b0)), p1 = fast_exp2(fmaf(s[bi][1], c, -b1));
+      const float p2 = fast_exp2(fmaf(s[bi][2], c, -b0)), p3 = fast_exp2(fmaf(s[bi][3], c, -b1));
+      l[0] += p0 + p2;
+      l[1] += p1 + p3;
+      uint32_t h01, l01, h23, l23;
+      split_bf16(p0, p1, h01, l01);  // token gid,   rows 2t4, 2t4+1
+      split_bf16(p2, p3, h23, l23);  // token gid+8
+      // B fragments of P^T (k = tokens, n = rows): 8x8 transposes of the two token halves
+      const uint32_t bh0 = movmatrix_trans(h01), bh1 = movmatrix_trans(h23);
+      const uint32_t bl0 = movmatrix_trans(l01), bl1 = movmatrix_trans(l23);
+      const int tok = r0[bi] + (mi >> 1) * 8 + (lane & 7);
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      uint32_t a[4];
-      ldsm_x4_t(v_smem + swz(tok, 2 * jj + (mi & 1), half), a[0], a[1], a[2], a[3]);
-      mma_bf16(o[jj], a, bl0, bl1);
+      for (int jj = 0; jj < 8; ++jj) {  // one V fragment load serves the hi and lo P planes
+        uint32_t a[4];
+        ldsm_x4_t(v_smem[bi] + swz(tok, 2 * jj + (mi & 1), half), a[0], a[1], a[2], a[3]);
+        mma_bf16(o[jj], a, bh0, bh1);
+        mma_bf16(o[jj], a, bl0, bl1);
+      }
     }
   }
 
@@ -126,8 +142,8 @@ struct DraftWarp {
 struct DCfg {
   static constexpr int kTile = 64;
   static constexpr int kMaxTiles = 3;   // resident tiles per round (192 keys)
-  static constexpr int kThreads = 256;
-  static constexpr int kWarps = kThreads / 32;
+  static constexpr int kMaxThreads = 256;  // 8 warps (two CTAs per SM: <= 128 registers per thread)
+  static constexpr int kMaxWarps = kMaxThreads / 32;
   static constexpr int kMaxCS = 16;
   static constexpr int kHalf = kTile * 128;
   static constexpr int kTileBytes = 2 * kHalf;
@@ -142,8 +158,8 @@ struct DCfg {
                                                                                   : kRecvFloats * 4;
   static constexpr int kOffBar = kOffRecv + kRecvBytes;
   static constexpr int kSmem = kOffBar + 16 + 1024;
-  static constexpr int kWarpPart = 8 * 128 + 16;     // per-warp partial, same layout
-  static_assert(kWarps * kWarpPart * 4 <= kOffPart, "warp partials must fit in the tile buffers");
+  static_assert(kMaxWarps * 8 * 128 * 4 <= kOffPart, "warp partials must fit in the tile buffers");
+  static_assert(kMaxTiles * kTile * 8 >= kMaxWarps * 16 * 4, "warp (m, l) table fits the row-source area");
   static_assert(kSmem <= 113 * 1024, "two CTAs per SM: the next PDL launch co-resides");
 };
 
@@ -154,7 +170,7 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
       const size_t launch = static_cast<size_t>((p.step - 1) & 7) * 64 + (p.layer & 63);
-      p.trace[(launch * 512 + cta) * 8 + phase] = gt;
+      p.trace[(launch * 512 + cta) * 16 + phase] = gt;
     }
   }
 }
@@ -172,13 +188,14 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
 // of the G x 128 outputs; every CTA pushes its partial slices and (m, l) into the owners' inboxes
 // with st.async (remote shared-memory stores completing as transaction bytes on the owner's
 // mbarrier), and each owner combines its slice once its inbox is full.
-__global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams p) {
+__global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const DraftParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* part = reinterpret_cast<float*>(smem + DCfg::kOffPart);
   float* inbox = reinterpret_cast<float*>(smem + DCfg::kOffRecv);
   uint64_t* inbox_bar = reinterpret_cast<uint64_t*>(smem + DCfg::kOffBar);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nthr = blockDim.x, nwarps = nthr >> 5;
   const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int CS = gridDim.x;
   const int seq = p.seq_ids[b];
@@ -213,7 +230,7 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
   // pre: true -> rows that exist before this launch (gathered ahead of the dependency wait)
   auto is_pre = [&](int v) { return v < k || (v != new_v && old_tail_ready); };
   auto resolve = [&](int r0, int rows, bool pre_pass) {
-    for (int r = tid; r < rows; r += DCfg::kThreads) {
+    for (int r = tid; r < rows; r += nthr) {
       const int v = v_begin + r0 + r;
       if (v >= v_end) {
         if (!pre_pass) src_row[r] = -2;
@@ -226,7 +243,7 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
     }
   };
   auto gather = [&](int r0, int rows, bool pre_pass) {
-    for (int i = tid; i < rows * 16; i += DCfg::kThreads) {
+    for (int i = tid; i < rows * 16; i += nthr) {
       const int r = i >> 4, ch = i & 15;
       const int v = v_begin + r0 + r;
       const bool in = v < v_end;
@@ -261,6 +278,14 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
   pdl_wait();  // previous layer complete: q and this step's new row are valid
   pdl_launch_dependents();
   dtrace(p, 1);
+  // post-wait rows of round 0 (this step's new row, zero fill) go out first, so their round trip
+  // overlaps the query loads below
+  const int rows0_pad = (min(kRoundRows, n) + 15) & ~15;
+  __syncthreads();  // src_row of the pre pass consumed by every thread
+  resolve(0, rows0_pad, false);
+  __syncthreads();
+  gather(0, rows0_pad, false);
+  cp_async_commit();
   DraftWarp w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
   // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45)
@@ -274,114 +299,154 @@ __global__ void __launch_bounds__(DCfg::kThreads) draft_kernel(const DraftParams
   for (int r0 = 0, round = 0; r0 < max(n, 1); r0 += kRoundRows, ++round) {
     const int rows = min(kRoundRows, n - r0);
     const int rows_pad = (rows + 15) & ~15;
-    if (round == 0) {
-      __syncthreads();                // src_row of the pre pass consumed by every thread
-      resolve(r0, rows_pad, false);   // new row, not-yet-ready tail rows, zero fill
-      __syncthreads();
-      gather(r0, rows_pad, false);
-    } else {
+    if (round > 0) {
       __syncthreads();  // previous round's tiles fully consumed
       resolve(r0, rows_pad, true);
       resolve(r0, rows_pad, false);
       __syncthreads();
       gather(r0, rows_pad, true);
       gather(r0, rows_pad, false);
+      cp_async_commit();
     }
-    cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
     dtrace(p, 2);
     const int n_sub = rows_pad >> 4;
-    for (int sb = warp; sb < n_sub; sb += DCfg::kWarps) {
-      const int tile = sb >> 2, r_in = (sb & 3) * 16;
-      w.step(smem_u32(smem + tile * DCfg::kTileBytes), smem_u32(smem + DCfg::kOffV + tile * DCfg::kTileBytes),
-             DCfg::kHalf, r_in, lane, p.scale_log2, min(16, n - (r0 + sb * 16)));
+    // warp w takes sub-blocks w, w + nwarps, ...; two at a time in one softmax step
+    const uint32_t kb = smem_u32(smem), vb = smem_u32(smem + DCfg::kOffV);
+    for (int sb = warp; sb < n_sub; sb += 2 * nwarps) {
+      const int sb2 = sb + nwarps;
+      const int nv0 = min(16, n - (r0 + sb * 16));
+      if (sb2 < n_sub) {
+        const uint32_t ks[2] = {kb + (sb >> 2) * DCfg::kTileBytes, kb + (sb2 >> 2) * DCfg::kTileBytes};
+        const uint32_t vs[2] = {vb + (sb >> 2) * DCfg::kTileBytes, vb + (sb2 >> 2) * DCfg::kTileBytes};
+        const int rr[2] = {(sb & 3) * 16, (sb2 & 3) * 16};
+        const int nv[2] = {nv0, min(16, n - (r0 + sb2 * 16))};
+        w.step<2>(ks, vs, DCfg::kHalf, rr, lane, p.scale_log2, nv);
+      } else {
+        const uint32_t ks[1] = {kb + (sb >> 2) * DCfg::kTileBytes};
+        const uint32_t vs[1] = {vb + (sb >> 2) * DCfg::kTileBytes};
+        const int rr[1] = {(sb & 3) * 16};
+        const int nv[1] = {nv0};
+        w.step<1>(ks, vs, DCfg::kHalf, rr, lane, p.scale_log2, nv);
+      }
     }
   }
   w.finalize_l();
   dtrace(p, 3);
 
-  // in-CTA merge of the warps' partials (only the G real query rows) -> part (smem)
+  // in-CTA merge of the warps' partials (only the G real query rows), fused with the push:
+  //  (1) every warp publishes its per-row (m, l); (2) every warp rescales its O fragments to the
+  //  CTA-wide row max and stores them; one thread per row forms (m*, l); (3) each thread sums the
+  //  warps' float4 groups and pushes the result straight into the owner's inbox with st.async.
+  float* wps = reinterpret_cast<float*>(smem);             // [nwarps][G x 128] rescaled partials
+  float* wml = reinterpret_cast<float*>(smem + DCfg::kOffRow);  // [kMaxWarps][16]: m[8], l[8]
+  __syncthreads();  // every warp done reading K/V tiles (wps aliases them) and src_row
+  dtrace(p, 8);
+  const int gid = lane >> 2, t4 = lane & 3;
+  if (gid == 0) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      wml[warp * 16 + 2 * t4 + e] = w.m[e];
+      wml[warp * 16 + 8 + 2 * t4 + e] = w.l[e];
+    }
+  }
   __syncthreads();
-  float* wps = reinterpret_cast<float*>(smem);
+  dtrace(p, 9);
   {
-    float* wp = wps + warp * DCfg::kWarpPart;
-    const int gid = lane >> 2, t4 = lane & 3;
+    float* wp = wps + warp * (p.G * 128);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int row = 2 * t4 + e;
       if (row < p.G) {
+        float mq[DCfg::kMaxWarps];  // independent loads, then a max tree (no serial smem chain)
+#pragma unroll
+        for (int q = 0; q < DCfg::kMaxWarps; ++q) mq[q] = q < nwarps ? wml[q * 16 + row] : -INFINITY;
+        float mstar = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < DCfg::kMaxWarps; ++q) mstar = fmaxf(mstar, mq[q]);
+        const float f = (w.m[e] == -INFINITY) ? 0.f : fast_exp2(w.m[e] - mstar);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-          wp[row * 128 + 16 * jj + gid] = w.o[jj][e];
-          wp[row * 128 + 16 * jj + gid + 8] = w.o[jj][2 + e];
-        }
-        if (gid == 0) {
-          wp[1024 + row] = w.m[e];
-          wp[1024 + 8 + row] = w.l[e];
+          wp[row * 128 + 16 * jj + gid] = w.o[jj][e] * f;
+          wp[row * 128 + 16 * jj + gid + 8] = w.o[jj][2 + e] * f;
         }
       }
     }
   }
-  __syncthreads();
-  for (int i = tid; i < n_out; i += DCfg::kThreads) {
-    const int row = i >> 7, col = i & 127;
+  dtrace(p, 10);
+  if (tid < p.G) {  // CTA-wide (m*, l) of row tid
+    float mq[DCfg::kMaxWarps], lq[DCfg::kMaxWarps];
+#pragma unroll
+    for (int q = 0; q < DCfg::kMaxWarps; ++q) {
+      mq[q] = q < nwarps ? wml[q * 16 + tid] : -INFINITY;
+      lq[q] = q < nwarps ? wml[q * 16 + 8 + tid] : 0.f;
+    }
     float mstar = -INFINITY;
 #pragma unroll
-    for (int q = 0; q < DCfg::kWarps; ++q) mstar = fmaxf(mstar, wps[q * DCfg::kWarpPart + 1024 + row]);
-    float acc = 0.f, lsum = 0.f;
-    if (mstar != -INFINITY) {
+    for (int q = 0; q < DCfg::kMaxWarps; ++q) mstar = fmaxf(mstar, mq[q]);
+    float lsum = 0.f;
 #pragma unroll
-      for (int q = 0; q < DCfg::kWarps; ++q) {
-        const float* wp = wps + q * DCfg::kWarpPart;
-        const float mq = wp[1024 + row];
-        if (mq == -INFINITY) continue;
-        const float f = fast_exp2(mq - mstar);
-        acc += wp[row * 128 + col] * f;
-        lsum += wp[1024 + 8 + row] * f;
-      }
-    }
-    part[row * 128 + col] = acc;
-    if (col == 0) {
-      part[1024 + row] = mstar;
-      part[1024 + 8 + row] = lsum;
-    }
+    for (int q = 0; q < DCfg::kMaxWarps; ++q) lsum += mq[q] == -INFINITY ? 0.f : lq[q] * fast_exp2(mq[q] - mstar);
+    part[1024 + tid] = mstar;
+    part[1024 + 8 + tid] = lsum;
   }
+  dtrace(p, 11);
   __syncthreads();
-
-  // push: partial slices -> their owners' inboxes, (m, l) -> every owner
+  dtrace(p, 5);
   cluster_wait_acquire();  // every owner's inbox barrier is initialised
   if (tid == 0) {
     const int my_vals = my_hi - my_lo;
     mbar_arrive_expect_tx(inbox_bar, static_cast<uint32_t>(CS) * (my_vals + 16) * 4u);
   }
   const uint32_t inbox_addr = smem_u32(inbox), bar_addr = smem_u32(inbox_bar);
-  for (int q4 = tid; q4 < n_out / 4; q4 += DCfg::kThreads) {
+  for (int q4 = tid; q4 < n_out / 4; q4 += nthr) {
+    float4 x[DCfg::kMaxWarps];
+#pragma unroll
+    for (int q = 0; q < DCfg::kMaxWarps; ++q)
+      x[q] = q < nwarps ? reinterpret_cast<const float4*>(wps + q * (p.G * 128))[q4] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 v = x[0];
+#pragma unroll
+    for (int q = 1; q < DCfg::kMaxWarps; ++q) {  // fixed warp order: deterministic
+      v.x += x[q].x;
+      v.y += x[q].y;
+      v.z += x[q].z;
+      v.w += x[q].w;
+    }
     const int e = q4 * 4, owner = e / per;
-    const float4 v = *reinterpret_cast<const float4*>(part + e);
     st_async_v4(mapa_shared(inbox_addr + (split * rstride + (e - owner * per)) * 4, owner), v,
                 mapa_shared(bar_addr, owner));
   }
-  for (int t = tid; t < CS * 4; t += DCfg::kThreads) {
+  for (int t = tid; t < CS * 4; t += nthr) {
     const int owner = t >> 2, q = t & 3;
     const float4 v = *reinterpret_cast<const float4*>(part + 1024 + 4 * q);  // m[0..7], l[0..7]
     st_async_v4(mapa_shared(inbox_addr + (split * rstride + per + 4 * q) * 4, owner), v,
                 mapa_shared(bar_addr, owner));
   }
   // combine my slice once every sender's contribution has landed
+  dtrace(p, 6);
   mbar_wait_cluster(inbox_bar, 0);
+  dtrace(p, 7);
   float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128;
-  for (int e = my_lo + tid; e < my_hi; e += DCfg::kThreads) {
+  for (int e = my_lo + tid; e < my_hi; e += nthr) {
     const int row = e >> 7, off = e - my_lo;
+    float ms[DCfg::kMaxCS], ls[DCfg::kMaxCS], os[DCfg::kMaxCS];  // all inbox loads in flight together
+#pragma unroll
+    for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2) {
+      const bool ok = s2 < CS;
+      ms[s2] = ok ? inbox[s2 * rstride + per + row] : -INFINITY;
+      ls[s2] = ok ? inbox[s2 * rstride + per + 8 + row] : 0.f;
+      os[s2] = ok ? inbox[s2 * rstride + off] : 0.f;
+    }
     float mstar = -INFINITY;
-    for (int s2 = 0; s2 < CS; ++s2) mstar = fmaxf(mstar, inbox[s2 * rstride + per + row]);
+#pragma unroll
+    for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2) mstar = fmaxf(mstar, ms[s2]);
     float acc = 0.f, lsum = 0.f;
-    for (int s2 = 0; s2 < CS; ++s2) {
-      const float ms = inbox[s2 * rstride + per + row];
-      if (ms == -INFINITY) continue;
-      const float f = fast_exp2(ms - mstar);
-      acc += inbox[s2 * rstride + off] * f;
-      lsum += inbox[s2 * rstride + per + 8 + row] * f;
+#pragma unroll
+    for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2) {
+      const float f = ms[s2] == -INFINITY ? 0.f : fast_exp2(ms[s2] - mstar);
+      acc += os[s2] * f;
+      lsum += ls[s2] * f;
     }
     out_unit[e] = acc / lsum;
   }
@@ -398,7 +463,8 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);
-  cfg.blockDim = dim3(DCfg::kThreads);
+  // one warp per 16-row sub-block of the CTA's chunk (<= 9 warps, two CTAs per SM)
+  cfg.blockDim = dim3(32 * std::min(DCfg::kMaxWarps, std::max(1, (std::min(p.chunk, DCfg::kMaxTiles * DCfg::kTile) + 15) / 16)));
   cfg.dynamicSmemBytes = DCfg::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attrs[2];

@@ -84,6 +84,8 @@ struct VerifyParams {
   unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production
   int use_pdl;  // programmatic dependent launch after the previous layer's verify (iteration graph)
   int next_layer;  // layer verified next (its first tiles are prefetched into L2), -1: none
+  int chunk_tiles;  // 128-token tiles per dynamically claimed chunk
+  int prefetch;     // tiles prefetched into L2 ahead of the K ring
 };
 
 struct DraftParams {

@@ -99,8 +99,8 @@ static unsigned long long* dev_verify_trace() {
   return t;
 }
 
-// dev-only draft trace (SA_TRACE=1): [(step-1) mod 8][layer mod 64][512 CTAs][8 phases] globaltimer ns.
-constexpr size_t kDTraceWords = static_cast<size_t>(8) * 64 * 512 * 8;
+// dev-only draft trace (SA_TRACE=1): [(step-1) mod 8][layer mod 64][512 CTAs][16 phases] globaltimer ns.
+constexpr size_t kDTraceWords = static_cast<size_t>(8) * 64 * 512 * 16;
 static unsigned long long* dev_draft_trace() {
   static unsigned long long* t = [] {
     unsigned long long* b = nullptr;
@@ -258,6 +258,8 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   if (!(a->scale > 0.f)) return fail(SA_INVALID_ARGUMENT, "softmax_stable: scale must be positive");
   if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(SA_INVALID_ARGUMENT, "verify: k_new/v_new");
   if (a->score_row_mask >> a->n_rows) return fail(SA_INVALID_ARGUMENT, "score_columns: row label not collected");
+  if (r->cache->max_pages_per_seq > 1024)
+    return fail(SA_NOT_SUPPORTED, "verify: more than 1024 pages per sequence (raise page_size)");
   if (a->score_layout != SA_PER_LAYER && a->score_layout != SA_PER_KV_HEAD)
     return fail(SA_INVALID_ARGUMENT, "verify: score_layout");
   if (a->logits && (a->collect_row_mask == 0 || (a->collect_row_mask >> a->n_rows) || a->ld_logits < r->p_max))
@@ -322,7 +324,17 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   } else {
     // at most one CTA per SM over all units, a single wave (floor: a 149th CTA would run as a
     // second wave); dynamic chunk claiming balances inside a unit
-    const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + 1) / 2);
+    static const int chunk_tiles = [] {
+      const char* v = getenv("SA_VERIFY_CHUNK");  // dev tuning knob
+      return v ? std::max(1, atoi(v)) : 2;
+    }();
+    static const int prefetch = [] {
+      const char* v = getenv("SA_VERIFY_PF");  // dev tuning knob
+      return v ? std::min(12, std::max(0, atoi(v))) : 0;
+    }();
+    p.chunk_tiles = chunk_tiles;
+    p.prefetch = prefetch;
+    const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
     p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, r->num_sms / units),
                                                      n_chunks, 128, r->v_units_cap / units}));
     p.chunk = 0;
@@ -403,12 +415,17 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.scale_log2 = a->scale * sa::kLog2e;
   p.out = a->out;
   const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
-  {  // one cluster of CS CTAs per (sequence, KV head); >= 64 keys per CTA, CS <= 16
+  {  // one cluster of CS CTAs per (sequence, KV head): the smallest CS whose chunk fits one resident
+     // round (192 rows); 12 before 16 because two launches of 12-CTA clusters co-reside on 148 SMs
+     // (the PDL successor gathers while this one computes) and two of 16-CTA clusters do not
     const int64_t m = r->k_cap + a->step;
-    int cs = static_cast<int>(std::min<int64_t>(sa::draft_max_splits(), std::max<int64_t>(1, (m + 63) / 64)));
-    if (cs > 8 && cs < 16) cs = 16;  // cluster sizes 1, 2, 4, 8, 16
-    else if (cs > 4 && cs < 8) cs = 8;
-    else if (cs == 3) cs = 4;
+    const int round_rows = sa::draft_round_rows();
+    int cs = 16;
+    for (int c : {1, 2, 4, 8, 12, 16})
+      if ((m + c - 1) / c <= round_rows) {
+        cs = c;
+        break;
+      }
     p.n_splits = cs;
     p.chunk = static_cast<int>(((m + cs - 1) / cs + 15) / 16 * 16);
   }
@@ -516,7 +533,7 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
       d.scale = a->scale;
       d.out = a->out_d + off * qd_l;
       if ((skip & 4) == 0)
-        if (sa_status st = draft_impl(r, &d, main, /*pdl=*/j > 1 || l > 0)) return st;
+        if (sa_status st = draft_impl(r, &d, main, /*pdl=*/(j > 1 || l > 0) && !getenv("SA_DRAFT_NOPDL"))) return st;
     }
   }
   SA_CUDA_CHECK(cudaEventRecord(r->ev_join, r->side));

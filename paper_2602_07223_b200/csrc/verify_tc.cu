@@ -34,7 +34,6 @@ struct TCfg {
   static constexpr int kTile = 128;
   static constexpr int kSK = 2;                       // K ring stages (K is recycled right after QK^T)
   static constexpr int kSV = (N <= 32) ? 3 : 2;       // V ring stages (V is held until PV retires)
-  static constexpr int kPrefetch = 4;                 // tiles prefetched into L2 ahead of the ring loads
   static constexpr int kHalf = kTile * 128;           // one 64-column half of a K or V tile (16 KB)
   static constexpr int kTileBytes = 2 * kHalf;         // K or V tile (32 KB)
   static constexpr int kQHalf = N * 128;
@@ -47,12 +46,13 @@ struct TCfg {
   static constexpr int kOffP = kOffQ + 2 * kQHalf;     // [wg][hi, lo]
   static constexpr int kOffBar = kOffP + 4 * kPBytes;
   static constexpr int kPosRing = 8;                  // published tile positions (consumer-visible)
-  static constexpr int kChunkTiles = 2;               // tiles per dynamically claimed chunk
   static constexpr int kNumBars = 2 * kSK + 2 * kSV + 10 + kPosRing + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   // misc: tmem slot, flag, ntiles[2] | mref[2][64] fac[2][64] ltot[2][64] wsc[64] lim[64] | red[2][4][64]
-  //       | tile_pos[kPosRing] | producer ring pring[16]
-  static constexpr int kMiscBytes = 16 + (2 + 2 + 2 + 1 + 1) * 64 * 4 + 2 * 4 * 64 * 4 + kPosRing * 4 + 16 * 4;
+  //       | tile_pos[kPosRing] | producer ring pring[32]
+  static constexpr int kBtMax = 1024;                  // block-table entries staged in smem
+  static constexpr int kMiscBytes = 16 + (2 + 2 + 2 + 1 + 1) * 64 * 4 + 2 * 4 * 64 * 4 + kPosRing * 4 + 32 * 4 +
+                                    kBtMax * 4;
   static constexpr int kSmem = kOffMisc + kMiscBytes + 1024;
   static constexpr int kThreads = 384;
   // TMEM columns: S[2] (N each) then O[2] (kNP each: O_hi | O_lo)
@@ -65,12 +65,17 @@ constexpr float kLazyMaxThresh = 8.0f;
 
 // Butterfly all-reduce of N independent values across the warp, level-outer so the N shuffles of
 // each level pipeline instead of forming N serial 5-deep chains.
+// Float max across the warp with one REDUX per value: IEEE bits mapped to an order-preserving s32
+// (negative values get their magnitude bits flipped), redux.sync.max.s32, mapped back.
+__device__ __forceinline__ int f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : (i ^ 0x7FFFFFFF);
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : (i ^ 0x7FFFFFFF)); }
 template <int N>
 __device__ __forceinline__ void warp_allreduce_max(float (&x)[N]) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-    for (int m = 0; m < N; ++m) x[m] = fmaxf(x[m], __shfl_xor_sync(0xffffffffu, x[m], off));
+  for (int m = 0; m < N; ++m) x[m] = ord2f(__reduce_max_sync(0xffffffffu, f2ord(x[m])));
 }
 template <int N>
 __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
@@ -127,7 +132,8 @@ __global__ void __launch_bounds__(384, 1)
   int* lim = reinterpret_cast<int*>(wsc + 64);                           // [64]
   float* red_all = reinterpret_cast<float*>(lim + 64);                   // [2][4][64]
   int* tile_pos = reinterpret_cast<int*>(red_all + 512);                 // [kPosRing]
-  int* pring = tile_pos + C::kPosRing;                                   // [16] producer-private
+  int* pring = tile_pos + C::kPosRing;                                   // [32] producer-private
+  int* bt = pring + 32;                                                  // [kBtMax] this sequence's pages
   int* ntiles_wg = flag + 1;                                             // [2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -149,7 +155,8 @@ __global__ void __launch_bounds__(384, 1)
   const int n_pref = p0 / C::kTile;
   const int win_lo = n_pref * C::kTile;
   const int n_win = (p0 + R - win_lo + C::kTile - 1) / C::kTile;
-  const int n_chunks = (n_pref + C::kChunkTiles - 1) / C::kChunkTiles;
+  const int chunk_tiles = p.chunk_tiles, prefetch = p.prefetch;
+  const int n_chunks = (n_pref + chunk_tiles - 1) / chunk_tiles;
   const int unit = b * p.Hkv + g;
   // ------------------------------------------------------------------ prologue (all threads)
   if (tid == 0) {
@@ -174,6 +181,8 @@ __global__ void __launch_bounds__(384, 1)
     fence_mbar_init();
   }
   uint8_t* sq = smem + C::kOffQ;
+  for (int i = tid; i < ((p0 + R + (1 << p.cache.page_shift) - 1) >> p.cache.page_shift); i += C::kThreads)
+    bt[i] = __ldg(p.cache.block_table + static_cast<int64_t>(seq) * p.cache.max_pages_per_seq + i);
   if (tid < 64) {
     mref_all[tid] = -INFINITY;
     mref_all[64 + tid] = -INFINITY;
@@ -204,43 +213,50 @@ __global__ void __launch_bounds__(384, 1)
       tma_prefetch_desc(&tmv);
       const uint64_t pol = policy_evict_first();
       // tile stream of this CTA: window tiles (last split), then its chunks; pring holds positions
-      int q_end = 0, cur_chunk = -1, cur_tile = 0, claims = 0;
+      int q_end = 0, cur_chunk = -1, cur_tile = 0, claims = 0, pending = 0;
       bool exhausted = false, done = false, dep_seen = false, win_added = false;
       auto fill = [&](int upto) {
         while (q_end < upto && !exhausted) {
-          if (cur_chunk < 0 || cur_tile == min(C::kChunkTiles, n_pref - cur_chunk * C::kChunkTiles)) {
+          if (cur_chunk < 0 || cur_tile == min(chunk_tiles, n_pref - cur_chunk * chunk_tiles)) {
             if (last && claims == 1 && !win_added) {  // window tiles go right after the first chunk
-              for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 15] = win_lo + w2 * C::kTile;
+              for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 31] = win_lo + w2 * C::kTile;
               win_added = true;
             }
-            cur_chunk = claims++ == 0 ? split : p.n_splits + atomicAdd(p.chunk_ctr + unit, 1);
+            // claims run one chunk ahead: the atomic's L2 round trip overlaps the current chunk (its
+            // result register is first read here, one chunk later); no claim is left unconsumed
+            cur_chunk = claims++ == 0 ? split : p.n_splits + pending;
+            if (cur_chunk < n_chunks) pending = atomicAdd(p.chunk_ctr + unit, 1);
             if (cur_chunk >= n_chunks) {
               exhausted = true;
               break;
             }
             cur_tile = 0;
           }
-          pring[q_end++ & 15] = (cur_chunk * C::kChunkTiles + cur_tile++) * C::kTile;
+          pring[q_end++ & 31] = (cur_chunk * chunk_tiles + cur_tile++) * C::kTile;
         }
         if (exhausted && !done) {  // (short prefixes: the window tiles close the stream)
           if (last && !win_added)
-            for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 15] = win_lo + w2 * C::kTile;
+            for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 31] = win_lo + w2 * C::kTile;
           done = true;
         }
       };
-      auto row_of = [&](int pos) { return static_cast<int>(cache_row(p.cache, seq, p.layer, g, pos)); };
+      // block table staged in shared memory by the prologue: no dependent global load per tile
+      auto row_of = [&](int pos) {
+        return ((((p.layer * p.cache.num_pages + bt[pos >> p.cache.page_shift]) * p.cache.n_kv_heads + g)
+                 << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1)));
+      };
       int nk = 0, nv = 0, npf = 0;
       while (true) {
-        fill(nk + 1 + C::kPrefetch);
-        for (; npf < min(q_end, nv + C::kSV + C::kPrefetch) && nk >= 1; ++npf) {  // L2 prefetch
-          const int row = row_of(pring[npf & 15]);
+        fill(nk + 1 + prefetch);
+        for (; npf < min(q_end, nv + C::kSV + prefetch) && nk >= 1; ++npf) {  // L2 prefetch
+          const int row = row_of(pring[npf & 31]);
           tma_prefetch_l2_2d(&tmk, 0, row);
           tma_prefetch_l2_2d(&tmk, 64, row);
           tma_prefetch_l2_2d(&tmv, 0, row);
           tma_prefetch_l2_2d(&tmv, 64, row);
         }
         if (nk < q_end && (nk < C::kSK || mbar_test(&k_empty[nk % C::kSK], ((nk / C::kSK) & 1) ^ 1))) {
-          const int st = nk % C::kSK, pos = pring[nk & 15];
+          const int st = nk % C::kSK, pos = pring[nk & 31];
           if (pos >= win_lo && !dep_seen) {  // window rows are appended after the dependency wait
             mbar_wait(dep_bar, 0);
             dep_seen = true;
@@ -257,7 +273,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         if (nv < nk && (nv < C::kSV || mbar_test(&v_empty[nv % C::kSV], ((nv / C::kSV) & 1) ^ 1))) {
           const int st = nv % C::kSV;
-          const int row = row_of(pring[nv & 15]);
+          const int row = row_of(pring[nv & 31]);
           uint8_t* dst = smem + C::kOffV + st * C::kTileBytes;
           mbar_expect_tx(&v_full[st], C::kTileBytes);
           tma_load_2d(dst, &tmv, &v_full[st], 0, row, pol);
@@ -270,9 +286,10 @@ __global__ void __launch_bounds__(384, 1)
       // keep HBM busy across the layer boundary: pull the next layer's first tiles of this unit
       // (the chunk the next layer's CTA `split` claims statically) into L2 while this layer drains
       if (p.next_layer >= 0 && split < n_chunks) {
-        for (int t = 0; t < min(C::kChunkTiles, n_pref - split * C::kChunkTiles); ++t) {
-          const int row = static_cast<int>(
-              cache_row(p.cache, seq, p.next_layer, g, (split * C::kChunkTiles + t) * C::kTile));
+        for (int t = 0; t < min(chunk_tiles, n_pref - split * chunk_tiles); ++t) {
+          const int pos = (split * chunk_tiles + t) * C::kTile;
+          const int row = (((p.next_layer * p.cache.num_pages + bt[pos >> p.cache.page_shift]) * p.cache.n_kv_heads + g)
+                           << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1));
           tma_prefetch_l2_2d(&tmk, 0, row);
           tma_prefetch_l2_2d(&tmk, 64, row);
           tma_prefetch_l2_2d(&tmv, 0, row);
@@ -285,33 +302,59 @@ __global__ void __launch_bounds__(384, 1)
         mbar_arrive(&pos_bar[(nk + e) % C::kPosRing]);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------- dependency wait, Q staging, fused window append
+  } else {
+    // ------------------------- warps 1-3: dependency wait, Q staging, fused window append (96 threads,
+    // every global load of a batch in flight together)
     pdl_wait();
+    const int t96 = tid - 32;
     const __nv_bfloat16* qb = p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
-    for (int i = lane; i < N * 16; i += 32) {
-      const int row = i >> 4, ch = i & 15;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (row < M) v = __ldg(reinterpret_cast<const uint4*>(qb + row * 128 + ch * 8));
-      *reinterpret_cast<uint4*>(sq + swz(row, ch, C::kQHalf)) = v;
+    constexpr int kQ = N * 16;  // 16-byte chunks of the padded Q tile
+    for (int base = t96; base < kQ; base += 96 * 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * 96, row = i >> 4, ch = i & 15;
+        v[u] = make_uint4(0, 0, 0, 0);
+        if (i < kQ && row < M) v[u] = __ldg(reinterpret_cast<const uint4*>(qb + row * 128 + ch * 8));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * 96;
+        if (i < kQ) *reinterpret_cast<uint4*>(sq + swz(i >> 4, i & 15, C::kQHalf)) = v[u];
+      }
     }
     if (last && p.k_new) {  // fused KvStore::append of the window rows, read back by TMA
-      for (int i = lane; i < 2 * R * 16; i += 32) {
-        const int which = i / (R * 16), row = (i >> 4) % R, ch = i & 15;
-        const __nv_bfloat16* src =
-            (which ? p.v_new : p.k_new) + ((static_cast<size_t>(b) * R + row) * p.Hkv + g) * 128;
-        const int64_t cr = cache_row(p.cache, seq, p.layer, g, p0 + row);
-        __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + cr * 128;
-        reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
+      for (int base = t96; base < 2 * R * 16; base += 96 * 8) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + u * 96;
+          if (i < 2 * R * 16) {
+            const int which = i / (R * 16), row = (i >> 4) % R, ch = i & 15;
+            v[u] = __ldg(reinterpret_cast<const uint4*>((which ? p.v_new : p.k_new) +
+                                                        ((static_cast<size_t>(b) * R + row) * p.Hkv + g) * 128) + ch);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = base + u * 96;
+          if (i < 2 * R * 16) {
+            const int which = i / (R * 16), row = (i >> 4) % R, ch = i & 15;
+            const int pos = p0 + row;
+            const int64_t cr = (((static_cast<int64_t>(p.layer) * p.cache.num_pages + bt[pos >> p.cache.page_shift]) *
+                                     p.cache.n_kv_heads + g) << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1));
+            reinterpret_cast<uint4*>((which ? p.cache.v : p.cache.k) + cr * 128)[ch] = v[u];
+          }
+        }
       }
       fence_proxy_async();  // generic-proxy global writes -> async-proxy (TMA) reads
     }
     fence_proxy_async_smem();  // Q tile: generic smem writes -> tensor-core reads
-    __syncwarp();
-    if (lane == 0) mbar_arrive(dep_bar);
+    named_bar_sync(5, 96);
+    if (warp == 1 && lane == 0) mbar_arrive(dep_bar);
     pdl_launch_dependents();
     // ---------------------------------------------------------------- MMA issuer (one thread)
-    if (lane == 0) {
+    if (warp == 1 && lane == 0) {
       constexpr uint32_t idesc_qk = umma_idesc_bf16(N, 0, 0);
       constexpr uint32_t idesc_pv = umma_idesc_bf16(C::kNP, 1, 1);
       const uint32_t q_base = smem_u32(sq);
@@ -361,7 +404,7 @@ __global__ void __launch_bounds__(384, 1)
       if (t >= 1) issue_pv(t - 1);
     }
   }
-  if (warp != 1) {  // producer and spare warps: trigger only once this CTA is past its wait
+  if (warp == 0) {  // producer warp: trigger only once this CTA is past its wait
     mbar_wait(dep_bar, 0);
     pdl_launch_dependents();
   }

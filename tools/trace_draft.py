@@ -51,7 +51,7 @@ f = lib().sa_dev_trace_dump
 f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
 assert f(path.encode()) == 0
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
-dr = raw[1024 + 64 * 8192:].reshape(8, 64, 512, 8)
+dr = raw[1024 + 64 * 8192:].reshape(8, 64, 512, 16)
 t0 = None
 prev = None
 print(f"{'step':>4s} {'layer':>5s} {'start':>7s} {'st_max':>7s} | after wait med/max | gathered med/max | computed med/max | end med/max | dt")
@@ -70,7 +70,9 @@ for j in range(gamma):
         if l < 3 or l == L - 1:
             print(f"{j + 1:4d} {l:5d} {s0.min():7.2f} {s0.max():7.2f} | {np.median(v(1)):7.2f} {v(1).max():7.2f} | "
                   f"{np.median(v(2)):7.2f} {v(2).max():7.2f} | {np.median(v(3)):7.2f} {v(3).max():7.2f} | "
-                  f"{np.median(en):7.2f} {en.max():7.2f} | {dt:5.2f}")
+                  f"{np.median(en):7.2f} {en.max():7.2f} | {dt:5.2f}  merge: sync1 {np.median(v(8)):7.2f} "
+                  f"written {np.median(v(9)):7.2f} t10 {np.median(v(10)):7.2f} t11 {np.median(v(11)):7.2f} ctamerged {np.median(v(5)):7.2f} "
+                  f"pushed {np.median(v(6)):7.2f} inbox {np.median(v(7)):7.2f}/{v(7).max():7.2f}")
 
 # verify phase on the same clock (globaltimer): last layer's end vs the first draft's start
 vt = raw[1024:1024 + 64 * 8192].reshape(64, 1024, 8)
