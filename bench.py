@@ -190,7 +190,32 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     ms = max_over_ranks(ms)
 
-    # ---- dominant kernel (verify) launch durations, CUDA events on the launching stream
+    # ---- dominant kernel (verify): its average duration INSIDE the iteration's PDL chain = the
+    # verify-only phase of the same graph (CUDA events on the launching stream) / L launches; the
+    # isolated back-to-back launch time is reported beside it
+    from paper_2602_07223_b200 import PHASE_DRAFT, PHASE_VERIFY
+
+    def phase_ms(phases, n):
+        a = runner.iteration_args(gamma, qv, kvn, vvn, qd, kdn, vdn, out_v, out_d, strategy=COLLECT2, mode=PER_LAYER,
+                                  scale=scale, use_graph=not args.no_graph, phases=phases)
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                runner.iteration(a, stream=stream)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a0.record(stream)
+            for _ in range(n):
+                runner.iteration(a, stream=stream)
+            a1.record(stream)
+        torch.cuda.synchronize()
+        return a0.elapsed_time(a1) / n
+
+    v_phase_ms = phase_ms(PHASE_VERIFY, args.steps)
+    d_phase_ms = phase_ms(PHASE_DRAFT, args.steps)  # selections of the last full iteration
+    with torch.cuda.stream(stream):  # restore a consistent state (sums consumed) for the e2e leg
+        runner.iteration(itargs, stream=stream)
+    vms = v_phase_ms / L
     nv = min(L, 32)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nv * 3)]
     torch.cuda.synchronize()
@@ -202,7 +227,7 @@ def run_ours(args, rank, world, local_rank):
             b_.record(stream)
             runner.select(l, stream=stream)  # consumes (re-arms) the per-layer score sums, outside the events
     torch.cuda.synchronize()
-    vms = sum(a.elapsed_time(b_) for a, b_ in ev[nv:]) / (len(ev) - nv)  # skip the first (warm) pass
+    vms_isolated = sum(a.elapsed_time(b_) for a, b_ in ev[nv:]) / (len(ev) - nv)  # skip the first (warm) pass
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the region
     host_in = [t.cpu().pin_memory() for t in (qv, kvn, vvn, qd, kdn, vdn)]
@@ -239,6 +264,17 @@ def run_ours(args, rank, world, local_rank):
     it_bytes = iteration_bytes(L, Hq, Hkv, p0, gamma, k, B)
     vb = verify_launch_bytes(Hq, Hkv, p0, R, B)
     v_gbs = vb / (vms / 1e3) / 1e9
+    draft_bytes = B * ((k + (gamma + 1) / 2) * 2 * Hkv * D * 2 + Hq * D * 6 + k * 4 + 2 * Hkv * D * 2)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "verify_dram_bytes.json")  # ncu dram__bytes_{read,write}.sum per launch
+    if os.path.exists(tf):
+        try:
+            with open(tf) as f:
+                t = json.load(f)
+            if t.get("workload") == args.workload:
+                traffic = t.get("bytes_per_launch")
+        except Exception:
+            traffic = None
     it_gbs = it_bytes / (ms / 1e3) / 1e9
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -252,9 +288,14 @@ def run_ours(args, rank, world, local_rank):
         "hbm": {"bytes_per_iter": it_bytes, "achieved_gbs": round(it_gbs, 1),
                 "frac_of_8tbs": round(it_gbs / HBM_NOMINAL, 4), "frac_of_measured": round(it_gbs / hbm_peak, 4),
                 "measured_peak_gbs": hbm_peak, "peak_source": peak_src},
-        "roofline": {"kernel": "verify_kernel (one layer)", "bound": "hbm", "achieved": round(v_gbs, 1),
-                     "peak": hbm_peak, "unit": "GB/s", "frac": round(v_gbs / hbm_peak, 4), "traffic": None,
-                     "bytes_per_launch": vb, "launch_us": round(vms * 1e3, 2), "peak_source": peak_src},
+        "roofline": {"kernel": "verify_tc_kernel (one layer, all KV heads)", "bound": "hbm", "achieved": round(v_gbs, 1),
+                     "peak": hbm_peak, "unit": "GB/s", "frac": round(v_gbs / hbm_peak, 4), "traffic": traffic,
+                     "bytes_per_launch": vb, "launch_us": round(vms * 1e3, 2),
+                     "launch_us_isolated": round(vms_isolated * 1e3, 2), "peak_source": peak_src,
+                     "timing": "verify-only phase of the iteration graph (PDL chain, CUDA events) / L launches"},
+        "phases": {"verify_ms": round(v_phase_ms, 4), "draft_ms": round(d_phase_ms, 4),
+                   "draft_us_per_launch": round(d_phase_ms * 1e3 / (gamma * L), 2),
+                   "draft_bytes_per_launch": draft_bytes, "draft_gbs": round(draft_bytes / (d_phase_ms / (gamma * L) / 1e3) / 1e9, 1)},
         "e2e": {"value": round(world * tok_per_step / (ms_e2e / 1e3), 2), "unit": "tokens/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4)},
         "gpu_launches": launches_per_step * args.steps,

@@ -216,7 +216,12 @@ typedef struct sa_iteration_args {
   const void *qv, *kv_new, *vv_new, *qd, *kd_new, *vd_new;
   float *out_v, *out_d;
   int32_t use_graph;
+  uint32_t phases;          /* 0 = all; else a mask of SA_PHASE_* (timing breakdowns: the phases left
+                               out are skipped, their buffers are left as the last run wrote them) */
 } sa_iteration_args;
+#define SA_PHASE_VERIFY 1u
+#define SA_PHASE_SELECT 2u
+#define SA_PHASE_DRAFT 4u
 SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void* stream);
 /* Number of kernels one sa_iteration_run launches (for gpu_launches accounting). */
 SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_args* a);

@@ -13,6 +13,7 @@ STATUS = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 
           5: "cuda_error", 6: "not_supported", 7: "nccl_error"}
 LAST_ACCEPTED, ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS = 2, 3, 4, 5
 PER_LAYER, PER_KV_HEAD = 0, 1
+PHASE_VERIFY, PHASE_SELECT, PHASE_DRAFT = 1, 2, 4
 F32, BF16 = 0, 1
 
 
@@ -55,7 +56,7 @@ class DraftArgs(C.Structure):
 class IterationArgs(C.Structure):
     _fields_ = [("gamma", _i32), ("strategy", C.c_int), ("mode", C.c_int), ("scale", _f32), ("qv", _vp),
                 ("kv_new", _vp), ("vv_new", _vp), ("qd", _vp), ("kd_new", _vp), ("vd_new", _vp), ("out_v", _vp),
-                ("out_d", _vp), ("use_graph", _i32)]
+                ("out_d", _vp), ("use_graph", _i32), ("phases", _u32)]
 
 
 # exported symbol -> (restype, argtypes)
@@ -311,11 +312,11 @@ class Runner:
         _check(lib().sa_draft_attention(self.h, C.byref(a), _stream(stream)))
 
     def iteration_args(self, gamma, qv, kv_new, vv_new, qd, kd_new, vd_new, out_v, out_d, strategy=COLLECT2,
-                       mode=PER_LAYER, scale=None, use_graph=True):
+                       mode=PER_LAYER, scale=None, use_graph=True, phases=0):
         if scale is None:
             scale = float((1.0 / 128 ** 0.5))
         return IterationArgs(gamma, strategy, mode, scale, _ptr(qv), _ptr(kv_new), _ptr(vv_new), _ptr(qd),
-                             _ptr(kd_new), _ptr(vd_new), _ptr(out_v), _ptr(out_d), int(use_graph))
+                             _ptr(kd_new), _ptr(vd_new), _ptr(out_v), _ptr(out_d), int(use_graph), int(phases))
 
     def iteration(self, args: IterationArgs, stream=None):
         _check(lib().sa_iteration_run(self.h, C.byref(args), _stream(stream)))

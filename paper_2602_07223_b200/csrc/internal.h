@@ -86,6 +86,7 @@ struct VerifyParams {
   int next_layer;  // layer verified next (its first tiles are prefetched into L2), -1: none
   int chunk_tiles;  // 128-token tiles per dynamically claimed chunk
   int prefetch;     // tiles prefetched into L2 ahead of the K ring
+  int next_pf;      // chunks of the next layer each CTA prefetches into L2 at the end of its stream
 };
 
 struct DraftParams {

@@ -46,8 +46,7 @@ struct sa_runner {
   cudaStream_t capture = nullptr;  // graphs are captured here (the caller's stream may be legacy)
   std::vector<cudaEvent_t> ev_v, ev_s;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  std::vector<char> gkey;
+  std::vector<std::pair<std::vector<char>, cudaGraphExec_t>> graphs;  // keyed by args + batch binding
 };
 
 namespace {
@@ -86,7 +85,7 @@ int mtiles_for(int G, int R) { return (G * R + 2 + 15) / 16; }
 // dev-only verify pipeline trace (SA_TRACE=1): [1024] per-tile events of CTA 0, then per layer
 // (mod 64) [1024 CTAs][8] = start, end, main-loop end, tiles | split << 32, last PV done,
 // partial stored, arrival counted, merge inputs landed (globaltimer ns).
-constexpr size_t kVTraceWords = 1024 + 64 * 8192;
+constexpr size_t kVTraceWords = 1024 + 64 * 16384;
 static unsigned long long* dev_verify_trace() {
   static unsigned long long* t = [] {
     unsigned long long* b = nullptr;
@@ -187,7 +186,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
 
 SA_API sa_status sa_runner_destroy(sa_runner* r) {
   if (!r) return SA_OK;
-  if (r->gexec) cudaGraphExecDestroy(r->gexec);
+  for (auto& kv : r->graphs) cudaGraphExecDestroy(kv.second);
   for (auto ev : r->ev_v) if (ev) cudaEventDestroy(ev);
   for (auto ev : r->ev_s) if (ev) cudaEventDestroy(ev);
   if (r->ev_fork) cudaEventDestroy(r->ev_fork);
@@ -332,6 +331,11 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
       const char* v = getenv("SA_VERIFY_PF");  // dev tuning knob
       return v ? std::min(12, std::max(0, atoi(v))) : 0;
     }();
+    static const int next_pf = [] {
+      const char* v = getenv("SA_VERIFY_NEXTPF");  // dev tuning knob
+      return v ? std::max(0, atoi(v)) : 0;
+    }();
+    p.next_pf = next_pf;
     p.chunk_tiles = chunk_tiles;
     p.prefetch = prefetch;
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
@@ -471,7 +475,9 @@ SA_API sa_status sa_draft_attention(sa_runner* r, const sa_draft_args* a, void* 
 SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_args* a) {
   if (!r || !a) return 0;
   const int64_t L = r->cache->n_layers;
-  return L /*verify*/ + L /*select*/ + static_cast<int64_t>(a->gamma) * L /*draft*/;
+  const uint32_t ph = a->phases ? a->phases : 7u;
+  return ((ph & SA_PHASE_VERIFY) ? L : 0) + ((ph & SA_PHASE_SELECT) ? L : 0) +
+         ((ph & SA_PHASE_DRAFT) ? static_cast<int64_t>(a->gamma) * L : 0);
 }
 
 static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cudaStream_t main) {
@@ -486,11 +492,12 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
   const auto* qd = static_cast<const __nv_bfloat16*>(a->qd);
   const auto* kdn = static_cast<const __nv_bfloat16*>(a->kd_new);
   const auto* vdn = static_cast<const __nv_bfloat16*>(a->vd_new);
-  // dev-only phase isolation for timing breakdowns: SA_ITER_SKIP bit0 verify, bit1 select, bit2 draft
-  static const int skip = [] {
+  // phase selection for timing breakdowns (sa_iteration_args::phases; SA_ITER_SKIP overrides in dev runs)
+  static const int env_skip = [] {
     const char* v = getenv("SA_ITER_SKIP");
-    return v ? atoi(v) : 0;
+    return v ? atoi(v) : -1;
   }();
+  const int skip = env_skip >= 0 ? env_skip : (a->phases ? static_cast<int>(~a->phases & 7u) : 0);
   SA_CUDA_CHECK(cudaEventRecord(r->ev_fork, main));
   SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
   for (int l = 0; l < L; ++l) {
@@ -558,7 +565,13 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
         SA_CUDA_CHECK(cudaMemsetAsync(fx, 0, sizeof(long long) * r->cfg.max_batch * r->ld, main));
         r->fx_dirty[l] = 0;
       }
-  if (!a->use_graph) return enqueue_iteration(r, a, main);
+  if (!a->use_graph) {
+    sa_status st = enqueue_iteration(r, a, main);
+    if (st == SA_OK && a->mode == SA_PER_LAYER && a->phases && (a->phases & SA_PHASE_VERIFY) &&
+        !(a->phases & SA_PHASE_SELECT))
+      for (int l = 0; l < r->cache->n_layers; ++l) r->fx_dirty[l] = 1;
+    return st;
+  }
   std::vector<char> key(sizeof(sa_iteration_args) + sizeof(int) + r->h_p0.size() * sizeof(int64_t) +
                         r->h_seq.size() * sizeof(int32_t));
   std::memcpy(key.data(), a, sizeof(*a));
@@ -566,10 +579,13 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
   std::memcpy(key.data() + sizeof(*a) + sizeof(int), r->h_p0.data(), r->h_p0.size() * sizeof(int64_t));
   std::memcpy(key.data() + sizeof(*a) + sizeof(int) + r->h_p0.size() * sizeof(int64_t), r->h_seq.data(),
               r->h_seq.size() * sizeof(int32_t));
-  if (!r->gexec || key != r->gkey) {
-    if (r->gexec) {
-      cudaGraphExecDestroy(r->gexec);
-      r->gexec = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  for (auto& kv : r->graphs)
+    if (kv.first == key) gexec = kv.second;
+  if (!gexec) {
+    if (r->graphs.size() >= 8) {  // bounded cache: drop the oldest
+      cudaGraphExecDestroy(r->graphs.front().second);
+      r->graphs.erase(r->graphs.begin());
     }
     cudaGraph_t graph = nullptr;
     SA_CUDA_CHECK(cudaStreamBeginCapture(r->capture, cudaStreamCaptureModeThreadLocal));
@@ -580,12 +596,15 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
       return st;
     }
     if (e != cudaSuccess) return sa::cuda_fail(e, "cudaStreamEndCapture");
-    e = cudaGraphInstantiate(&r->gexec, graph, 0);
+    e = cudaGraphInstantiate(&gexec, graph, 0);
     cudaGraphDestroy(graph);
     if (e != cudaSuccess) return sa::cuda_fail(e, "cudaGraphInstantiate");
-    r->gkey = std::move(key);
+    r->graphs.emplace_back(std::move(key), gexec);
   }
-  SA_CUDA_CHECK(cudaGraphLaunch(r->gexec, main));
+  SA_CUDA_CHECK(cudaGraphLaunch(gexec, main));
+  // a verify without its select leaves per-layer sums unconsumed: zero them before the next use
+  if (a->mode == SA_PER_LAYER && a->phases && (a->phases & SA_PHASE_VERIFY) && !(a->phases & SA_PHASE_SELECT))
+    for (int l = 0; l < r->cache->n_layers; ++l) r->fx_dirty[l] = 1;
   return SA_OK;
 }
 

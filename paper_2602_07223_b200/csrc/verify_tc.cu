@@ -91,7 +91,7 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
     if (p.trace && cta_lin < 1024) {                                                            \
       unsigned long long gt_;                                                                   \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                                   \
-      p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + (k)] = gt_;                          \
+      p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + (k)] = gt_;                          \
     }                                                                                           \
   } while (0)
 
@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(384, 1)
   if (p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin] = gt;
+    p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin] = gt;
+    for (int k = 4; k < 16; ++k) p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + k] = 0;
   }
   const uint32_t tmem = *tmem_slot;
 
@@ -283,24 +284,25 @@ __global__ void __launch_bounds__(384, 1)
         }
         if (done && nk == q_end && nv == nk) break;
       }
-      // keep HBM busy across the layer boundary: pull the next layer's first tiles of this unit
-      // (the chunk the next layer's CTA `split` claims statically) into L2 while this layer drains
-      if (p.next_layer >= 0 && split < n_chunks) {
-        for (int t = 0; t < min(chunk_tiles, n_pref - split * chunk_tiles); ++t) {
-          const int pos = (split * chunk_tiles + t) * C::kTile;
-          const int row = (((p.next_layer * p.cache.num_pages + bt[pos >> p.cache.page_shift]) * p.cache.n_kv_heads + g)
-                           << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1));
-          tma_prefetch_l2_2d(&tmk, 0, row);
-          tma_prefetch_l2_2d(&tmk, 64, row);
-          tma_prefetch_l2_2d(&tmv, 0, row);
-          tma_prefetch_l2_2d(&tmv, 64, row);
-        }
-      }
       // end of stream for both softmax warpgroups and the MMA issuer
       for (int e = 0; e < 2; ++e) {
         tile_pos[(nk + e) % C::kPosRing] = -1;
         mbar_arrive(&pos_bar[(nk + e) % C::kPosRing]);
       }
+      // keep HBM busy across the layer boundary: pull the next layer's first chunks of this unit
+      // into L2 while this layer drains (chunks split, split + n_splits, ...: the ones the next
+      // layer's CTAs claim first)
+      if (p.next_layer >= 0)
+        for (int c = split, i = 0; i < p.next_pf && c < n_chunks; c += p.n_splits, ++i)
+          for (int t = 0; t < min(chunk_tiles, n_pref - c * chunk_tiles); ++t) {
+            const int pos = (c * chunk_tiles + t) * C::kTile;
+            const int row = (((p.next_layer * p.cache.num_pages + bt[pos >> p.cache.page_shift]) * p.cache.n_kv_heads + g)
+                             << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1));
+            tma_prefetch_l2_2d(&tmk, 0, row);
+            tma_prefetch_l2_2d(&tmk, 64, row);
+            tma_prefetch_l2_2d(&tmv, 0, row);
+            tma_prefetch_l2_2d(&tmv, 64, row);
+          }
     }
   } else {
     // ------------------------- warps 1-3: dependency wait, Q staging, fused window append (96 threads,
@@ -571,8 +573,8 @@ __global__ void __launch_bounds__(384, 1)
     if (p.trace && ts == 0 && wg == 0 && cta_lin < 1024) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + 2] = gt;  // main loop done
-      p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + 3] = static_cast<unsigned long long>(i) | (static_cast<unsigned long long>(split) << 32);
+      p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + 2] = gt;  // main loop done
+      p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + 3] = static_cast<unsigned long long>(i) | (static_cast<unsigned long long>(split) << 32);
     }
     const int my_tiles = i;  // tiles this warpgroup processed
     if (ts == 0) ntiles_wg[wg] = my_tiles;
@@ -670,33 +672,57 @@ __global__ void __launch_bounds__(384, 1)
           const float4* so = reinterpret_cast<const float4*>(smem);
           float2* sml = reinterpret_cast<float2*>(smem + p.n_splits * obytes);  // [split][N] (m, l)
           const int t256 = wg * 128 + ts;
-          if (t256 < M) {  // merge weights w_s = 2^(m_s - m*) / L in place of m_s
+          if (t256 < M) {  // merge weights w_s = 2^(m_s - m*) / L in place of m_s (batched loads)
             float mstar = -INFINITY;
-            for (int s2 = 0; s2 < p.n_splits; ++s2) mstar = fmaxf(mstar, sml[s2 * N + t256].x);
+            for (int s0 = 0; s0 < p.n_splits; s0 += 8) {
+              float mm[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) mm[u] = s0 + u < p.n_splits ? sml[(s0 + u) * N + t256].x : -INFINITY;
+#pragma unroll
+              for (int u = 0; u < 8; ++u) mstar = fmaxf(mstar, mm[u]);
+            }
             float lsum = 0.f;
-            for (int s2 = 0; s2 < p.n_splits; ++s2) {
-              const float2 v = sml[s2 * N + t256];
-              const float f = v.x == -INFINITY ? 0.f : fast_exp2(v.x - mstar);
-              sml[s2 * N + t256].x = f;
-              lsum += v.y * f;
+            for (int s0 = 0; s0 < p.n_splits; s0 += 8) {
+              float2 v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[u] = s0 + u < p.n_splits ? sml[(s0 + u) * N + t256] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const float f = v[u].x == -INFINITY ? 0.f : fast_exp2(v[u].x - mstar);
+                if (s0 + u < p.n_splits) sml[(s0 + u) * N + t256].x = f;
+                lsum += v[u].y * f;
+              }
             }
             const float inv = 1.f / lsum;
             for (int s2 = 0; s2 < p.n_splits; ++s2) sml[s2 * N + t256].x *= inv;
           }
           named_bar_sync(1, 256);
+          if (wg == 0 && ts == 0) SA_TSTAMP(8);
           for (int it = t256; it < M * 32; it += 256) {
             const int row = it >> 5, c4 = it & 31;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s2 = 0; s2 < p.n_splits; ++s2) {
-              const float4 v = so[(s2 * M + row) * 32 + c4];
-              const float w = sml[s2 * N + row].x;
-              acc.x = fmaf(v.x, w, acc.x);
-              acc.y = fmaf(v.y, w, acc.y);
-              acc.z = fmaf(v.z, w, acc.z);
-              acc.w = fmaf(v.w, w, acc.w);
+            float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+            for (int s0 = 0; s0 < p.n_splits; s0 += 8) {  // 8 independent smem loads per batch
+              float4 v[8];
+              float w[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const bool ok = s0 + u < p.n_splits;
+                v[u] = ok ? so[((s0 + u) * M + row) * 32 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+                w[u] = ok ? sml[(s0 + u) * N + row].x : 0.f;
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                float4& a = acc[u & 1];
+                a.x = fmaf(v[u].x, w[u], a.x);
+                a.y = fmaf(v[u].y, w[u], a.y);
+                a.z = fmaf(v[u].z, w[u], a.z);
+                a.w = fmaf(v[u].w, w[u], a.w);
+              }
             }
-            reinterpret_cast<float4*>(out_unit + static_cast<size_t>(row) * 128)[c4] = acc;
+            reinterpret_cast<float4*>(out_unit + static_cast<size_t>(row) * 128)[c4] =
+                make_float4(acc[0].x + acc[1].x, acc[0].y + acc[1].y, acc[0].z + acc[1].z, acc[0].w + acc[1].w);
           }
+          if (wg == 0 && ts == 0) SA_TSTAMP(9);
           if (wg == 0 && ts == 0) p.counters[unit] = 0;  // re-arm for the next launch
         } else {
           // too many splits for shared memory: latency-aware merge straight from L2
@@ -712,7 +738,7 @@ __global__ void __launch_bounds__(384, 1)
   if (p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[1024 + (p.layer & 63) * 8192 + 8 * cta_lin + 1] = gt;
+    p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + 1] = gt;
   }
   if (warp == 1) {
     tc_fence_after();

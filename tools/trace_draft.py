@@ -51,7 +51,7 @@ f = lib().sa_dev_trace_dump
 f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
 assert f(path.encode()) == 0
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
-dr = raw[1024 + 64 * 8192:].reshape(8, 64, 512, 16)
+dr = raw[1024 + 64 * 16384:].reshape(8, 64, 512, 16)
 t0 = None
 prev = None
 print(f"{'step':>4s} {'layer':>5s} {'start':>7s} {'st_max':>7s} | after wait med/max | gathered med/max | computed med/max | end med/max | dt")
@@ -75,7 +75,7 @@ for j in range(gamma):
                   f"pushed {np.median(v(6)):7.2f} inbox {np.median(v(7)):7.2f}/{v(7).max():7.2f}")
 
 # verify phase on the same clock (globaltimer): last layer's end vs the first draft's start
-vt = raw[1024:1024 + 64 * 8192].reshape(64, 1024, 8)
+vt = raw[1024:1024 + 64 * 16384].reshape(64, 1024, 16)
 v_st = [vt[l][vt[l][:, 0] > 0][:, 0].min() for l in range(L) if (vt[l][:, 0] > 0).any()]
 v_en = [vt[l][vt[l][:, 0] > 0][:, 1].max() for l in range(L) if (vt[l][:, 0] > 0).any()]
 if v_st:

@@ -54,7 +54,7 @@ t0 = None
 print(f"{'layer':>5s} {'start':>8s} {'st_med':>8s} {'loop_med':>8s} {'loop_max':>8s} {'end_med':>8s} {'end_max':>8s} {'dt':>7s}")
 prev = None
 for l in range(min(L, 64)):
-    blk = raw[1024 + l * 8192: 1024 + (l + 1) * 8192].reshape(1024, 8)
+    blk = raw[1024 + l * 16384: 1024 + (l + 1) * 16384].reshape(1024, 16)
     blk = blk[blk[:, 0] > 0]
     if not len(blk):
         continue

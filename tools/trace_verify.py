@@ -36,7 +36,7 @@ f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
 assert f(dump.encode()) == 0
 raw = np.fromfile(dump, dtype=np.uint64).astype(np.int64)
 ev = raw[:1024].reshape(16, 64)
-se = raw[1024:1024 + 8192].reshape(1024, 8)
+se = raw[1024:1024 + 16384].reshape(1024, 16)
 se = se[se[:, 0] > 0]
 g0 = se[:, 0].min()
 rel = lambda k: (se[:, k] - g0) / 1e3  # noqa: E731
@@ -51,8 +51,10 @@ print(f"epilogue medians (us): loop_end->pv_done {np.median(pv - ml):.2f}  pv_do
       f"{np.median((en - cnt)[has]):.2f}")
 mg = se[:, 7] > 0
 if mg.any():
-    print(f"mergers {mg.sum()}: counted->inputs_landed med {np.median((mrg - cnt)[mg]):.2f}  landed->end med "
-          f"{np.median((en - mrg)[mg]):.2f}  merger end max {en[mg].max():.2f}")
+    w8, c9 = rel(8), rel(9)
+    print(f"mergers {mg.sum()}: counted->inputs_landed med {np.median((mrg - cnt)[mg]):.2f}  landed->weights "
+          f"{np.median((w8 - mrg)[mg]):.2f}  weights->combined {np.median((c9 - w8)[mg]):.2f}  combined->end "
+          f"{np.median((en - c9)[mg]):.2f}  merger end max {en[mg].max():.2f}")
 order = np.argsort(en)[-8:]
 print("slowest CTAs (lin, split, wg0 tiles, start, loop_end, end):",
       [(int(i), int(split[i]), int(tiles[i]), round(float(st[i]), 2), round(float(ml[i]), 2), round(float(en[i]), 2)) for i in order])
