@@ -228,12 +228,12 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
 
   int64_t* src_row = reinterpret_cast<int64_t*>(smem + DCfg::kOffRow);  // -1: new row (k_new), -2: zero fill
   // pre: true -> rows that exist before this launch (gathered ahead of the dependency wait)
-  auto is_pre = [&](int v) { return v < k || (v != new_v && old_tail_ready); };
+  auto is_pre = [&](int v) { return v < k || (v == new_v ? !p.k_new : old_tail_ready); };
   auto resolve = [&](int r0, int rows, bool pre_pass) {
     for (int r = tid; r < rows; r += nthr) {
       const int v = v_begin + r0 + r;
-      if (v >= v_end) {
-        if (!pre_pass) src_row[r] = -2;
+      if (v >= v_end) {  // zero fill: known before the dependency
+        if (pre_pass) src_row[r] = -2;
         continue;
       }
       if (is_pre(v) != pre_pass) continue;
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
       const int r = i >> 4, ch = i & 15;
       const int v = v_begin + r0 + r;
       const bool in = v < v_end;
-      if (in ? (is_pre(v) != pre_pass) : pre_pass) continue;
+      if (in ? (is_pre(v) != pre_pass) : !pre_pass) continue;
       const int tile = r >> 6, rr = r & 63;
       const uint32_t off = tile * DCfg::kTileBytes + swz(rr, ch, DCfg::kHalf);
       const int64_t row = src_row[r];
@@ -278,13 +278,21 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
   pdl_wait();  // previous layer complete: q and this step's new row are valid
   pdl_launch_dependents();
   dtrace(p, 1);
-  // post-wait rows of round 0 (this step's new row, zero fill) go out first, so their round trip
-  // overlaps the query loads below
+  // post-wait rows of round 0: this step's new row (straight from k_new/v_new, one warp, no
+  // barrier) — its round trip overlaps the query loads below; the general path only when earlier
+  // steps' rows may still be in flight (a one-layer chain)
   const int rows0_pad = (min(kRoundRows, n) + 15) & ~15;
-  __syncthreads();  // src_row of the pre pass consumed by every thread
-  resolve(0, rows0_pad, false);
-  __syncthreads();
-  gather(0, rows0_pad, false);
+  if (!old_tail_ready) {
+    __syncthreads();  // src_row of the pre pass consumed by every thread
+    resolve(0, rows0_pad, false);
+    __syncthreads();
+    gather(0, rows0_pad, false);
+  } else if (p.k_new && warp == nwarps - 1 && new_v >= v_begin && new_v < v_begin + rows0_pad && new_v < v_end) {
+    const int r = new_v - v_begin, ch = lane & 15;
+    const uint32_t off = (r >> 6) * DCfg::kTileBytes + swz(r & 63, ch, DCfg::kHalf);
+    const __nv_bfloat16* src = (lane < 16 ? p.k_new : p.v_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128 + ch * 8;
+    cp_async_16(smem + (lane < 16 ? 0 : DCfg::kOffV) + off, src, 16);
+  }
   cp_async_commit();
   DraftWarp w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);

@@ -79,7 +79,11 @@ struct VerifyParams {
   int n_splits, chunk;
   float* part_o;   // [B*Hkv][n_splits][MT*16][128]
   float* part_ml;  // [B*Hkv][n_splits][MT*16][2]
-  int* counters;   // [B*Hkv]
+  float* part_g;   // [B*Hkv][n_groups][N][128] group partials (two-level merge)
+  float* part_gml; // [B*Hkv][n_groups][N][2]
+  int n_groups, group_size;
+  int no_prefill;  // dev knob
+  int* counters;   // [B*Hkv][32]: [0] groups arrived, [1+g] splits of group g arrived
   int* chunk_ctr;  // [B*Hkv] dynamic chunk claims (tcgen05 verify), re-armed by the merging CTA
   unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production
   int use_pdl;  // programmatic dependent launch after the previous layer's verify (iteration graph)
@@ -132,6 +136,7 @@ int draft_max_splits();
 int draft_round_rows();
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 size_t verify_smem_bytes(int MT);
+int verify_tc_merge_capacity(int M);  // bytes of smem a merge may fill (tcgen05 verify, rows M)
 int verify_max_ctas_per_sm(int MT);
 
 }  // namespace sa

@@ -102,6 +102,78 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
       p.trace[(e) * 64 + (t)] = clock64();                                                      \
   } while (0)  // log2 units: p <= 2^8 before a forced max update
 
+// Merge `cnt` split partials of one unit (O rows [N][128] unnormalised, (m, l) per row, both in the
+// partial layout at src_o / src_ml with per-partial strides N*128 / N*2 floats) with bulk copies into
+// the idle ring buffers.  normalize: rows O/l -> dst_o (row stride 128);  else the merged partial
+// (O, m*, l) -> dst_o / dst_ml in the same partial layout (the next merge level reads it).
+// Called by the 256 softmax threads (t256); `bar` / `parity` is this use of the merge mbarrier.
+__device__ __forceinline__ void merge_partials(uint8_t* smem, uint32_t smem_cap, uint64_t* bar, uint32_t parity,
+                                               const float* src_o, const float* src_ml, int cnt, int N, int M,
+                                               bool normalize, float* dst_o, float* dst_ml, int t256) {
+  const uint32_t obytes = static_cast<uint32_t>(M) * 512u;
+  const uint32_t mlbytes = static_cast<uint32_t>(cnt) * N * 8u;
+  (void)smem_cap;
+  if (t256 == 0) {
+    fence_proxy_async();  // generic writes of the other CTAs (acquired by the caller) -> async-proxy reads
+    mbar_expect_tx(bar, cnt * obytes + mlbytes);
+    for (int s2 = 0; s2 < cnt; ++s2) bulk_load(smem + s2 * obytes, src_o + static_cast<size_t>(s2) * N * 128, obytes, bar);
+    bulk_load(smem + cnt * obytes, src_ml, mlbytes, bar);
+  }
+  mbar_wait(bar, parity);
+  const float4* so = reinterpret_cast<const float4*>(smem);
+  float2* sml = reinterpret_cast<float2*>(smem + cnt * obytes);  // [partial][N] (m, l)
+  if (t256 < M) {  // weights w_s = 2^(m_s - m*) (/ L when normalising) in place of m_s
+    float mstar = -INFINITY;
+    for (int s0 = 0; s0 < cnt; s0 += 16) {
+      float mm[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) mm[u] = s0 + u < cnt ? sml[(s0 + u) * N + t256].x : -INFINITY;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) mstar = fmaxf(mstar, mm[u]);
+    }
+    float lsum = 0.f;
+    for (int s0 = 0; s0 < cnt; s0 += 16) {
+      float2 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = s0 + u < cnt ? sml[(s0 + u) * N + t256] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float f = v[u].x == -INFINITY ? 0.f : fast_exp2(v[u].x - mstar);
+        lsum += v[u].y * f;
+        if (s0 + u < cnt) sml[(s0 + u) * N + t256].x = f;
+      }
+    }
+    const float inv = normalize ? 1.f / lsum : 1.f;
+    if (normalize)
+      for (int s2 = 0; s2 < cnt; ++s2) sml[s2 * N + t256].x *= inv;
+    if (!normalize) {
+      dst_ml[t256 * 2] = mstar;
+      dst_ml[t256 * 2 + 1] = lsum;
+    }
+  }
+  named_bar_sync(1, 256);
+  for (int it = t256; it < M * 32; it += 256) {
+    const int row = it >> 5, c4 = it & 31;
+    float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+    for (int s0 = 0; s0 < cnt; s0 += 8) {  // 8 independent smem loads per batch
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (s0 + u < cnt) {
+          const float4 v = so[((s0 + u) * M + row) * 32 + c4];
+          const float w = sml[(s0 + u) * N + row].x;
+          float4& a = acc[u & 1];
+          a.x = fmaf(v.x, w, a.x);
+          a.y = fmaf(v.y, w, a.y);
+          a.z = fmaf(v.z, w, a.z);
+          a.w = fmaf(v.w, w, a.w);
+        }
+      }
+    }
+    reinterpret_cast<float4*>(dst_o + static_cast<size_t>(row) * 128)[c4] =
+        make_float4(acc[0].x + acc[1].x, acc[0].y + acc[1].y, acc[0].z + acc[1].z, acc[0].w + acc[1].w);
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(384, 1)
     verify_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
@@ -213,6 +285,7 @@ __global__ void __launch_bounds__(384, 1)
       tma_prefetch_desc(&tmk);
       tma_prefetch_desc(&tmv);
       const uint64_t pol = policy_evict_first();
+      if (p.no_prefill) mbar_wait(dep_bar, 0);  // dev knob: no ring prefill before the dependency
       // tile stream of this CTA: window tiles (last split), then its chunks; pring holds positions
       int q_end = 0, cur_chunk = -1, cur_tile = 0, claims = 0, pending = 0;
       bool exhausted = false, done = false, dep_seen = false, win_added = false;
@@ -644,93 +717,57 @@ __global__ void __launch_bounds__(384, 1)
     if (single) {
       if (wg == 0 && ts == 0) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
     } else {
-      // arrival: one fence + one atomic per CTA after the CTA-wide barrier (cumulativity)
+      // Two-level merge (groups of <= 16 splits, at most 16 groups): the last-arriving CTA of each
+      // group merges that group's partials into a group partial; the last-arriving group merger
+      // merges the group partials and normalises.  Arrival: one acq_rel atomic per CTA after the
+      // CTA-wide barrier (release of this CTA's partial stores; acquire of everyone else's).
+      const int n_groups = p.n_groups;
+      const int gsize = p.group_size;
+      const int grp = split / gsize;
+      const int g_lo = grp * gsize, g_cnt = min(gsize, p.n_splits - g_lo);
+      const int t256 = wg * 128 + ts;
+      int* ctr = p.counters + unit * 32;  // [0]: unit (groups arrived), [1 + grp]: splits arrived
       named_bar_sync(1, 256);
-      if (wg == 0 && ts == 0) {
+      if (t256 == 0) {
         SA_TSTAMP(5);
-        int old;  // release: this CTA's partial stores (ordered by the barrier) before the count
-        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + unit) : "memory");
+        int old;
+        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr + 1 + grp) : "memory");
         *flag = old;
         SA_TSTAMP(6);
       }
       named_bar_sync(1, 256);
-      if (*flag == p.n_splits - 1) {
-        // last-arriving CTA merges the unit: all partials (M rows each) and (m, l) are pulled into
-        // the now idle ring buffers with bulk copies in flight together, then combined from smem
-        const uint32_t obytes = static_cast<uint32_t>(M) * 512u;
-        const uint32_t mlbytes = static_cast<uint32_t>(p.n_splits) * N * 8u;
-        if (static_cast<size_t>(p.n_splits) * obytes + mlbytes <= static_cast<size_t>(C::kOffBar)) {
-          if (wg == 0 && ts == 0) {
-            fence_proxy_async();  // generic writes of the other CTAs (acquired above) -> async-proxy reads
-            mbar_expect_tx(merge_bar, p.n_splits * obytes + mlbytes);
-            for (int s2 = 0; s2 < p.n_splits; ++s2)
-              bulk_load(smem + s2 * obytes, po + static_cast<size_t>(s2) * N * 128, obytes, merge_bar);
-            bulk_load(smem + p.n_splits * obytes, pml, mlbytes, merge_bar);
-          }
-          mbar_wait(merge_bar, 0);
-          if (wg == 0 && ts == 0) SA_TSTAMP(7);
-          const float4* so = reinterpret_cast<const float4*>(smem);
-          float2* sml = reinterpret_cast<float2*>(smem + p.n_splits * obytes);  // [split][N] (m, l)
-          const int t256 = wg * 128 + ts;
-          if (t256 < M) {  // merge weights w_s = 2^(m_s - m*) / L in place of m_s (batched loads)
-            float mstar = -INFINITY;
-            for (int s0 = 0; s0 < p.n_splits; s0 += 8) {
-              float mm[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) mm[u] = s0 + u < p.n_splits ? sml[(s0 + u) * N + t256].x : -INFINITY;
-#pragma unroll
-              for (int u = 0; u < 8; ++u) mstar = fmaxf(mstar, mm[u]);
-            }
-            float lsum = 0.f;
-            for (int s0 = 0; s0 < p.n_splits; s0 += 8) {
-              float2 v[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) v[u] = s0 + u < p.n_splits ? sml[(s0 + u) * N + t256] : make_float2(-INFINITY, 0.f);
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const float f = v[u].x == -INFINITY ? 0.f : fast_exp2(v[u].x - mstar);
-                if (s0 + u < p.n_splits) sml[(s0 + u) * N + t256].x = f;
-                lsum += v[u].y * f;
-              }
-            }
-            const float inv = 1.f / lsum;
-            for (int s2 = 0; s2 < p.n_splits; ++s2) sml[s2 * N + t256].x *= inv;
+      if (*flag == g_cnt - 1) {
+        const bool one_level = n_groups == 1;
+        float* pg = p.part_g + static_cast<size_t>(unit) * n_groups * N * 128;
+        float* pgml = p.part_gml + static_cast<size_t>(unit) * n_groups * N * 2;
+        merge_partials(smem, C::kOffBar, merge_bar, 0, po + static_cast<size_t>(g_lo) * N * 128,
+                       pml + static_cast<size_t>(g_lo) * N * 2, g_cnt, N, M, one_level,
+                       one_level ? out_unit : pg + static_cast<size_t>(grp) * N * 128,
+                       pgml + static_cast<size_t>(grp) * N * 2, t256);
+        if (t256 == 0) {
+          SA_TSTAMP(7);
+          ctr[1 + grp] = 0;  // re-arm
+        }
+        if (!one_level) {
+          named_bar_sync(1, 256);  // group partial stored by every thread
+          if (t256 == 0) {
+            int old;
+            asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+            *flag = old;
           }
           named_bar_sync(1, 256);
-          if (wg == 0 && ts == 0) SA_TSTAMP(8);
-          for (int it = t256; it < M * 32; it += 256) {
-            const int row = it >> 5, c4 = it & 31;
-            float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-            for (int s0 = 0; s0 < p.n_splits; s0 += 8) {  // 8 independent smem loads per batch
-              float4 v[8];
-              float w[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const bool ok = s0 + u < p.n_splits;
-                v[u] = ok ? so[((s0 + u) * M + row) * 32 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
-                w[u] = ok ? sml[(s0 + u) * N + row].x : 0.f;
-              }
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                float4& a = acc[u & 1];
-                a.x = fmaf(v[u].x, w[u], a.x);
-                a.y = fmaf(v[u].y, w[u], a.y);
-                a.z = fmaf(v[u].z, w[u], a.z);
-                a.w = fmaf(v[u].w, w[u], a.w);
-              }
+          if (*flag == n_groups - 1) {
+            merge_partials(smem, C::kOffBar, merge_bar, 1, pg, pgml, n_groups, N, M, true, out_unit, nullptr, t256);
+            if (t256 == 0) {
+              SA_TSTAMP(9);
+              ctr[0] = 0;
+              p.chunk_ctr[unit] = 0;  // re-arm chunk claims
             }
-            reinterpret_cast<float4*>(out_unit + static_cast<size_t>(row) * 128)[c4] =
-                make_float4(acc[0].x + acc[1].x, acc[0].y + acc[1].y, acc[0].z + acc[1].z, acc[0].w + acc[1].w);
           }
-          if (wg == 0 && ts == 0) SA_TSTAMP(9);
-          if (wg == 0 && ts == 0) p.counters[unit] = 0;  // re-arm for the next launch
-        } else {
-          // too many splits for shared memory: latency-aware merge straight from L2
-          combine_splits(po, pml, p.n_splits, N, M, p.counters + unit, flag, reinterpret_cast<float*>(smem),
-                         wg * 128 + ts, 256, 1, [&](int row) { return out_unit + static_cast<size_t>(row) * 128; },
-                         /*arrived=*/true);
+        } else if (t256 == 0) {
+          SA_TSTAMP(9);
+          p.chunk_ctr[unit] = 0;
         }
-        if (wg == 0 && ts == 0) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
       }
     }
   }
@@ -766,6 +803,15 @@ static cudaError_t launch_n(const VerifyParams& p, const CUtensorMap& tk, const 
   cfg.attrs = attr;
   cfg.numAttrs = p.use_pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, tk, tv, p);
+}
+
+int verify_tc_merge_capacity(int M) {
+  switch ((M + 2 + 15) / 16 * 16) {
+    case 16: return TCfg<16>::kOffBar;
+    case 32: return TCfg<32>::kOffBar;
+    case 48: return TCfg<48>::kOffBar;
+    default: return TCfg<64>::kOffBar;
+  }
 }
 
 cudaError_t launch_verify_tc(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s) {

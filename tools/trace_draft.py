@@ -46,7 +46,7 @@ with torch.cuda.stream(st):
     for _ in range(4):
         r.iteration(args, stream=st)
 torch.cuda.synchronize()
-path = os.path.join(ROOT, "gpurun_out", "trace_draft.bin")
+path = "/tmp/sa_trace_draft.bin"
 f = lib().sa_dev_trace_dump
 f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
 assert f(path.encode()) == 0
