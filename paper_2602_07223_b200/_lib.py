@@ -6,7 +6,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(HERE, "lib", "libspecattn_b200.so")
+lib_path = os.environ.get("SA_LIB_PATH") or os.path.join(HERE, "lib", "libspecattn_b200.so")  # env: dev A/B only
 
 SA_OK = 0
 STATUS = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 4: "length_error",

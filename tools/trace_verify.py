@@ -46,6 +46,8 @@ print(f"CTAs {len(se)}: start us min/med/max {st.min():.2f}/{np.median(st):.2f}/
       f"main-loop end min/med/max {ml.min():.2f}/{np.median(ml):.2f}/{ml.max():.2f}; "
       f"end min/med/max {en.min():.2f}/{np.median(en):.2f}/{en.max():.2f}")
 has = se[:, 5] > 0
+print(f"epilogue detail (us): pv_done->both_wg {np.median((rel(10) - pv)[has]):.2f}  ->fin_l {np.median((rel(11) - rel(10))[has]):.2f}  "
+      f"->O_stored {np.median((rel(12) - rel(11))[has]):.2f}  ->barrier {np.median((sto - rel(12))[has]):.2f}")
 print(f"epilogue medians (us): loop_end->pv_done {np.median(pv - ml):.2f}  pv_done->partial_stored "
       f"{np.median((sto - pv)[has]):.2f}  stored->counted {np.median((cnt - sto)[has]):.2f}  counted->end(non-merger) "
       f"{np.median((en - cnt)[has]):.2f}")
