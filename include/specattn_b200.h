@@ -210,7 +210,7 @@ SA_API sa_status sa_draft_attention(sa_runner* r, const sa_draft_args* a, void* 
  * use_graph != 0 captures the launch sequence into a CUDA graph on first use and replays it. */
 typedef struct sa_iteration_args {
   int32_t gamma;
-  sa_strategy strategy;     /* SA_COLLECT2 or SA_ALL_DRAFT on this path */
+  sa_strategy strategy;     /* SA_COLLECT2, SA_ALL_DRAFT or SA_LAST_ACCEPTED */
   sa_select_mode mode;
   float scale;
   const void *qv, *kv_new, *vv_new, *qd, *kd_new, *vd_new;
@@ -218,6 +218,8 @@ typedef struct sa_iteration_args {
   int32_t use_graph;
   uint32_t phases;          /* 0 = all; else a mask of SA_PHASE_* (timing breakdowns: the phases left
                                out are skipped, their buffers are left as the last run wrote them) */
+  int32_t accepted;         /* SA_LAST_ACCEPTED: drafts accepted by the previous verify (row a+1,
+                               selection.cpp:198-207); 0 <= accepted <= gamma */
 } sa_iteration_args;
 #define SA_PHASE_VERIFY 1u
 #define SA_PHASE_SELECT 2u
@@ -230,6 +232,22 @@ SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_
  * verify kernel records per-CTA start / main-loop-end / end timestamps per layer; this writes the
  * trace buffer to `path` after a device sync.  Returns 0 on success, < 0 otherwise. */
 SA_API int sa_dev_trace_dump(const char* path);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * The path's only collective: when a layer's KV heads are sharded over several GPUs (one process
+ * per GPU) and selection is per layer, the per-layer fixed-point column sums are all-reduced over
+ * the head group between verify and select (int64 sum: exact, order-independent).  NCCL is
+ * loaded at run time (libnccl.so.2).  A group of one rank needs no NCCL. */
+typedef struct sa_comm sa_comm;
+/* 128-byte NCCL unique id, created on one rank and shared with the group out of band. */
+SA_API sa_status sa_comm_unique_id(void* id_out_128);
+SA_API sa_status sa_comm_create(const void* id_128, int32_t nranks, int32_t rank, sa_comm** out);
+SA_API sa_status sa_comm_destroy(sa_comm* comm);
+/* Attach the head-group communicator: sa_iteration_run then exchanges every layer's sums before
+ * its select (per-layer mode).  NULL detaches. */
+SA_API sa_status sa_runner_set_comm(sa_runner* r, sa_comm* comm);
+/* Exchange one slot's per-layer sums on `stream` (direct-API use between verify and select). */
+SA_API sa_status sa_exchange_layer_scores(sa_runner* r, int32_t layer_slot, void* stream);
 
 /* Reference helper: selection_k (selection.cpp:63-66). */
 SA_API int64_t sa_selection_k(double sparse_ratio, int64_t prefix_len, int64_t k_min);

@@ -7,8 +7,8 @@ shared library is missing or no CUDA device is present, every entry point raises
 """
 from ._lib import (  # noqa: F401
     ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS, LAST_ACCEPTED, PER_KV_HEAD, PER_LAYER, PHASE_DRAFT, PHASE_SELECT,
-    PHASE_VERIFY, Cache, Runner, SpecAttnError, build, lib, lib_path, selection_k,
+    PHASE_VERIFY, Cache, Comm, Runner, SpecAttnError, build, lib, lib_path, selection_k,
 )
 
-__all__ = ["Cache", "Runner", "SpecAttnError", "build", "lib", "lib_path", "selection_k", "COLLECT2", "ALL_DRAFT",
+__all__ = ["Cache", "Comm", "Runner", "SpecAttnError", "build", "lib", "lib_path", "selection_k", "COLLECT2", "ALL_DRAFT",
            "LAST_ACCEPTED", "COLLECT2_WEIGHTS", "PER_LAYER", "PER_KV_HEAD", "PHASE_VERIFY", "PHASE_SELECT", "PHASE_DRAFT"]

@@ -56,7 +56,7 @@ class DraftArgs(C.Structure):
 class IterationArgs(C.Structure):
     _fields_ = [("gamma", _i32), ("strategy", C.c_int), ("mode", C.c_int), ("scale", _f32), ("qv", _vp),
                 ("kv_new", _vp), ("vv_new", _vp), ("qd", _vp), ("kd_new", _vp), ("vd_new", _vp), ("out_v", _vp),
-                ("out_d", _vp), ("use_graph", _i32), ("phases", _u32)]
+                ("out_d", _vp), ("use_graph", _i32), ("phases", _u32), ("accepted", _i32)]
 
 
 # exported symbol -> (restype, argtypes)
@@ -90,6 +90,11 @@ SIGNATURES = {
     "sa_iteration_run": (C.c_int, [_vp, C.POINTER(IterationArgs), _vp]),
     "sa_iteration_kernel_count": (_i64, [_vp, C.POINTER(IterationArgs)]),
     "sa_dev_trace_dump": (C.c_int, [C.c_char_p]),
+    "sa_comm_unique_id": (C.c_int, [_vp]),
+    "sa_comm_create": (C.c_int, [_vp, _i32, _i32, C.POINTER(_vp)]),
+    "sa_comm_destroy": (C.c_int, [_vp]),
+    "sa_runner_set_comm": (C.c_int, [_vp, _vp]),
+    "sa_exchange_layer_scores": (C.c_int, [_vp, _i32, _vp]),
 }
 
 _LIB = None
@@ -312,17 +317,51 @@ class Runner:
         _check(lib().sa_draft_attention(self.h, C.byref(a), _stream(stream)))
 
     def iteration_args(self, gamma, qv, kv_new, vv_new, qd, kd_new, vd_new, out_v, out_d, strategy=COLLECT2,
-                       mode=PER_LAYER, scale=None, use_graph=True, phases=0):
+                       mode=PER_LAYER, scale=None, use_graph=True, phases=0, accepted=0):
         if scale is None:
             scale = float((1.0 / 128 ** 0.5))
         return IterationArgs(gamma, strategy, mode, scale, _ptr(qv), _ptr(kv_new), _ptr(vv_new), _ptr(qd),
-                             _ptr(kd_new), _ptr(vd_new), _ptr(out_v), _ptr(out_d), int(use_graph), int(phases))
+                             _ptr(kd_new), _ptr(vd_new), _ptr(out_v), _ptr(out_d), int(use_graph), int(phases),
+                             int(accepted))
 
     def iteration(self, args: IterationArgs, stream=None):
         _check(lib().sa_iteration_run(self.h, C.byref(args), _stream(stream)))
 
+    def set_comm(self, comm: "Comm | None"):
+        """Attach the KV-head group communicator (per-layer score exchange inside the iteration)."""
+        self._comm = comm
+        _check(lib().sa_runner_set_comm(self.h, comm.h if comm is not None else None))
+
+    def exchange_layer_scores(self, slot, stream=None):
+        _check(lib().sa_exchange_layer_scores(self.h, slot, _stream(stream)))
+
     def iteration_kernel_count(self, args: IterationArgs) -> int:
         return int(lib().sa_iteration_kernel_count(self.h, C.byref(args)))
+
+
+class Comm:
+    """KV-head group communicator (sa_comm): NCCL over NVLink for the per-layer score exchange.
+    `unique_id` (128 bytes) comes from Comm.unique_id() on one rank of the group, shared out of band
+    (e.g. torch.distributed.broadcast_object_list)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().sa_comm_unique_id(buf))
+        return buf.raw
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        h = _vp()
+        _check(lib().sa_comm_create(buf, nranks, rank, C.byref(h)))
+        self.h, self.nranks, self.rank = h, nranks, rank
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sa_comm_destroy(self.h)
+            self.h = None
+
+    __del__ = close
 
 
 def cudart_memcpy(dst: int, src: int, nbytes: int) -> None:

@@ -129,6 +129,8 @@ struct SelectParams {
   int32_t* k_out;  // [B][n_sets]
 };
 
+sa_status comm_allreduce_i64(sa_comm* c, long long* buf, size_t count, cudaStream_t s);
+
 cudaError_t launch_verify(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
 cudaError_t launch_verify_tc(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s);

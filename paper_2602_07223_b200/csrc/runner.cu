@@ -48,6 +48,7 @@ struct sa_runner {
   std::vector<cudaEvent_t> ev_v, ev_s;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<std::vector<char>, cudaGraphExec_t>> graphs;  // keyed by args + batch binding
+  sa_comm* comm = nullptr;  // KV-head group communicator (per-layer score exchange), may be null
 };
 
 namespace {
@@ -475,6 +476,21 @@ SA_API int sa_dev_trace_dump(const char* path) {
   return 0;
 }
 
+SA_API sa_status sa_runner_set_comm(sa_runner* r, sa_comm* comm) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  r->comm = comm;
+  for (auto& kv : r->graphs) cudaGraphExecDestroy(kv.second);  // captured graphs depend on it
+  r->graphs.clear();
+  return SA_OK;
+}
+
+SA_API sa_status sa_exchange_layer_scores(sa_runner* r, int32_t slot, void* stream) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  if (slot < 0 || slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "exchange: layer_slot");
+  long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, slot, nullptr));
+  return sa::comm_allreduce_i64(r->comm, fx, static_cast<size_t>(r->B) * r->ld, static_cast<cudaStream_t>(stream));
+}
+
 SA_API sa_status sa_verify_attention(sa_runner* r, const sa_verify_args* a, void* stream) {
   if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
   return verify_impl(r, a, static_cast<cudaStream_t>(stream));
@@ -498,7 +514,11 @@ SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_
 
 static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cudaStream_t main) {
   const int L = static_cast<int>(r->cache->n_layers), B = r->B, R = a->gamma + 1;
-  const uint32_t mask = a->strategy == SA_ALL_DRAFT ? ((1u << R) - 1u) : (1u | (1u << a->gamma));
+  // score rows (bit r = row label r+1): AllDraft all gamma+1 rows (selection.cpp:183-185), Collect-2
+  // {1, gamma+1} (:187-196), LastAccepted the single row a+1 (:198-207)
+  const uint32_t mask = a->strategy == SA_ALL_DRAFT     ? ((1u << R) - 1u)
+                        : a->strategy == SA_LAST_ACCEPTED ? (1u << a->accepted)
+                                                           : (1u | (1u << a->gamma));
   const int rows_in_score = __builtin_popcount(mask);
   const size_t qv_l = static_cast<size_t>(B) * r->Hq * R * 128, kv_l = static_cast<size_t>(B) * R * r->Hkv * 128;
   const size_t qd_l = static_cast<size_t>(B) * r->Hq * 128, kd_l = static_cast<size_t>(B) * r->Hkv * 128;
@@ -537,8 +557,13 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     sel.layer_slot = l;
     sel.mode = a->mode;
     sel.rows_in_score = rows_in_score;
-    if ((skip & 2) == 0)
+    if ((skip & 2) == 0) {
+      if (r->comm && a->mode == SA_PER_LAYER) {  // §8e exchange: sums of the other KV-head shards
+        long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, l, nullptr));
+        if (sa_status st = sa::comm_allreduce_i64(r->comm, fx, static_cast<size_t>(B) * r->ld, r->side)) return st;
+      }
       if (sa_status st = select_impl(r, &sel, r->side)) return st;
+    }
     SA_CUDA_CHECK(cudaEventRecord(r->ev_s[l], r->side));
   }
   for (int j = 1; j <= a->gamma; ++j) {
@@ -568,8 +593,10 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
   if (!r || !a) return fail(SA_INVALID_ARGUMENT, "null argument");
   if (a->gamma < 0 || a->gamma + 1 > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "gamma out of range");
   if (a->gamma < 1) return fail(SA_INVALID_ARGUMENT, "DecodeParams: gamma must be >= 1");
-  if (a->strategy != SA_COLLECT2 && a->strategy != SA_ALL_DRAFT)
-    return fail(SA_NOT_SUPPORTED, "iteration: strategy must be collect2 or all_draft");
+  if (a->strategy != SA_COLLECT2 && a->strategy != SA_ALL_DRAFT && a->strategy != SA_LAST_ACCEPTED)
+    return fail(SA_NOT_SUPPORTED, "iteration: strategy must be collect2, all_draft or last_accepted");
+  if (a->strategy == SA_LAST_ACCEPTED && (a->accepted < 0 || a->accepted > a->gamma))
+    return fail(SA_INVALID_ARGUMENT, "select_last_accepted: row accepted+1 not collected");
   if (r->n_slots < r->cache->n_layers) return fail(SA_INVALID_ARGUMENT, "iteration needs n_layers_buf >= n_layers");
   if (!a->qv || !a->qd || !a->out_v || !a->out_d) return fail(SA_INVALID_ARGUMENT, "iteration: null buffer");
   cudaStream_t main = static_cast<cudaStream_t>(stream);

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 from oracle.counter_rng import normal_bf16
-from oracle.pyoracle import ALL_DRAFT, COLLECT2, scale_for
+from oracle.pyoracle import ALL_DRAFT, COLLECT2, LAST_ACCEPTED, scale_for
 
 from .helpers import D, Matched, check_selection, rel_err_elem, rel_err_rows, to_dev_bf16
 
@@ -277,8 +277,9 @@ def test_draft_parity(cuda, ref, mode):
 
 # ----------------------------------------------------------------------------------- iteration
 
-@pytest.mark.parametrize("strategy,mode,use_graph", [(COLLECT2, 0, True), (ALL_DRAFT, 1, False)])
-def test_iteration_parity(cuda, ref, strategy, mode, use_graph):
+@pytest.mark.parametrize("strategy,mode,use_graph,accepted", [(COLLECT2, 0, True, 0), (ALL_DRAFT, 1, False, 0),
+                                                                (LAST_ACCEPTED, 0, True, 2)])
+def test_iteration_parity(cuda, ref, strategy, mode, use_graph, accepted):
     """One full speculation iteration (verify -> select -> gamma drafts, all layers) through
     sa_iteration_run vs the reference composition (SURVEY.md §8d unit of work)."""
     torch = cuda
@@ -296,7 +297,7 @@ def test_iteration_parity(cuda, ref, strategy, mode, use_graph):
     out_d = torch.zeros((gamma, L, 1, Hq, D), dtype=torch.float32, device="cuda")
     dev = [to_dev_bf16(x) for x in (qv, kvn, vvn, qd, kdn, vdn)]
     args = r.iteration_args(gamma, *dev, out_v, out_d, strategy=strategy, mode=mode, scale=SCALE,
-                            use_graph=use_graph)
+                            use_graph=use_graph, accepted=accepted)
     assert r.iteration_kernel_count(args) == L * (2 + gamma)
     for _ in range(2):  # second launch replays the graph
         r.iteration(args)
@@ -306,7 +307,7 @@ def test_iteration_parity(cuda, ref, strategy, mode, use_graph):
     for t in range(R):
         kv.append(kvn[:, 0, t].reshape(L * Hkv, D), vvn[:, 0, t].reshape(L * Hkv, D))
     n_sets = 1 if mode == 0 else Hkv
-    rows = [1, R] if strategy == COLLECT2 else list(range(1, R + 1))
+    rows = {COLLECT2: [1, R], ALL_DRAFT: list(range(1, R + 1)), LAST_ACCEPTED: [accepted + 1]}[strategy]
     k = selection_k(0.07, p0, 16)
     sets_by_layer = []
     for layer in range(L):
@@ -319,6 +320,9 @@ def test_iteration_parity(cuda, ref, strategy, mode, use_graph):
             sc = ref.score_columns(l_ref[heads], list(range(1, R + 1)), rows)
             got = idx[0, s, : cnt[0, s]]
             check_selection(got, sc, k)
+            if strategy == LAST_ACCEPTED and mode == 0:  # the reference entry point itself (selection.cpp:198-207)
+                want = ref.select(LAST_ACCEPTED, l_ref, list(range(1, R + 1)), 0.07, 16, accepted=accepted)
+                assert len(want) == len(got) and len(set(want.tolist()) ^ set(got.tolist())) <= 2
             sets.append(got.astype(np.int64))
         sets_by_layer.append(sets)
     kv.truncate(p0)
@@ -371,3 +375,39 @@ def test_head_sharded_layer_scores_sum_exactly(cuda):
     i_full, c_full = full[1].selection(0, 1)
     i_a, c_a = a[1].selection(0, 1)
     assert c_full[0, 0] == c_a[0, 0] and np.array_equal(i_full[0, 0, :c_full[0, 0]], i_a[0, 0, :c_a[0, 0]])
+
+
+def test_iteration_with_score_exchange(cuda):
+    """§8e exchange wired into the iteration graph: a KV-head group communicator (one rank here, a
+    real NCCL communicator: the all-reduce runs inside the captured graph between every layer's
+    verify and select) leaves the selections bit-identical to a run without it."""
+    torch = cuda
+    from paper_2602_07223_b200 import Cache, Comm, Runner
+    L, Hkv, G, gamma, p0 = 2, 2, 4, 4, 1500
+    R, Hq = gamma + 1, Hkv * G
+    K = normal_bf16(97, 1, (p0, L * Hkv, D))
+    V = normal_bf16(97, 2, (p0, L * Hkv, D))
+    ins = [to_dev_bf16(normal_bf16(97, 3 + i, s)) for i, s in enumerate(
+        [(L, 1, Hq, R, D), (L, 1, R, Hkv, D), (L, 1, R, Hkv, D), (gamma, L, 1, Hq, D), (gamma, L, 1, Hkv, D),
+         (gamma, L, 1, Hkv, D)])]
+
+    def run(comm):
+        c = Cache(L, Hkv, D, p0 + 64, page_size=128)
+        c.append(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+        r = Runner(c, Hq, max_rows=R, max_prefix=p0)
+        r.set_batch([0], [p0])
+        if comm is not None:
+            r.set_comm(comm)
+        ov = torch.zeros((L, 1, Hq, R, D), dtype=torch.float32, device="cuda")
+        od = torch.zeros((gamma, L, 1, Hq, D), dtype=torch.float32, device="cuda")
+        a = r.iteration_args(gamma, *ins, ov, od, scale=SCALE, use_graph=True)
+        for _ in range(2):
+            r.iteration(a)
+        torch.cuda.synchronize()
+        return [r.selection(l, 1) for l in range(L)], ov.cpu().numpy(), od.cpu().numpy()
+
+    comm = Comm(Comm.unique_id(), 1, 0)
+    base, with_comm = run(None), run(comm)
+    for (i0, c0), (i1, c1) in zip(base[0], with_comm[0]):
+        assert np.array_equal(c0, c1) and np.array_equal(i0, i1)
+    assert np.array_equal(base[1], with_comm[1]) and np.array_equal(base[2], with_comm[2])
