@@ -183,6 +183,13 @@ typedef struct sa_select_args {
 } sa_select_args;
 SA_API sa_status sa_select_topk(sa_runner* r, const sa_select_args* a, void* stream);
 
+/* Collect2Weights metric (score_columns_weights, selection.cpp:110-135): from the raw prefix logits
+ * a verify wrote (sa_verify_args.logits, [B][Hq][n_rows][ld_logits] f32, rows = the collected score
+ * rows), the softmax-weight column scores for layer_slot, laid out for `mode` (per-layer fixed-point
+ * sums or per-KV-head fp32), ready for sa_select_topk with the same mode. */
+SA_API sa_status sa_score_weights(sa_runner* r, int32_t layer_slot, const float* logits, int64_t ld_logits,
+                                  int32_t n_rows, sa_select_mode mode, void* stream);
+
 /* Sparse draft attention for one layer (gather(T) ++ tail, then attend; kv_store.cpp:67-88,
  * attention.cpp:70-76): query of q-head h at position p0+step-1 attends to the
  * selected prefix T (layer_slot's index list; per-layer or per-KV-head) and the tail rows
@@ -210,7 +217,7 @@ SA_API sa_status sa_draft_attention(sa_runner* r, const sa_draft_args* a, void* 
  * use_graph != 0 captures the launch sequence into a CUDA graph on first use and replays it. */
 typedef struct sa_iteration_args {
   int32_t gamma;
-  sa_strategy strategy;     /* SA_COLLECT2, SA_ALL_DRAFT or SA_LAST_ACCEPTED */
+  sa_strategy strategy;     /* SA_COLLECT2, SA_ALL_DRAFT, SA_LAST_ACCEPTED or SA_COLLECT2_WEIGHTS */
   sa_select_mode mode;
   float scale;
   const void *qv, *kv_new, *vv_new, *qd, *kd_new, *vd_new;

@@ -90,6 +90,7 @@ SIGNATURES = {
     "sa_iteration_run": (C.c_int, [_vp, C.POINTER(IterationArgs), _vp]),
     "sa_iteration_kernel_count": (_i64, [_vp, C.POINTER(IterationArgs)]),
     "sa_dev_trace_dump": (C.c_int, [C.c_char_p]),
+    "sa_score_weights": (C.c_int, [_vp, _i32, _vp, _i64, _i32, C.c_int, _vp]),
     "sa_comm_unique_id": (C.c_int, [_vp]),
     "sa_comm_create": (C.c_int, [_vp, _i32, _i32, C.POINTER(_vp)]),
     "sa_comm_destroy": (C.c_int, [_vp]),
@@ -303,6 +304,11 @@ class Runner:
                        scale, score_row_mask, _ptr(out), _ptr(logits),
                        0 if logits is None else logits.shape[-1], collect_row_mask, score_layout)
         _check(lib().sa_verify_attention(self.h, C.byref(a), _stream(stream)))
+
+    def score_weights(self, layer_slot, logits, n_rows, mode=PER_LAYER, stream=None):
+        """Collect2Weights scores for layer_slot from a verify's raw logits [B][Hq][n_rows][ld]."""
+        _check(lib().sa_score_weights(self.h, layer_slot, _ptr(logits), logits.shape[-1], n_rows, mode,
+                                      _stream(stream)))
 
     def select(self, layer_slot, mode=PER_LAYER, rows_in_score=2, stream=None):
         a = SelectArgs(layer_slot, mode, rows_in_score)

@@ -130,6 +130,9 @@ struct SelectParams {
 };
 
 sa_status comm_allreduce_i64(sa_comm* c, long long* buf, size_t count, cudaStream_t s);
+cudaError_t launch_weights(const float* logits, int64_t ld, const int32_t* p0, int B, int Hq, int G, int n_rows,
+                           double scale, float2* stats, int n_sets, long long* fx, float* scores, int64_t ld_scores,
+                           int64_t max_p, cudaStream_t s);
 
 cudaError_t launch_verify(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);
 cudaError_t launch_verify_tc(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s);

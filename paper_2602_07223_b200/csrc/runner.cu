@@ -49,6 +49,9 @@ struct sa_runner {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::pair<std::vector<char>, cudaGraphExec_t>> graphs;  // keyed by args + batch binding
   sa_comm* comm = nullptr;  // KV-head group communicator (per-layer score exchange), may be null
+  // Collect2Weights: raw logits of the collected rows per slot ([max_batch][Hq][2][ld]), row stats
+  std::vector<float*> wlogits;
+  float2* wstats = nullptr;
 };
 
 namespace {
@@ -191,6 +194,8 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
 SA_API sa_status sa_runner_destroy(sa_runner* r) {
   if (!r) return SA_OK;
   for (auto& kv : r->graphs) cudaGraphExecDestroy(kv.second);
+  for (float* w : r->wlogits) cudaFree(w);
+  cudaFree(r->wstats);
   for (auto ev : r->ev_v) if (ev) cudaEventDestroy(ev);
   for (auto ev : r->ev_s) if (ev) cudaEventDestroy(ev);
   if (r->ev_fork) cudaEventDestroy(r->ev_fork);
@@ -476,6 +481,42 @@ SA_API int sa_dev_trace_dump(const char* path) {
   return 0;
 }
 
+static sa_status ensure_weight_buffers(sa_runner* r) {  // lazily: only the weights metric needs them
+  if (r->wlogits.empty()) r->wlogits.assign(r->n_slots, nullptr);
+  const size_t bytes = sizeof(float) * r->cfg.max_batch * r->Hq * 2 * r->ld;
+  for (auto& w : r->wlogits)
+    if (!w) SA_CUDA_CHECK(cudaMalloc(&w, bytes));
+  if (!r->wstats) SA_CUDA_CHECK(cudaMalloc(&r->wstats, sizeof(float2) * r->cfg.max_batch * r->Hq * r->cfg.max_rows));
+  return SA_OK;
+}
+
+static sa_status weights_impl(sa_runner* r, int32_t slot, const float* logits, int64_t ld, int32_t n_rows,
+                              sa_select_mode mode, cudaStream_t s) {
+  if (!logits) return fail(SA_INVALID_ARGUMENT, "score_weights: null logits");
+  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "score_weights: no batch bound");
+  if (slot < 0 || slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "score_weights: layer_slot");
+  if (n_rows < 1 || n_rows > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "score_columns_weights: empty row subset");
+  if (ld < r->p_max) return fail(SA_INVALID_ARGUMENT, "score_weights: ld_logits < prefix");
+  if (mode != SA_PER_LAYER && mode != SA_PER_KV_HEAD) return fail(SA_INVALID_ARGUMENT, "score_weights: mode");
+  if (!r->wstats) SA_CUDA_CHECK(cudaMalloc(&r->wstats, sizeof(float2) * r->cfg.max_batch * r->Hq * r->cfg.max_rows));
+  const int n_sets = mode == SA_PER_LAYER ? 1 : r->Hkv;
+  long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, slot, nullptr));
+  float* scores = sa_runner_scores(r, slot, nullptr);
+  const double scale = 1.0 / std::sqrt(static_cast<double>(r->cache->head_dim));  // selection.cpp:117
+  cudaError_t e = sa::launch_weights(logits, ld, r->d_p0, r->B, r->Hq, r->G, n_rows, scale, r->wstats, n_sets, fx,
+                                     scores, r->ld, r->p_max, s);
+  if (e != cudaSuccess) return sa::cuda_fail(e, "score_weights launch");
+  r->slot_layout[slot] = mode;
+  if (mode == SA_PER_LAYER) r->fx_dirty[slot] = 1;  // written (not accumulated); the select consumes it
+  return SA_OK;
+}
+
+SA_API sa_status sa_score_weights(sa_runner* r, int32_t slot, const float* logits, int64_t ld, int32_t n_rows,
+                                  sa_select_mode mode, void* stream) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  return weights_impl(r, slot, logits, ld, n_rows, mode, static_cast<cudaStream_t>(stream));
+}
+
 SA_API sa_status sa_runner_set_comm(sa_runner* r, sa_comm* comm) {
   if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
   r->comm = comm;
@@ -508,7 +549,8 @@ SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_
   if (!r || !a) return 0;
   const int64_t L = r->cache->n_layers;
   const uint32_t ph = a->phases ? a->phases : 7u;
-  return ((ph & SA_PHASE_VERIFY) ? L : 0) + ((ph & SA_PHASE_SELECT) ? L : 0) +
+  const int64_t sel_kernels = a->strategy == SA_COLLECT2_WEIGHTS ? 3 : 1;  // (+ row stats, weight scores)
+  return ((ph & SA_PHASE_VERIFY) ? L : 0) + ((ph & SA_PHASE_SELECT) ? sel_kernels * L : 0) +
          ((ph & SA_PHASE_DRAFT) ? static_cast<int64_t>(a->gamma) * L : 0);
 }
 
@@ -519,6 +561,7 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
   const uint32_t mask = a->strategy == SA_ALL_DRAFT     ? ((1u << R) - 1u)
                         : a->strategy == SA_LAST_ACCEPTED ? (1u << a->accepted)
                                                            : (1u | (1u << a->gamma));
+  const bool weights = a->strategy == SA_COLLECT2_WEIGHTS;  // rows {1, gamma+1}, softmax-weight metric
   const int rows_in_score = __builtin_popcount(mask);
   const size_t qv_l = static_cast<size_t>(B) * r->Hq * R * 128, kv_l = static_cast<size_t>(B) * R * r->Hkv * 128;
   const size_t qd_l = static_cast<size_t>(B) * r->Hq * 128, kd_l = static_cast<size_t>(B) * r->Hkv * 128;
@@ -545,8 +588,13 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     v.k_new = kvn ? kvn + l * kv_l : nullptr;
     v.v_new = vvn ? vvn + l * kv_l : nullptr;
     v.scale = a->scale;
-    v.score_row_mask = mask;
+    v.score_row_mask = weights ? 0u : mask;
     v.score_layout = a->mode;
+    if (weights) {  // LogitMatrix of the collected rows for the weights kernels
+      v.logits = r->wlogits[l];
+      v.ld_logits = r->ld;
+      v.collect_row_mask = mask;
+    }
     v.out = a->out_v + l * qv_l;
     if ((skip & 1) == 0)
       if (sa_status st = verify_impl(r, &v, main, /*pdl=*/l > 0, /*in_iteration=*/true, l + 1 < L ? l + 1 : -1))
@@ -558,6 +606,8 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     sel.mode = a->mode;
     sel.rows_in_score = rows_in_score;
     if ((skip & 2) == 0) {
+      if (weights)
+        if (sa_status st = weights_impl(r, l, r->wlogits[l], r->ld, rows_in_score, a->mode, r->side)) return st;
       if (r->comm && a->mode == SA_PER_LAYER) {  // §8e exchange: sums of the other KV-head shards
         long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, l, nullptr));
         if (sa_status st = sa::comm_allreduce_i64(r->comm, fx, static_cast<size_t>(B) * r->ld, r->side)) return st;
@@ -593,8 +643,11 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
   if (!r || !a) return fail(SA_INVALID_ARGUMENT, "null argument");
   if (a->gamma < 0 || a->gamma + 1 > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "gamma out of range");
   if (a->gamma < 1) return fail(SA_INVALID_ARGUMENT, "DecodeParams: gamma must be >= 1");
-  if (a->strategy != SA_COLLECT2 && a->strategy != SA_ALL_DRAFT && a->strategy != SA_LAST_ACCEPTED)
-    return fail(SA_NOT_SUPPORTED, "iteration: strategy must be collect2, all_draft or last_accepted");
+  if (a->strategy != SA_COLLECT2 && a->strategy != SA_ALL_DRAFT && a->strategy != SA_LAST_ACCEPTED &&
+      a->strategy != SA_COLLECT2_WEIGHTS)
+    return fail(SA_NOT_SUPPORTED, "iteration: unknown strategy");
+  if (a->strategy == SA_COLLECT2_WEIGHTS)
+    if (sa_status st = ensure_weight_buffers(r)) return st;  // (outside any graph capture)
   if (a->strategy == SA_LAST_ACCEPTED && (a->accepted < 0 || a->accepted > a->gamma))
     return fail(SA_INVALID_ARGUMENT, "select_last_accepted: row accepted+1 not collected");
   if (r->n_slots < r->cache->n_layers) return fail(SA_INVALID_ARGUMENT, "iteration needs n_layers_buf >= n_layers");

@@ -24,15 +24,17 @@ def rel_err_elem(gpu: np.ndarray, ref: np.ndarray, tau: float = 1e-2) -> float:
     return float((np.abs(gpu - ref) / np.maximum(np.abs(ref), floor)).max())
 
 
-def check_selection(gpu_idx, ref_scores, k, band_rel=2e-3):
-    """North-star index contract: |GPU| = k, GPU ⊇ {s > s_k + band}, GPU ⊆ {s >= s_k - band}."""
+def check_selection(gpu_idx, ref_scores, k, band_rel=2e-3, relative=False):
+    """North-star index contract: |GPU| = k, GPU ⊇ {s > s_k + band}, GPU ⊆ {s >= s_k - band};
+    band = band_rel * max(|s_k|, 1) (raw-logit scores) or band_rel * |s_k| (relative=True: softmax
+    weights, whose scale is ~1/p)."""
     gpu = np.asarray(gpu_idx, np.int64)
     assert len(gpu) == k, (len(gpu), k)
     assert np.all(np.diff(gpu) > 0), "indices must be strictly increasing"
     if k == 0:
         return True
     s_k = np.sort(ref_scores)[::-1][k - 1]
-    band = band_rel * max(abs(s_k), 1.0)
+    band = band_rel * (abs(s_k) if relative else max(abs(s_k), 1.0))
     must = np.nonzero(ref_scores > s_k + band)[0]
     allowed = np.nonzero(ref_scores >= s_k - band)[0]
     gs = set(gpu.tolist())

@@ -411,3 +411,66 @@ def test_iteration_with_score_exchange(cuda):
     for (i0, c0), (i1, c1) in zip(base[0], with_comm[0]):
         assert np.array_equal(c0, c1) and np.array_equal(i0, i1)
     assert np.array_equal(base[1], with_comm[1]) and np.array_equal(base[2], with_comm[2])
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_collect2_weights_selection(cuda, ref, mode):
+    """Collect2Weights (score_columns_weights, selection.cpp:110-135): softmax-weight scores from the
+    verify kernel's raw logits of rows {1, gamma+1}, then top-k — vs the reference's select."""
+    torch = cuda
+    from oracle.pyoracle import COLLECT2_WEIGHTS
+    Hkv, G, R, p0 = 4, 4, 5, 3000
+    m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=53, score_layout=mode)
+    l_ref = res[0][1]
+    _, _, selection_k = _lib()
+    lg = torch.from_numpy(np.ascontiguousarray(logits[:, :, [0, R - 1], :])).cuda()
+    r.score_weights(1, lg, 2, mode=mode)
+    n_sets = 1 if mode == 0 else Hkv
+    r.select(1, mode=mode, rows_in_score=2)
+    idx, cnt = r.selection(1, n_sets)
+    k = selection_k(r.sparse_ratio, p0, r.k_min)
+    exact = 0
+    for s in range(n_sets):
+        heads = list(range(Hkv * G)) if mode == 0 else list(range(s * G, (s + 1) * G))
+        L = l_ref[heads]
+        want = ref.select(COLLECT2_WEIGHTS, L, list(range(1, R + 1)), r.sparse_ratio, r.k_min, head_dim=D)
+        sc = ref.score_columns(L, list(range(1, R + 1)), [1, R], weights=True, head_dim=D)
+        got = idx[0, s, : cnt[0, s]]
+        assert cnt[0, s] == k == len(want)
+        check_selection(got, sc, k, relative=True)
+        exact += int(np.array_equal(got, want))
+    assert exact >= n_sets - 1
+
+
+def test_iteration_collect2_weights(cuda, ref):
+    """The weights metric inside the iteration graph (verify -> raw logits -> weights -> select)."""
+    torch = cuda
+    from oracle.pyoracle import COLLECT2_WEIGHTS
+    Runner, _, selection_k = _lib()
+    L, Hkv, G, gamma, p0 = 2, 2, 4, 4, 1100
+    R, Hq = gamma + 1, Hkv * G
+    m = Matched(ref, L=L, Hkv=Hkv, n_tokens=p0, seed=87, max_context=p0 + 64, page_size=128)
+    r = Runner(m.cache, Hq, max_rows=R, max_prefix=p0, sparse_ratio=0.07, k_min=16)
+    r.set_batch([0], [p0])
+    qv = normal_bf16(88, 1, (L, 1, Hq, R, D))
+    kvn, vvn = normal_bf16(88, 2, (L, 1, R, Hkv, D)), normal_bf16(88, 3, (L, 1, R, Hkv, D))
+    qd = normal_bf16(88, 4, (gamma, L, 1, Hq, D))
+    kdn, vdn = normal_bf16(88, 5, (gamma, L, 1, Hkv, D)), normal_bf16(88, 6, (gamma, L, 1, Hkv, D))
+    out_v = torch.zeros((L, 1, Hq, R, D), dtype=torch.float32, device="cuda")
+    out_d = torch.zeros((gamma, L, 1, Hq, D), dtype=torch.float32, device="cuda")
+    dev = [to_dev_bf16(x) for x in (qv, kvn, vvn, qd, kdn, vdn)]
+    args = r.iteration_args(gamma, *dev, out_v, out_d, strategy=COLLECT2_WEIGHTS, scale=SCALE, use_graph=True)
+    assert r.iteration_kernel_count(args) == L * (4 + gamma)
+    for _ in range(2):
+        r.iteration(args)
+    torch.cuda.synchronize()
+    kv = m.refs[0]
+    for t in range(R):
+        kv.append(kvn[:, 0, t].reshape(L * Hkv, D), vvn[:, 0, t].reshape(L * Hkv, D))
+    k = selection_k(0.07, p0, 16)
+    for layer in range(L):
+        o_ref, l_ref = kv.verify_layer(layer, Hq, qv[layer, 0], p0, R, SCALE, threads=8)
+        assert rel_err_rows(out_v.cpu().numpy()[layer, 0], o_ref) < 2e-4
+        idx, cnt = r.selection(layer, 1)
+        sc = ref.score_columns(l_ref, list(range(1, R + 1)), [1, R], weights=True, head_dim=D)
+        check_selection(idx[0, 0, : cnt[0, 0]], sc, k, relative=True)
