@@ -323,7 +323,6 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   }();
   cudaError_t e;
   if (use_mma_sync) {
-    if (p.score_fx) return fail(SA_NOT_SUPPORTED, "SA_VERIFY_IMPL=mma: per-KV-head score layout only");
     p.n_splits = choose_splits(units, r->p_max, 64, 0, r->num_sms, r->v_units_cap, 128, &p.chunk);
     p.part_o = r->v_po;
     p.part_ml = r->v_pml;

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(VCfg<MT, TG>::kThreads, 1)
   }
   named_bar_sync(1, nct);
   // q_sum rows (hi at hi_row, lo at hi_row+1) for the fused score byproduct.
-  if (p.scores && tid < 128) {
+  if ((p.scores || p.score_fx) && tid < 128) {
     float acc = 0.f;
     const uint32_t off = swz(0, tid >> 3, Cfg::kQHalf) + (tid & 7) * 2;  // row 0 position of column tid
     for (int m = 0; m < M; ++m) {
@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(VCfg<MT, TG>::kThreads, 1)
   w.load_q(smem_u32(sq), Cfg::kQHalf, mt, lane);
   const float c = p.scale_log2;
   const int gid = lane >> 2, t4 = lane & 3;
-  const bool score_warp = (mt == MT - 1) && (p.scores != nullptr);
+  const bool score_warp = (mt == MT - 1) && (p.scores != nullptr || p.score_fx != nullptr);
+  long long* score_fx = p.score_fx ? p.score_fx + static_cast<size_t>(b) * p.ld_scores : nullptr;
   const int hi_local = p.hi_row - 16 * (MT - 1), lo_local = hi_local + 1;
   float* score_out = p.scores ? p.scores + (static_cast<size_t>(b) * p.Hkv + g) * p.ld_scores : nullptr;
 
@@ -191,7 +192,13 @@ __global__ void __launch_bounds__(VCfg<MT, TG>::kThreads, 1)
           }
           const int pos = tile_tok0 + r0 + 8 * nt + 2 * t4;
           if (gid == (hi_local & 7)) {
-            if (pos + 1 < tok_end) {
+            if (score_fx) {  // per-layer: integer atomics over the KV heads (order-independent)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+                if (pos + e < tok_end)
+                  atomicAdd(reinterpret_cast<unsigned long long*>(score_fx + pos + e),
+                            static_cast<unsigned long long>(__float2ll_rn(v[e] * kScoreFxScale)));
+            } else if (pos + 1 < tok_end) {
               *reinterpret_cast<float2*>(score_out + pos) = make_float2(v[0], v[1]);
             } else if (pos < tok_end) {
               score_out[pos] = v[0];
