@@ -158,9 +158,14 @@ struct DCfg {
                                                                                   : kRecvFloats * 4;
   static constexpr int kOffBar = kOffRecv + kRecvBytes;
   static constexpr int kSmem = kOffBar + 16 + 1024;
+  // streaming mode (chunks of several rounds): a second K/V buffer after everything else, so round
+  // r+1 is gathered while round r is computed (one CTA per SM)
+  static constexpr int kOffBuf1 = (kOffBar + 16 + 1023) / 1024 * 1024;
+  static constexpr int kSmemStream = kOffBuf1 + 2 * kMaxTiles * kTileBytes + 1024;
   static_assert(kMaxWarps * 8 * 128 * 4 <= kOffPart, "warp partials must fit in the tile buffers");
   static_assert(kMaxTiles * kTile * 8 >= kMaxWarps * 16 * 4, "warp (m, l) table fits the row-source area");
   static_assert(kSmem <= 113 * 1024, "two CTAs per SM: the next PDL launch co-resides");
+  static_assert(kSmemStream <= 227 * 1024, "streaming mode fits one CTA per SM");
 };
 
 __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
@@ -188,7 +193,8 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
 // of the G x 128 outputs; every CTA pushes its partial slices and (m, l) into the owners' inboxes
 // with st.async (remote shared-memory stores completing as transaction bytes on the owner's
 // mbarrier), and each owner combines its slice once its inbox is full.
-__global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const DraftParams p) {
+template <bool kStream>
+__global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kernel(const DraftParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* part = reinterpret_cast<float*>(smem + DCfg::kOffPart);
@@ -242,7 +248,8 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
       src_row[r] = (p.k_new && pos == new_pos) ? -1 : cache_row(p.cache, seq, p.layer, g, pos);
     }
   };
-  auto gather = [&](int r0, int rows, bool pre_pass) {
+  auto gather = [&](int r0, int rows, bool pre_pass, int buf = 0) {
+    uint8_t* const base = buf ? smem + DCfg::kOffBuf1 : smem;
     for (int i = tid; i < rows * 16; i += nthr) {
       const int r = i >> 4, ch = i & 15;
       const int v = v_begin + r0 + r;
@@ -262,8 +269,8 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
       } else {
         bytes = 0;  // zero-fill (keeps 0 * V finite)
       }
-      cp_async_16(smem + off, sk, bytes);
-      cp_async_16(smem + DCfg::kOffV + off, sv, bytes);
+      cp_async_16(base + off, sk, bytes);
+      cp_async_16(base + DCfg::kOffV + off, sv, bytes);
     }
   };
 
@@ -304,24 +311,33 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
     __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + row * 128;
     reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
   }
-  for (int r0 = 0, round = 0; r0 < max(n, 1); r0 += kRoundRows, ++round) {
+  const int n_rounds = max(1, (n + kRoundRows - 1) / kRoundRows);
+  const bool dbuf = kStream && n_rounds > 1;  // double-buffered rounds (streaming mode)
+  auto issue_round = [&](int round, int buf) {  // every row of a later round (after the wait)
+    const int rr0 = round * kRoundRows;
+    const int rp = (min(kRoundRows, n - rr0) + 15) & ~15;
+    __syncthreads();  // buffer `buf` and src_row free
+    resolve(rr0, rp, true);
+    resolve(rr0, rp, false);
+    __syncthreads();
+    gather(rr0, rp, true, buf);
+    gather(rr0, rp, false, buf);
+    cp_async_commit();
+  };
+  if (dbuf) issue_round(1, 1);
+  for (int round = 0; round < n_rounds; ++round) {
+    const int r0 = round * kRoundRows;
     const int rows = min(kRoundRows, n - r0);
     const int rows_pad = (rows + 15) & ~15;
-    if (round > 0) {
-      __syncthreads();  // previous round's tiles fully consumed
-      resolve(r0, rows_pad, true);
-      resolve(r0, rows_pad, false);
-      __syncthreads();
-      gather(r0, rows_pad, true);
-      gather(r0, rows_pad, false);
-      cp_async_commit();
-    }
-    cp_async_wait_all();
+    const int buf = dbuf ? (round & 1) : 0;
+    if (!dbuf && round > 0) issue_round(round, 0);
+    if (dbuf && round + 1 < n_rounds) cp_async_wait_group<1>();  // this round landed, the next in flight
+    else cp_async_wait_all();
     __syncthreads();
     dtrace(p, 2);
     const int n_sub = rows_pad >> 4;
     // warp w takes sub-blocks w, w + nwarps, ...; two at a time in one softmax step
-    const uint32_t kb = smem_u32(smem), vb = smem_u32(smem + DCfg::kOffV);
+    const uint32_t kb = smem_u32(buf ? smem + DCfg::kOffBuf1 : smem), vb = kb + DCfg::kOffV;
     for (int sb = warp; sb < n_sub; sb += 2 * nwarps) {
       const int sb2 = sb + nwarps;
       const int nv0 = min(16, n - (r0 + sb * 16));
@@ -339,6 +355,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
         w.step<1>(ks, vs, DCfg::kHalf, rr, lane, p.scale_log2, nv);
       }
     }
+    if (dbuf && round + 2 < n_rounds) issue_round(round + 2, buf);
   }
   w.finalize_l();
   dtrace(p, 3);
@@ -464,8 +481,13 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, 2) draft_kernel(const Draft
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg::kSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(draft_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaError_t e = cudaFuncSetAttribute(draft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(draft_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(draft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg::kSmemStream);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(draft_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -473,7 +495,7 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);
   // one warp per 16-row sub-block of the CTA's chunk (<= 9 warps, two CTAs per SM)
   cfg.blockDim = dim3(32 * std::min(DCfg::kMaxWarps, std::max(1, (std::min(p.chunk, DCfg::kMaxTiles * DCfg::kTile) + 15) / 16)));
-  cfg.dynamicSmemBytes = DCfg::kSmem;
+  cfg.dynamicSmemBytes = p.stream ? DCfg::kSmemStream : DCfg::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
@@ -484,7 +506,7 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = p.use_pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, draft_kernel, p);
+  return p.stream ? cudaLaunchKernelEx(&cfg, draft_kernel<true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<false>, p);
 }
 
 int draft_max_splits() { return DCfg::kMaxCS; }

@@ -112,6 +112,7 @@ struct DraftParams {
   int* counters;
   unsigned long long* trace;  // dev-only per-CTA phase timestamps; null in production
   int use_pdl;  // launch with programmatic stream serialization (iteration graph only)
+  int stream;   // double-buffered multi-round chunks (one CTA per SM)
 };
 
 struct SelectParams {

@@ -442,15 +442,25 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   const int64_t units = static_cast<int64_t>(r->B) * r->Hkv;
   {  // one cluster of CS CTAs per (sequence, KV head): the smallest CS whose chunk fits one resident
      // round (192 rows); 12 before 16 because two launches of 12-CTA clusters co-reside on 148 SMs
-     // (the PDL successor gathers while this one computes) and two of 16-CTA clusters do not
+     // (the PDL successor gathers while this one computes) and two of 16-CTA clusters do not.
+     // Chunks of several rounds (large k) or grids far beyond two waves (many sequences x heads)
+     // switch to the streaming mode: one CTA per SM, CS sized to one wave, rounds double-buffered.
     const int64_t m = r->k_cap + a->step;
     const int round_rows = sa::draft_round_rows();
-    int cs = 16;
+    int cs = -1;
     for (int c : {1, 2, 4, 8, 12, 16})
       if ((m + c - 1) / c <= round_rows) {
         cs = c;
         break;
       }
+    p.stream = 0;
+    if (cs < 0 || units * cs > 2 * r->num_sms) {
+      p.stream = 1;
+      const int64_t fit = std::max<int64_t>(1, r->num_sms / units);
+      cs = 1;
+      for (int c : {2, 4, 8, 12, 16})
+        if (c <= fit && (m + c - 1) / c >= round_rows) cs = c;  // keep >= one full round per CTA
+    }
     p.n_splits = cs;
     p.chunk = static_cast<int>(((m + cs - 1) / cs + 15) / 16 * 16);
   }

@@ -474,3 +474,40 @@ def test_iteration_collect2_weights(cuda, ref):
         idx, cnt = r.selection(layer, 1)
         sc = ref.score_columns(l_ref, list(range(1, R + 1)), [1, R], weights=True, head_dim=D)
         check_selection(idx[0, 0, : cnt[0, 0]], sc, k, relative=True)
+
+
+def test_draft_streaming_mode(cuda, ref):
+    """Draft launches whose chunks span several resident rounds (large k x many sequences: the
+    streaming mode, one CTA per SM with double-buffered rounds) vs the reference gather + attend."""
+    torch = cuda
+    Runner, _, selection_k = _lib()
+    Hkv, G, R, B = 8, 4, 3, 6
+    p0s = [2600, 3000, 1900, 2800, 3000, 2200]
+    Hq = Hkv * G
+    m = Matched(ref, L=2, Hkv=Hkv, n_tokens=0, seed=61, max_context=max(p0s) + 64, page_size=128, n_seqs=B,
+                lens=p0s)
+    r = Runner(m.cache, Hq, max_rows=R, max_prefix=max(p0s), max_batch=B, sparse_ratio=0.5, k_min=16)
+    r.set_batch(list(range(B)), p0s)
+    q = normal_bf16(62, 1, (B, Hq, R, D))
+    kn, vn = normal_bf16(62, 2, (B, R, Hkv, D)), normal_bf16(62, 3, (B, R, Hkv, D))
+    out = torch.zeros((B, Hq, R, D), dtype=torch.float32, device="cuda")
+    r.verify(1, to_dev_bf16(q), out, to_dev_bf16(kn), to_dev_bf16(vn), SCALE)
+    r.select(1)
+    idx, cnt = r.selection(1, 1)
+    for b in range(B):
+        assert cnt[b, 0] == selection_k(0.5, p0s[b], 16)
+        m.cache.set_size(p0s[b], seq=b)
+    qd = normal_bf16(63, 1, (B, Hq, D))
+    kd, vd = normal_bf16(63, 2, (B, Hkv, D)), normal_bf16(63, 3, (B, Hkv, D))
+    od = torch.zeros((B, Hq, D), dtype=torch.float32, device="cuda")
+    r.draft(1, 1, to_dev_bf16(qd), od, to_dev_bf16(kd), to_dev_bf16(vd), scale=SCALE)
+    got = od.cpu().numpy()
+    for b in range(B):
+        kv = m.refs[b]
+        kk, vv = np.zeros((2 * Hkv, D), np.float32), np.zeros((2 * Hkv, D), np.float32)
+        kk[Hkv:], vv[Hkv:] = kd[b], vd[b]
+        kv.append(kk, vv)
+        sets = [idx[b, 0, : cnt[b, 0]].astype(np.int64)]
+        o_ref = kv.draft_layer(1, Hq, qd[b], sets, p0s[b], 1, SCALE, threads=8)
+        assert rel_err_rows(got[b], o_ref) < 2e-4, (b, rel_err_rows(got[b], o_ref))
+        assert rel_err_elem(got[b], o_ref) < 2e-3
