@@ -51,6 +51,11 @@ print(f"epilogue detail (us): pv_done->both_wg {np.median((rel(10) - pv)[has]):.
 print(f"epilogue medians (us): loop_end->pv_done {np.median(pv - ml):.2f}  pv_done->partial_stored "
       f"{np.median((sto - pv)[has]):.2f}  stored->counted {np.median((cnt - sto)[has]):.2f}  counted->end(non-merger) "
       f"{np.median((en - cnt)[has]):.2f}")
+mg = se[:, 12] > 0
+if mg.any():
+    print(f"merger detail (us): counted->landed {np.median((rel(12) - cnt)[mg]):.2f}  weights {np.median((rel(13) - rel(12))[mg]):.2f}  "
+          f"barrier {np.median((rel(14) - rel(13))[mg]):.2f}  combine {np.median((rel(15) - rel(14))[mg]):.2f}  "
+          f"->end {np.median((en - rel(15))[mg]):.2f}")
 mg = se[:, 7] > 0
 if mg.any():
     w8, c9 = rel(8), rel(9)
