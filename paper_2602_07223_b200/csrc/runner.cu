@@ -662,8 +662,10 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
   if (r->n_slots < r->cache->n_layers) return fail(SA_INVALID_ARGUMENT, "iteration needs n_layers_buf >= n_layers");
   if (!a->qv || !a->qd || !a->out_v || !a->out_d) return fail(SA_INVALID_ARGUMENT, "iteration: null buffer");
   cudaStream_t main = static_cast<cudaStream_t>(stream);
-  // per-layer sums left unconsumed by direct verify calls: zero before the iteration accumulates
-  if (a->mode == SA_PER_LAYER)
+  // per-layer sums left unconsumed (direct verify calls, verify-only phase runs): zero them before an
+  // iteration whose selects will consume them (a run without the select phase reads none)
+  const uint32_t ph = a->phases ? a->phases : 7u;
+  if (a->mode == SA_PER_LAYER && (ph & SA_PHASE_SELECT))
     for (int l = 0; l < r->cache->n_layers; ++l)
       if (r->fx_dirty[l]) {
         long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, l, nullptr));
