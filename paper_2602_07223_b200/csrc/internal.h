@@ -83,6 +83,7 @@ struct VerifyParams {
   float* part_gml; // [B*Hkv][n_groups][N][2]
   int n_groups, group_size;
   int no_prefill;  // dev knob
+  int static_first;  // first chunk = split index (else every chunk claimed from the counter)
   int* counters;   // [B*Hkv][32]: [0] groups arrived, [1+g] splits of group g arrived
   int* chunk_ctr;  // [B*Hkv] dynamic chunk claims (tcgen05 verify), re-armed by the merging CTA
   unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production

@@ -173,8 +173,15 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
   alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r->capture, cudaStreamNonBlocking);
+  // the selection side stream at the lowest priority, the capture stream at the highest: when SMs
+  // free up, the next layer's verify CTAs are scheduled ahead of the (off-critical-path) selects
+  static const bool prio = !getenv("SA_NO_STREAM_PRIORITY");  // dev knob
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  if (e == cudaSuccess)
+    e = cudaStreamCreateWithPriority(&r->side, cudaStreamNonBlocking, prio ? least : 0);
+  if (e == cudaSuccess)
+    e = cudaStreamCreateWithPriority(&r->capture, cudaStreamNonBlocking, prio ? greatest : 0);
   r->ev_v.resize(S);
   r->ev_s.resize(S);
   for (int64_t i = 0; i < S && e == cudaSuccess; ++i) {
@@ -346,6 +353,11 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.next_pf = next_pf;
     static const int no_prefill = getenv("SA_VERIFY_NOPREFILL") ? 1 : 0;
     p.no_prefill = no_prefill;
+    static const int static_first = [] {
+      const char* v = getenv("SA_VERIFY_STATIC_FIRST");  // dev tuning knob
+      return v ? atoi(v) : 1;
+    }();
+    p.static_first = static_first;
     p.chunk_tiles = chunk_tiles;
     p.prefetch = prefetch;
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);

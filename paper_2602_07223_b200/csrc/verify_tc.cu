@@ -329,8 +329,12 @@ __global__ void __launch_bounds__(384, 1)
             }
             // claims run one chunk ahead: the atomic's L2 round trip overlaps the current chunk (its
             // result register is first read here, one chunk later); no claim is left unconsumed
-            cur_chunk = claims++ == 0 ? split : p.n_splits + pending;
-            if (cur_chunk < n_chunks) pending = atomicAdd(p.chunk_ctr + unit, 1);
+            if (p.static_first) {
+              cur_chunk = claims++ == 0 ? split : p.n_splits + pending;
+            } else {  // fully dynamic: a CTA that starts late (SM held by another kernel) takes no chunk
+              cur_chunk = claims++ == 0 ? atomicAdd(p.chunk_ctr + unit, 1) : pending;
+            }
+            if (cur_chunk < n_chunks) pending = (p.static_first ? 0 : 0) + atomicAdd(p.chunk_ctr + unit, 1);
             if (cur_chunk >= n_chunks) {
               exhausted = true;
               break;
