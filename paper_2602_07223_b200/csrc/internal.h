@@ -79,12 +79,10 @@ struct VerifyParams {
   int n_splits, chunk;
   float* part_o;   // [B*Hkv][n_splits][MT*16][128]
   float* part_ml;  // [B*Hkv][n_splits][MT*16][2]
-  float* part_g;   // [B*Hkv][n_groups][N][128] group partials (two-level merge)
-  float* part_gml; // [B*Hkv][n_groups][N][2]
-  int n_groups, group_size;
+  int n_mergers;   // CTAs (the last arrivals of a unit) that split the merge's rows
   int no_prefill;  // dev knob
   int static_first;  // first chunk = split index (else every chunk claimed from the counter)
-  int* counters;   // [B*Hkv][32]: [0] groups arrived, [1+g] splits of group g arrived
+  int* counters;   // [B*Hkv][4]: [0] arrivals, [1] go (all partials stored), [2] mergers done
   int* chunk_ctr;  // [B*Hkv] dynamic chunk claims (tcgen05 verify), re-armed by the merging CTA
   unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production
   int use_pdl;  // programmatic dependent launch after the previous layer's verify (iteration graph)

@@ -40,7 +40,7 @@ struct sa_runner {
   uint32_t* keys = nullptr;    // [max_batch][Hkv][ld]
   // split-KV workspaces
   int64_t v_units_cap = 0, d_units_cap = 0;
-  float *v_po = nullptr, *v_pml = nullptr, *d_po = nullptr, *d_pml = nullptr, *v_pg = nullptr, *v_pgml = nullptr;
+  float *v_po = nullptr, *v_pml = nullptr, *d_po = nullptr, *d_pml = nullptr;
   int *v_cnt = nullptr, *d_cnt = nullptr, *v_chunk = nullptr;
   // streams / graph
   cudaStream_t side = nullptr;
@@ -166,9 +166,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   // verify split workspaces x2: consecutive layers alternate (PDL-chained verify launches)
   alloc(reinterpret_cast<void**>(&r->v_po), 2 * sizeof(float) * r->v_units_cap * 64 * 128);
   alloc(reinterpret_cast<void**>(&r->v_pml), 2 * sizeof(float) * r->v_units_cap * 64 * 2);
-  alloc(reinterpret_cast<void**>(&r->v_pg), 2 * sizeof(float) * r->v_units_cap * 64 * 128);
-  alloc(reinterpret_cast<void**>(&r->v_pgml), 2 * sizeof(float) * r->v_units_cap * 64 * 2);
-  alloc(reinterpret_cast<void**>(&r->v_cnt), 2 * 32 * sizeof(int) * mb * H);
+  alloc(reinterpret_cast<void**>(&r->v_cnt), 2 * 4 * sizeof(int) * mb * H);
   alloc(reinterpret_cast<void**>(&r->v_chunk), 2 * sizeof(int) * mb * H);
   alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
@@ -211,7 +209,7 @@ SA_API sa_status sa_runner_destroy(sa_runner* r) {
   if (r->capture) cudaStreamDestroy(r->capture);
   for (void* p : {static_cast<void*>(r->d_seq), static_cast<void*>(r->d_p0), static_cast<void*>(r->scores),
                   static_cast<void*>(r->idx), static_cast<void*>(r->score_fx), static_cast<void*>(r->kcnt), static_cast<void*>(r->keys),
-                  static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_pg), static_cast<void*>(r->v_pgml), static_cast<void*>(r->v_cnt), static_cast<void*>(r->v_chunk),
+                  static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_cnt), static_cast<void*>(r->v_chunk),
                   static_cast<void*>(r->d_po), static_cast<void*>(r->d_pml), static_cast<void*>(r->d_cnt)})
     cudaFree(p);
   delete r;
@@ -361,24 +359,22 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.chunk_tiles = chunk_tiles;
     p.prefetch = prefetch;
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
-    // split merge: groups of <= gmax partials (they must fit the ring buffers), <= 16 groups; one
-    // level (a single group) whenever it fits — every merge level costs two L2 round trips, which
-    // under the streaming load outweigh the smaller per-level merge (measured)
-    const int gmax = std::max(1, std::min(128, sa::verify_tc_merge_capacity(p.M) / (p.M * 512 + 64 * 8)));
+    // split merge: the last n_mergers arrivals of a unit normalise a slice of rows each; their
+    // partial rows and the (m, l) table must fit the ring buffers
+    static const int n_mergers = [] {
+      const char* v = getenv("SA_VERIFY_MERGERS");  // dev tuning knob
+      return v ? std::max(1, std::min(8, atoi(v))) : 4;
+    }();
+    const int rows_per = (p.M + n_mergers - 1) / n_mergers;
+    const int fit = std::max(1, (sa::verify_tc_merge_capacity(p.M) - 128) / (rows_per * 512 + 64 * 8));
     p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, r->num_sms / units),
-                                                     n_chunks, 128, r->v_units_cap / units, 16 * gmax}));
-    {
-      const int ns = p.n_splits;
-      p.group_size = std::min(gmax, ns);
-      p.n_groups = (ns + p.group_size - 1) / p.group_size;
-    }
+                                                     n_chunks, 128, r->v_units_cap / units, fit}));
+    p.n_mergers = n_mergers;
     p.chunk = 0;
     p.chunk_ctr = r->v_chunk + par * cnt_stride;
     p.part_o = r->v_po + par * po_stride;
     p.part_ml = r->v_pml + par * pml_stride;
-    p.counters = r->v_cnt + par * cnt_stride * 32;
-    p.part_g = r->v_pg + par * po_stride;
-    p.part_gml = r->v_pgml + par * pml_stride;
+    p.counters = r->v_cnt + par * cnt_stride * 4;
     p.use_pdl = pdl ? 1 : 0;
     p.next_layer = next_layer;
     p.trace = dev_verify_trace();

@@ -205,6 +205,66 @@ __device__ __forceinline__ void merge_partials(uint8_t* smem, uint32_t smem_cap,
   stamp(15);
 }
 
+// Rows [r_lo, r_hi) of one unit's output from its `cnt` split partials (O rows [N][128]
+// unnormalised and (m, l) per row at src_o / src_ml, per-partial strides N*128 / N*2 floats): the
+// partial rows and the (m, l) table are bulk-copied into the idle ring buffers, then every thread
+// forms its rows' merge weights on the fly and writes normalised rows to dst_o (row stride 128).
+__device__ __forceinline__ void merge_rows(uint8_t* smem, uint64_t* bar, const float* src_o, const float* src_ml,
+                                           int cnt, int N, int r_lo, int r_hi, float* dst_o, int t256) {
+  const int nr = r_hi - r_lo;
+  if (nr <= 0) return;
+  const uint32_t obytes = static_cast<uint32_t>(nr) * 512u;
+  const uint32_t mlbytes = static_cast<uint32_t>(cnt) * N * 8u;
+  float2* sml = reinterpret_cast<float2*>(smem);                       // [partial][N] (m, l)
+  uint8_t* sop = smem + ((mlbytes + 127u) & ~127u);                      // [partial][nr][128]
+  if (t256 == 0) {
+    fence_proxy_async();  // generic writes of the other CTAs (acquired by the caller) -> async-proxy reads
+    mbar_expect_tx(bar, cnt * obytes + mlbytes);
+    bulk_load(sml, src_ml, mlbytes, bar);
+    for (int s2 = 0; s2 < cnt; ++s2)
+      bulk_load(sop + s2 * obytes, src_o + static_cast<size_t>(s2) * N * 128 + r_lo * 128, obytes, bar);
+  }
+  mbar_wait(bar, 0);
+  const float4* so = reinterpret_cast<const float4*>(sop);
+  for (int it = t256; it < nr * 32; it += 256) {
+    const int rr = it >> 5, c4 = it & 31, row = r_lo + rr;
+    float mstar = -INFINITY;
+    for (int s0 = 0; s0 < cnt; s0 += 8) {
+      float mm[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mm[u] = s0 + u < cnt ? sml[(s0 + u) * N + row].x : -INFINITY;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) mstar = fmaxf(mstar, mm[u]);
+    }
+    float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+    float lsum = 0.f;
+    for (int s0 = 0; s0 < cnt; s0 += 8) {  // 8 independent smem loads per batch
+      float4 v[8];
+      float2 ml[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = s0 + u < cnt;
+        v[u] = ok ? so[((s0 + u) * nr + rr) * 32 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        ml[u] = ok ? sml[(s0 + u) * N + row] : make_float2(-INFINITY, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float w = ml[u].x == -INFINITY ? 0.f : fast_exp2(ml[u].x - mstar);
+        lsum = fmaf(ml[u].y, w, lsum);
+        float4& a = acc[u & 1];
+        a.x = fmaf(v[u].x, w, a.x);
+        a.y = fmaf(v[u].y, w, a.y);
+        a.z = fmaf(v[u].z, w, a.z);
+        a.w = fmaf(v[u].w, w, a.w);
+      }
+    }
+    const float inv = 1.f / lsum;
+    reinterpret_cast<float4*>(dst_o + static_cast<size_t>(row) * 128)[c4] =
+        make_float4((acc[0].x + acc[1].x) * inv, (acc[0].y + acc[1].y) * inv, (acc[0].z + acc[1].z) * inv,
+                    (acc[0].w + acc[1].w) * inv);
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(384, 1)
     verify_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
@@ -752,57 +812,52 @@ __global__ void __launch_bounds__(384, 1)
     if (single) {
       if (wg == 0 && ts == 0) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
     } else {
-      // Two-level merge (groups of <= 16 splits, at most 16 groups): the last-arriving CTA of each
-      // group merges that group's partials into a group partial; the last-arriving group merger
-      // merges the group partials and normalises.  Arrival: one acq_rel atomic per CTA after the
-      // CTA-wide barrier (release of this CTA's partial stores; acquire of everyone else's).
-      const int n_groups = p.n_groups;
-      const int gsize = p.group_size;
-      const int grp = split / gsize;
-      const int g_lo = grp * gsize, g_cnt = min(gsize, p.n_splits - g_lo);
+      // Split merge by the last-arriving CTAs of the unit, each normalising a slice of the rows.
+      // Arrival: one acq_rel atomic per CTA after the CTA-wide barrier (release of this CTA's
+      // partial stores).  The last arrival has acquired every partial; it releases `go`, which the
+      // other mergers (the few arrivals before it, still resident) acquire before reading partials.
       const int t256 = wg * 128 + ts;
-      int* ctr = p.counters + unit * 32;  // [0]: unit (groups arrived), [1 + grp]: splits arrived
+      int* ctr = p.counters + unit * 4;  // [0] arrivals, [1] go, [2] mergers done
       named_bar_sync(1, 256);
       if (t256 == 0) {
         SA_TSTAMP(5);
         int old;
-        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr + 1 + grp) : "memory");
+        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
         *flag = old;
         SA_TSTAMP(6);
       }
       named_bar_sync(1, 256);
-      if (*flag == g_cnt - 1) {
-        const bool one_level = n_groups == 1;
-        float* pg = p.part_g + static_cast<size_t>(unit) * n_groups * N * 128;
-        float* pgml = p.part_gml + static_cast<size_t>(unit) * n_groups * N * 2;
-        merge_partials(smem, C::kOffBar, merge_bar, 0, po + static_cast<size_t>(g_lo) * N * 128,
-                       pml + static_cast<size_t>(g_lo) * N * 2, g_cnt, N, M, one_level,
-                       one_level ? out_unit : pg + static_cast<size_t>(grp) * N * 128,
-                       pgml + static_cast<size_t>(grp) * N * 2, t256,
-                       (p.trace && cta_lin < 1024) ? p.trace + 1024 + (p.layer & 63) * 16384 + 16 * cta_lin : nullptr);
-        if (t256 == 0) {
-          SA_TSTAMP(7);
-          ctr[1 + grp] = 0;  // re-arm
-        }
-        if (!one_level) {
-          named_bar_sync(1, 256);  // group partial stored by every thread
+      const int arrival = *flag;
+      const int nm = min(p.n_mergers, p.n_splits);
+      if (arrival >= p.n_splits - nm) {
+        const int part = arrival - (p.n_splits - nm);  // the last arrival takes the last slice
+        if (arrival == p.n_splits - 1) {
+          if (t256 == 0 && nm > 1) asm volatile("st.release.gpu.s32 [%0], 1;" ::"l"(ctr + 1) : "memory");
+        } else {
           if (t256 == 0) {
-            int old;
-            asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
-            *flag = old;
-          }
-          named_bar_sync(1, 256);
-          if (*flag == n_groups - 1) {
-            merge_partials(smem, C::kOffBar, merge_bar, 1, pg, pgml, n_groups, N, M, true, out_unit, nullptr, t256);
-            if (t256 == 0) {
-              SA_TSTAMP(9);
-              ctr[0] = 0;
-              p.chunk_ctr[unit] = 0;  // re-arm chunk claims
+            int go = 0;
+            while (true) {
+              asm volatile("ld.acquire.gpu.s32 %0, [%1];" : "=r"(go) : "l"(ctr + 1) : "memory");
+              if (go) break;
+              __nanosleep(64);
             }
           }
-        } else if (t256 == 0) {
+          named_bar_sync(1, 256);
+        }
+        const int per = (M + nm - 1) / nm;
+        merge_rows(smem, merge_bar, po, pml, p.n_splits, N, min(M, part * per), min(M, (part + 1) * per), out_unit,
+                   t256);
+        named_bar_sync(1, 256);
+        if (t256 == 0) {
           SA_TSTAMP(9);
-          p.chunk_ctr[unit] = 0;
+          int done = nm - 1;
+          if (nm > 1) asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(done) : "l"(ctr + 2) : "memory");
+          if (done == nm - 1) {  // the last merger re-arms the unit's counters for the next use
+            ctr[0] = 0;
+            ctr[1] = 0;
+            ctr[2] = 0;
+            p.chunk_ctr[unit] = 0;
+          }
         }
       }
     }
