@@ -190,6 +190,14 @@ SA_API sa_status sa_select_topk(sa_runner* r, const sa_select_args* a, void* str
 SA_API sa_status sa_score_weights(sa_runner* r, int32_t layer_slot, const float* logits, int64_t ld_logits,
                                   int32_t n_rows, sa_select_mode mode, void* stream);
 
+/* Baseline selectors of the paper (selection.cpp:209-274), writing the same per-layer index slot the
+ * draft kernel reads.  QuestLike needs the cache's page summaries (kv_store.cpp:90-139, enabled once
+ * with sa_kv_enable_page_summaries; refreshed lazily); q: bf16 [B][Hq][128], the query rows the
+ * bounds are taken over (select_quest's q_heads).  Window: sink + sliding window. */
+SA_API sa_status sa_kv_enable_page_summaries(sa_cache* cache, int64_t page_size);
+SA_API sa_status sa_select_quest(sa_runner* r, int32_t layer, int32_t layer_slot, const void* q, void* stream);
+SA_API sa_status sa_select_window(sa_runner* r, int32_t layer_slot, int64_t sink, int64_t window, void* stream);
+
 /* Sparse draft attention for one layer (gather(T) ++ tail, then attend; kv_store.cpp:67-88,
  * attention.cpp:70-76): query of q-head h at position p0+step-1 attends to the
  * selected prefix T (layer_slot's index list; per-layer or per-KV-head) and the tail rows

@@ -236,6 +236,10 @@ class Ref(_Base):
         lib.ref_kv_set_committed.argtypes = [_vp, _i64]
         lib.ref_kv_gather.argtypes = [_vp, _i64, _i64, _i64p, _i64, _f32p, _f32p]
         lib.ref_kv_rows.argtypes = [_vp, _i64, _i64, _i64, _i64, _f32p, _f32p]
+        lib.ref_kv_enable_page_summaries.argtypes = [_vp, _i64]
+        lib.ref_kv_page_minmax.argtypes = [_vp, _i64, _i64, _f32p, _f32p, C.POINTER(_i64)]
+        lib.ref_select_quest.argtypes = [_vp, _f32p, _i64, _i64, _i64, C.c_double, _i64, _i64p, C.POINTER(_i64)]
+        lib.ref_select_window.argtypes = [_i64, _i64, _i64, _i64p, C.POINTER(_i64)]
         lib.ref_verify_layer.argtypes = [_vp, _i64, _i64, _f32p, _i64, _i64, C.c_float, _f32p, _vp, C.c_int]
         lib.ref_draft_layer.argtypes = [_vp, _i64, _i64, _f32p, _i64p, _i64p, _i64, _i64, _i64, _i64, C.c_float,
                                         _f32p, C.c_int]
@@ -314,6 +318,27 @@ class KvHandle:
             return K[:n].copy(), V[:n].copy()
         return self.gather(layer, head, np.arange(begin, begin + n))
 
+    # ---- Quest page summaries / baseline selectors (reference backend: the reference's own code)
+    def enable_page_summaries(self, page_size):
+        _check(self.b.lib.ref_kv_enable_page_summaries(self.h, int(page_size)), "enable_page_summaries")
+        self.page_size = int(page_size)
+
+    def page_minmax(self, layer, head):
+        n_max = (self.size() + self.page_size - 1) // self.page_size
+        mn = np.empty((max(n_max, 1), self.d), np.float32)
+        mx = np.empty_like(mn)
+        n = _i64(0)
+        _check(self.b.lib.ref_kv_page_minmax(self.h, layer, head, mn, mx, C.byref(n)), "page_minmax")
+        return mn[: n.value].copy(), mx[: n.value].copy()
+
+    def select_quest(self, q_heads, layer, prefix_len, ratio, k_min):
+        q = _f32(q_heads).reshape(-1, self.d)
+        out = np.empty(max(prefix_len, 1), np.int64)
+        n = _i64(0)
+        _check(self.b.lib.ref_select_quest(self.h, q, q.shape[0], layer, prefix_len, float(ratio), int(k_min), out,
+                                           C.byref(n)), "select_quest")
+        return out[: n.value].copy()
+
     def verify_layer(self, layer, n_q_heads, q, p0, R, scale, want_logits=True, threads=1):
         q = _f32(q).reshape(n_q_heads, R, self.d)
         out = np.empty((n_q_heads, R, self.d), np.float32)
@@ -344,6 +369,41 @@ class KvHandle:
                                            tail_len, float(scale), out)
         _check(st, "draft_layer")
         return out
+
+
+def ref_select_window(ref, prefix_len, sink, window):
+    """select_window (selection.cpp:209-222) from the reference's own code."""
+    out = np.empty(max(prefix_len, 1), np.int64)
+    n = _i64(0)
+    _check(ref.lib.ref_select_window(int(prefix_len), int(sink), int(window), out, C.byref(n)), "select_window")
+    return out[: n.value].copy()
+
+
+def quest_bounds(mins, maxs, q_heads, group):
+    """Restatement of select_quest's page upper bounds (selection.cpp:237-248): per q-head h (KV head
+    h // group) the float sum over d of max(q*min, q*max), accumulated over heads in double.
+    mins/maxs: [Hkv][n_pages][d] f32, q_heads: [Hq][d] f32 -> [n_pages] f64."""
+    q = np.asarray(q_heads, np.float32)
+    b = np.zeros(mins.shape[1], np.float64)
+    for h in range(q.shape[0]):
+        g = h // group
+        t = np.maximum(q[h] * mins[g], q[h] * maxs[g]).astype(np.float32)
+        b += t.sum(axis=1, dtype=np.float32).astype(np.float64)
+    return b
+
+
+def quest_pick(bounds, prefix_len, page, k):
+    """Restatement of select_quest's page ordering and token pick (selection.cpp:250-271)."""
+    order = sorted(range(len(bounds)), key=lambda p: (-bounds[p], p))
+    picked = []
+    for p in order:
+        if len(picked) >= k:
+            break
+        for i in range(p * page, min(p * page + page, prefix_len)):
+            if len(picked) >= k:
+                break
+            picked.append(i)
+    return np.array(sorted(picked), np.int64)
 
 
 def bf16_round(x: np.ndarray) -> np.ndarray:

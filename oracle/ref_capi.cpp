@@ -219,6 +219,51 @@ int ref_kv_rows(void* h, int64_t layer, int64_t head, int64_t begin, int64_t n, 
   });
 }
 
+// Quest page summaries and the baseline selectors (kv_store.cpp:90-139, selection.cpp:209-274).
+int ref_kv_enable_page_summaries(void* h, int64_t page_size) {
+  return guard([&] { static_cast<specattn::KvStore*>(h)->enable_page_summaries(page_size); });
+}
+// mins/maxs: [n_pages][d] (n_pages = ceil(size / page_size))
+int ref_kv_page_minmax(void* h, int64_t layer, int64_t head, float* mins, float* maxs, int64_t* n_pages) {
+  auto* kv = static_cast<specattn::KvStore*>(h);
+  return guard([&] {
+    auto mn = kv->page_min(layer, head);
+    auto mx = kv->page_max(layer, head);
+    *n_pages = mn.rows();
+    for (int64_t r = 0; r < mn.rows(); ++r)
+      for (int64_t j = 0; j < kv->head_dim(); ++j) {
+        mins[r * kv->head_dim() + j] = mn(r, j);
+        maxs[r * kv->head_dim() + j] = mx(r, j);
+      }
+  });
+}
+// q_heads: [Hq][d]; out: ascending positions (capacity prefix_len)
+int ref_select_quest(void* h, const float* q_heads, int64_t Hq, int64_t layer, int64_t prefix_len, double ratio,
+                     int64_t k_min, int64_t* out, int64_t* n_out) {
+  auto* kv = static_cast<specattn::KvStore*>(h);
+  return guard([&] {
+    specattn::SelectorConfig cfg;
+    cfg.strategy = specattn::Strategy::kQuestLike;
+    cfg.sparse_ratio = ratio;
+    cfg.k_min = k_min;
+    cfg.page_size = kv->page_size();
+    const auto set = specattn::select_quest(rows_of(q_heads, Hq, kv->head_dim()), *kv, layer, prefix_len, cfg);
+    *n_out = static_cast<int64_t>(set.indices.size());
+    for (size_t i = 0; i < set.indices.size(); ++i) out[i] = set.indices[i];
+  });
+}
+int ref_select_window(int64_t prefix_len, int64_t sink, int64_t window, int64_t* out, int64_t* n_out) {
+  return guard([&] {
+    specattn::SelectorConfig cfg;
+    cfg.strategy = specattn::Strategy::kWindow;
+    cfg.sink = sink;
+    cfg.window = window;
+    const auto set = specattn::select_window(prefix_len, cfg, 0);
+    *n_out = static_cast<int64_t>(set.indices.size());
+    for (size_t i = 0; i < set.indices.size(); ++i) out[i] = set.indices[i];
+  });
+}
+
 // ---------------------------------------------------------------- caller compositions
 
 // Verify, one layer: q-head h, row t in 1..R (query at p0+t-1) sees

@@ -91,6 +91,9 @@ SIGNATURES = {
     "sa_iteration_kernel_count": (_i64, [_vp, C.POINTER(IterationArgs)]),
     "sa_dev_trace_dump": (C.c_int, [C.c_char_p]),
     "sa_score_weights": (C.c_int, [_vp, _i32, _vp, _i64, _i32, C.c_int, _vp]),
+    "sa_kv_enable_page_summaries": (C.c_int, [_vp, _i64]),
+    "sa_select_quest": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),
+    "sa_select_window": (C.c_int, [_vp, _i32, _i64, _i64, _vp]),
     "sa_comm_unique_id": (C.c_int, [_vp]),
     "sa_comm_create": (C.c_int, [_vp, _i32, _i32, C.POINTER(_vp)]),
     "sa_comm_destroy": (C.c_int, [_vp]),
@@ -208,6 +211,10 @@ class Cache:
     def set_size(self, n, seq=0):
         _check(lib().sa_kv_set_size(self.h, seq, n))
 
+    def enable_page_summaries(self, page_size=8):
+        """KvStore::enable_page_summaries (kv_store.cpp:90-112): QuestLike page min / max."""
+        _check(lib().sa_kv_enable_page_summaries(self.h, page_size))
+
     def gather(self, layer, kv_head, indices, seq=0, stream=None):
         import torch
         idx = [int(i) for i in indices]
@@ -309,6 +316,15 @@ class Runner:
         """Collect2Weights scores for layer_slot from a verify's raw logits [B][Hq][n_rows][ld]."""
         _check(lib().sa_score_weights(self.h, layer_slot, _ptr(logits), logits.shape[-1], n_rows, mode,
                                       _stream(stream)))
+
+    def select_quest(self, layer, q, layer_slot=None, stream=None):
+        """select_quest (selection.cpp:224-274) for every bound sequence; q: bf16 [B][Hq][128]."""
+        _check(lib().sa_select_quest(self.h, layer, layer if layer_slot is None else layer_slot, _ptr(q),
+                                     _stream(stream)))
+
+    def select_window(self, layer_slot, sink=4, window=0, stream=None):
+        """select_window (selection.cpp:209-222)."""
+        _check(lib().sa_select_window(self.h, layer_slot, sink, window, _stream(stream)))
 
     def select(self, layer_slot, mode=PER_LAYER, rows_in_score=2, stream=None):
         a = SelectArgs(layer_slot, mode, rows_in_score)

@@ -197,10 +197,28 @@ SA_API sa_status sa_cache_create(const sa_cache_config* cfg, sa_cache** out) {
   return SA_OK;
 }
 
+SA_API sa_status sa_kv_enable_page_summaries(sa_cache* c, int64_t page_size) {
+  if (!c) return fail(SA_INVALID_ARGUMENT, "null cache");
+  if (page_size < 1) return fail(SA_INVALID_ARGUMENT, "KvStore: page_size must be >= 1");  // kv_store.cpp:91-93
+  if (c->page_size % page_size || (page_size & (page_size - 1)))
+    return fail(SA_NOT_SUPPORTED, "summary page size must be a power of two dividing the cache page size");
+  const uint64_t rows = static_cast<uint64_t>(c->n_layers) * c->num_pages * c->n_kv_heads * c->page_size / page_size;
+  cudaFree(c->qmin);
+  cudaFree(c->qmax);
+  c->qmin = c->qmax = nullptr;
+  SA_CUDA_CHECK(cudaMalloc(&c->qmin, rows * 128 * sizeof(__nv_bfloat16)));
+  SA_CUDA_CHECK(cudaMalloc(&c->qmax, rows * 128 * sizeof(__nv_bfloat16)));
+  c->qpage = page_size;
+  c->summ_valid.assign(c->max_seqs, 0);  // built lazily (the first Quest selection of each sequence)
+  return SA_OK;
+}
+
 SA_API sa_status sa_cache_destroy(sa_cache* c) {
   if (!c) return SA_OK;
   cudaFree(c->k_pool);
   cudaFree(c->v_pool);
+  cudaFree(c->qmin);
+  cudaFree(c->qmax);
   cudaFree(c->d_block_table);
   delete c;
   return SA_OK;
@@ -268,6 +286,7 @@ SA_API sa_status sa_kv_append(sa_cache* c, int32_t seq, int64_t n_tokens, const 
     SA_CUDA_CHECK(cudaFreeAsync(tk, s));
     SA_CUDA_CHECK(cudaFreeAsync(tv, s));
   }
+  c->summaries_stale_from(seq, c->len[seq]);
   c->len[seq] += n_tokens;
   return SA_OK;
 }
@@ -275,6 +294,7 @@ SA_API sa_status sa_kv_append(sa_cache* c, int32_t seq, int64_t n_tokens, const 
 SA_API sa_status sa_kv_truncate(sa_cache* c, int32_t seq, int64_t to_len) {
   if (sa_status st = check_seq(c, seq)) return st;
   if (to_len < 0 || to_len > c->len[seq]) return fail(SA_OUT_OF_RANGE, "KvStore: truncate beyond current length");
+  c->summaries_stale_from(seq, to_len);
   c->len[seq] = to_len;
   c->committed[seq] = std::min(c->committed[seq], to_len);
   return SA_OK;
@@ -297,6 +317,7 @@ SA_API sa_status sa_kv_set_size(sa_cache* c, int32_t seq, int64_t new_len) {
   if (sa_status st = check_seq(c, seq)) return st;
   if (new_len < 0 || new_len > c->max_context) return fail(SA_LENGTH_ERROR, "KvStore: length past max_context");
   if (sa_status st = c->reserve(seq, new_len)) return st;
+  c->summaries_stale_from(seq, std::min(new_len, c->len[seq]));
   c->len[seq] = new_len;
   c->committed[seq] = std::min(c->committed[seq], new_len);
   return SA_OK;

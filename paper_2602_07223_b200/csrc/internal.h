@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,15 @@ struct sa_cache {
   std::vector<int32_t> free_pages;           // LIFO free list
   CUtensorMap tmap_k{}, tmap_v{};            // 2-D [rows][128] bf16, box {64, 64}, SWIZZLE_128B
   CUtensorMap tmap_k128{}, tmap_v128{};      // same tensors, box {64, 128} (tcgen05 verify tiles)
+  // Quest page summaries (kv_store.cpp:90-139): per (layer, page, KV head, quest page) elementwise key
+  // min / max, bf16 (exact: min/max of bf16 keys); summ_valid[seq]: tokens whose quest pages are current
+  int64_t qpage = 0;
+  __nv_bfloat16* qmin = nullptr;
+  __nv_bfloat16* qmax = nullptr;
+  std::vector<int64_t> summ_valid;
+  void summaries_stale_from(int32_t seq, int64_t pos) {  // rows >= pos changed
+    if (qpage > 0) summ_valid[seq] = std::min(summ_valid[seq], pos / qpage * qpage);
+  }
   int device = 0;
 
   sa::CacheView view() const {
@@ -130,6 +140,14 @@ struct SelectParams {
 };
 
 sa_status comm_allreduce_i64(sa_comm* c, long long* buf, size_t count, cudaStream_t s);
+cudaError_t launch_quest_summarize(const CacheView& c, const __nv_bfloat16* qmin, const __nv_bfloat16* qmax, int qpage,
+                                   int seq, int64_t tok_lo, int64_t len, cudaStream_t s);
+cudaError_t launch_quest_select(const CacheView& c, const __nv_bfloat16* qmin, const __nv_bfloat16* qmax, int qpage,
+                                int layer, const int32_t* seq_ids, const int32_t* p0, int B, int Hq, int G,
+                                const __nv_bfloat16* q, double ratio, int64_t k_min, int k_cap, double* bounds,
+                                int64_t max_qpages, int32_t* idx, int32_t* k_out, cudaStream_t s);
+cudaError_t launch_window(const int32_t* p0, int B, int64_t sink, int64_t window, int k_cap, int32_t* idx,
+                          int32_t* k_out, cudaStream_t s);
 cudaError_t launch_weights(const float* logits, int64_t ld, const int32_t* p0, int B, int Hq, int G, int n_rows,
                            double scale, float2* stats, int n_sets, long long* fx, float* scores, int64_t ld_scores,
                            int64_t max_p, cudaStream_t s);

@@ -52,6 +52,7 @@ struct sa_runner {
   // Collect2Weights: raw logits of the collected rows per slot ([max_batch][Hq][2][ld]), row stats
   std::vector<float*> wlogits;
   float2* wstats = nullptr;
+  double* qbounds = nullptr;  // QuestLike page bounds [max_batch][max quest pages]
 };
 
 namespace {
@@ -201,6 +202,7 @@ SA_API sa_status sa_runner_destroy(sa_runner* r) {
   for (auto& kv : r->graphs) cudaGraphExecDestroy(kv.second);
   for (float* w : r->wlogits) cudaFree(w);
   cudaFree(r->wstats);
+  cudaFree(r->qbounds);
   for (auto ev : r->ev_v) if (ev) cudaEventDestroy(ev);
   for (auto ev : r->ev_s) if (ev) cudaEventDestroy(ev);
   if (r->ev_fork) cudaEventDestroy(r->ev_fork);
@@ -532,6 +534,48 @@ SA_API sa_status sa_score_weights(sa_runner* r, int32_t slot, const float* logit
                                   sa_select_mode mode, void* stream) {
   if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
   return weights_impl(r, slot, logits, ld, n_rows, mode, static_cast<cudaStream_t>(stream));
+}
+
+SA_API sa_status sa_select_quest(sa_runner* r, int32_t layer, int32_t slot, const void* q, void* stream) {
+  if (!r || !q) return fail(SA_INVALID_ARGUMENT, "null argument");
+  sa_cache* c = r->cache;
+  if (c->qpage <= 0) return fail(SA_INVALID_ARGUMENT, "select_quest: page summaries not enabled on the store");
+  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "select_quest: no batch bound");
+  if (layer < 0 || layer >= c->n_layers) return fail(SA_OUT_OF_RANGE, "select_quest: layer out of range");
+  if (slot < 0 || slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "select_quest: layer_slot");
+  const int64_t max_qp = (r->cfg.max_prefix + c->qpage - 1) / c->qpage;
+  if (max_qp > 8192) return fail(SA_NOT_SUPPORTED, "select_quest: more than 8192 summary pages (raise page_size)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (!r->qbounds) SA_CUDA_CHECK(cudaMalloc(&r->qbounds, sizeof(double) * r->cfg.max_batch * std::max<int64_t>(1, max_qp)));
+  for (int i = 0; i < r->B; ++i) {  // lazily refresh stale summaries (kv_store.cpp:127-139)
+    const int seq = r->h_seq[i];
+    const int64_t from = std::min(c->summ_valid[seq], r->h_p0[i] / c->qpage * c->qpage);
+    cudaError_t e = sa::launch_quest_summarize(c->view(), c->qmin, c->qmax, static_cast<int>(c->qpage), seq, from,
+                                               c->len[seq], s);
+    if (e != cudaSuccess) return sa::cuda_fail(e, "quest summaries");
+    c->summ_valid[seq] = c->len[seq];
+  }
+  cudaError_t e = sa::launch_quest_select(c->view(), c->qmin, c->qmax, static_cast<int>(c->qpage), layer, r->d_seq, r->d_p0,
+                                          r->B, r->Hq, r->G, static_cast<const __nv_bfloat16*>(q), r->cfg.sparse_ratio,
+                                          r->cfg.k_min, r->k_cap, r->qbounds, std::max<int64_t>(1, max_qp),
+                                          sa_runner_indices(r, slot, nullptr), sa_runner_counts(r, slot), s);
+  if (e != cudaSuccess) return sa::cuda_fail(e, "select_quest launch");
+  r->slot_layout[slot] = SA_PER_LAYER;
+  return SA_OK;
+}
+
+SA_API sa_status sa_select_window(sa_runner* r, int32_t slot, int64_t sink, int64_t window, void* stream) {
+  if (!r) return fail(SA_INVALID_ARGUMENT, "null runner");
+  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "select_window: no batch bound");
+  if (slot < 0 || slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "select_window: layer_slot");
+  if (sink < 0 || window < 0 || sink + window < 1)
+    return fail(SA_INVALID_ARGUMENT, "SelectorConfig: sink + window must be >= 1");  // selection.cpp:55-56
+  if (sink + window > r->k_cap) return fail(SA_INVALID_ARGUMENT, "select_window: sink + window exceeds index capacity");
+  cudaError_t e = sa::launch_window(r->d_p0, r->B, sink, window, r->k_cap, sa_runner_indices(r, slot, nullptr),
+                                    sa_runner_counts(r, slot), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return sa::cuda_fail(e, "select_window launch");
+  r->slot_layout[slot] = SA_PER_LAYER;
+  return SA_OK;
 }
 
 SA_API sa_status sa_runner_set_comm(sa_runner* r, sa_comm* comm) {

@@ -511,3 +511,62 @@ def test_draft_streaming_mode(cuda, ref):
         o_ref = kv.draft_layer(1, Hq, qd[b], sets, p0s[b], 1, SCALE, threads=8)
         assert rel_err_rows(got[b], o_ref) < 2e-4, (b, rel_err_rows(got[b], o_ref))
         assert rel_err_elem(got[b], o_ref) < 2e-3
+
+
+def test_quest_and_window_selectors(cuda, ref):
+    """Baseline selectors on the GPU vs the reference's own select_quest / select_window
+    (selection.cpp:209-274) over page summaries maintained like KvStore's (kv_store.cpp:90-139),
+    including a lazy refresh after appends; the draft kernel consumes the Quest set."""
+    torch = cuda
+    from oracle.pyoracle import quest_bounds, ref_select_window
+    Runner, _, selection_k = _lib()
+    L, Hkv, G, p0, page = 2, 4, 4, 2000, 8
+    Hq = Hkv * G
+    m = Matched(ref, L=L, Hkv=Hkv, n_tokens=p0, seed=111, max_context=p0 + 200, page_size=128)
+    kv = m.refs[0]
+    kv.enable_page_summaries(page)
+    m.cache.enable_page_summaries(page)
+    r = Runner(m.cache, Hq, max_rows=5, max_prefix=p0 + 100, sparse_ratio=0.1, k_min=16)
+
+    def check(prefix, layer, seed):
+        r.set_batch([0], [prefix])
+        q = normal_bf16(seed, layer, (1, Hq, D))
+        r.select_quest(layer, to_dev_bf16(q))
+        idx, cnt = r.selection(layer, 1)
+        got = idx[0, 0, : cnt[0, 0]]
+        want = kv.select_quest(q[0], layer, prefix, 0.1, 16)
+        assert cnt[0, 0] == selection_k(0.1, prefix, 16) == len(want)
+        if not np.array_equal(got, want):  # only near-tied page bounds may differ (fp32 sum order)
+            mins = np.stack([kv.page_minmax(layer, g)[0] for g in range(Hkv)])
+            maxs = np.stack([kv.page_minmax(layer, g)[1] for g in range(Hkv)])
+            n_pages = (prefix + page - 1) // page
+            b = quest_bounds(mins[:, :n_pages], maxs[:, :n_pages], q[0], G)
+            diff = set(got.tolist()) ^ set(want.tolist())
+            pages = {i // page for i in diff}
+            b_last = min(b[i // page] for i in want)
+            assert all(abs(b[pp] - b_last) <= 1e-4 * max(abs(b_last), 1.0) for pp in pages), sorted(pages)
+        return got, q
+
+    check(p0, 1, 5)
+    check(1500, 0, 6)
+    # appends (the summaries' tail pages go stale and are rebuilt lazily on the next selection)
+    extra = normal_bf16(112, 1, (60, L * Hkv, D))
+    m.cache.append(torch.from_numpy(extra).cuda(), torch.from_numpy(extra).cuda())
+    for t in range(60):
+        kv.append(extra[t], extra[t])
+    got, q = check(p0 + 60, 1, 7)
+    # the draft kernel over the Quest set (gather(T) ++ tail, then attend)
+    qd = normal_bf16(113, 1, (1, Hq, D))
+    kd, vd = normal_bf16(113, 2, (1, Hkv, D)), normal_bf16(113, 3, (1, Hkv, D))
+    od = torch.zeros((1, Hq, D), dtype=torch.float32, device="cuda")
+    r.draft(1, 1, to_dev_bf16(qd), od, to_dev_bf16(kd), to_dev_bf16(vd), scale=SCALE)
+    kk, vv = np.zeros((L * Hkv, D), np.float32), np.zeros((L * Hkv, D), np.float32)
+    kk[Hkv:], vv[Hkv:] = kd[0], vd[0]
+    kv.append(kk, vv)
+    o_ref = kv.draft_layer(1, Hq, qd[0], [got.astype(np.int64)], p0 + 60, 1, SCALE, threads=8)
+    assert rel_err_rows(od.cpu().numpy()[0], o_ref) < 2e-4
+    # window selector
+    r.set_batch([0], [p0])
+    r.select_window(1, sink=4, window=150)
+    idx, cnt = r.selection(1, 1)
+    assert np.array_equal(idx[0, 0, : cnt[0, 0]], ref_select_window(ref, p0, 4, 150))

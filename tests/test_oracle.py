@@ -257,3 +257,37 @@ def test_golden_vectors(oracle):
         sets = [g[f"dr_set_{layer}_{h}"] for h in range(Hkv)]
         assert np.array_equal(kv.draft_layer(layer, Hq, g["dr_q"], sets, p0, 2, s), g[f"dr_out_{layer}"])
     assert math.isfinite(s)
+
+
+# ----------------------------------------------------------------- Quest / window baselines
+
+def test_window_and_quest_restatement_vs_reference(ref):
+    """The Quest page bounds / pick restatement (oracle/pyoracle.py) against the reference's own
+    select_quest, and select_window KATs (selection.cpp:209-274)."""
+    from oracle.pyoracle import quest_bounds, quest_pick, ref_select_window
+    assert ref_select_window(ref, 10, 4, 3).tolist() == [0, 1, 2, 3, 7, 8, 9]
+    assert ref_select_window(ref, 5, 4, 3).tolist() == [0, 1, 2, 3, 4]
+    assert ref_select_window(ref, 0, 4, 3).tolist() == []
+    L, Hkv, d, page = 2, 2, 16, 8
+    kv = ref.kv(L, Hkv, d, 512)
+    K = normal_bf16(201, 1, (203, L * Hkv, d))
+    for t in range(100):
+        kv.append(K[t], K[t])
+    kv.enable_page_summaries(page)
+    for t in range(100, 203):  # summaries refreshed on append (refresh_tail_page)
+        kv.append(K[t], K[t])
+    for layer in range(L):
+        mins = np.stack([kv.page_minmax(layer, g)[0] for g in range(Hkv)])
+        maxs = np.stack([kv.page_minmax(layer, g)[1] for g in range(Hkv)])
+        Kl = K[:, layer * Hkv:(layer + 1) * Hkv]
+        for g in range(Hkv):
+            for p_ in range(mins.shape[1]):
+                blk = Kl[p_ * page:(p_ + 1) * page, g]
+                assert np.array_equal(mins[g, p_], blk.min(0)) and np.array_equal(maxs[g, p_], blk.max(0))
+        q = normal_bf16(202, layer, (4 * Hkv, d))
+        for prefix in (203, 150, 57):
+            want = kv.select_quest(q, layer, prefix, 0.3, 16)
+            n_pages = (prefix + page - 1) // page
+            b = quest_bounds(mins[:, :n_pages], maxs[:, :n_pages], q, 4)
+            k = min(prefix, max(int(np.floor(0.3 * prefix + 0.5)), 16))
+            assert np.array_equal(quest_pick(b, prefix, page, k), want)

@@ -51,7 +51,8 @@ f.argtypes = [ctypes.c_char_p]
 assert f(path.encode()) == 0
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 t0 = None
-print(f"{'layer':>5s} {'start':>8s} {'st_med':>8s} {'loop_med':>8s} {'loop_max':>8s} {'end_med':>8s} {'end_max':>8s} {'dt':>7s}")
+print(f"{'layer':>5s} {'start':>8s} {'st_med':>8s} {'loop_med':>8s} {'loop_max':>8s} {'end_med':>8s} {'end_max':>8s} {'dt':>7s}"
+      "   (arrival->merge_done max, loop_max->end_max)")
 prev = None
 for l in range(min(L, 64)):
     blk = raw[1024 + l * 16384: 1024 + (l + 1) * 16384].reshape(1024, 16)
@@ -63,4 +64,8 @@ for l in range(min(L, 64)):
     s0, ml, en = (blk[:, 0] - t0) / 1e3, (blk[:, 2] - t0) / 1e3, (blk[:, 1] - t0) / 1e3
     dt = s0.min() - prev if prev is not None else 0.0
     prev = s0.min()
-    print(f"{l:5d} {s0.min():8.2f} {np.median(s0):8.2f} {np.median(ml):8.2f} {ml.max():8.2f} {np.median(en):8.2f} {en.max():8.2f} {dt:7.2f}")
+    arr, mdone = (blk[:, 6] - t0) / 1e3, (blk[:, 9] - t0) / 1e3
+    has_m = blk[:, 9] > 0
+    extra = f"   {(mdone[has_m].max() - arr[blk[:, 6] > 0].max()) if has_m.any() else float('nan'):6.2f} {en.max() - ml.max():6.2f}"
+    print(extra, end="")
+    print(f"\r{l:5d} {s0.min():8.2f} {np.median(s0):8.2f} {np.median(ml):8.2f} {ml.max():8.2f} {np.median(en):8.2f} {en.max():8.2f} {dt:7.2f}")
