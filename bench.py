@@ -38,6 +38,7 @@ WORKLOADS = {
     "config4": (80, 64, 8, 131072, 4, 4, "Llama-3.1-70B-shaped (64q/8kv, 80 layers), 128K ctx, gamma 4, batch 4"),
 }
 RATIO, K_MIN, D = 0.07, 16, 128
+STRATEGIES = {"collect2": 4, "all_draft": 3, "last_accepted": 2, "collect2_weights": 5, "quest": 1, "window": 0}
 
 
 def peaks():
@@ -142,6 +143,7 @@ def run_ours(args, rank, world, local_rank):
     g.manual_seed(1234 + rank)
 
     cache = Cache(L, Hkv, D, p0 + R + 64, max_seqs=B, page_size=256)
+    strategy = STRATEGIES[args.strategy]
     # fill the prefix with synthetic post-RoPE keys/values (bf16), chunked appends
     chunk = 2048
     for b in range(B):
@@ -152,6 +154,8 @@ def run_ours(args, rank, world, local_rank):
             vv = torch.randn((n, L * Hkv, D), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
             cache.append(kk, vv, seq=b)
             done += n
+    if args.strategy == "quest":
+        cache.enable_page_summaries(8)  # SelectorConfig::page_size default (selection.hpp:36)
     torch.cuda.synchronize()
     runner = Runner(cache, Hq, max_rows=R, max_prefix=p0, max_batch=B, sparse_ratio=RATIO, k_min=K_MIN)
     runner.set_batch(list(range(B)), [p0] * B)
@@ -176,7 +180,7 @@ def run_ours(args, rank, world, local_rank):
     out_v = torch.empty((L, B, Hq, R, D), dtype=torch.float32, device=dev)
     out_d = torch.empty((gamma, L, B, Hq, D), dtype=torch.float32, device=dev)
     stream = torch.cuda.Stream(device=dev)
-    itargs = runner.iteration_args(gamma, qv, kvn, vvn, qd, kdn, vdn, out_v, out_d, strategy=COLLECT2,
+    itargs = runner.iteration_args(gamma, qv, kvn, vvn, qd, kdn, vdn, out_v, out_d, strategy=strategy,
                                    mode=PER_LAYER, scale=scale, use_graph=not args.no_graph)
     launches_per_step = runner.iteration_kernel_count(itargs)
 
@@ -217,7 +221,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2602_07223_b200 import PHASE_DRAFT, PHASE_VERIFY
 
     def phase_ms(phases, n):
-        a = runner.iteration_args(gamma, qv, kvn, vvn, qd, kdn, vdn, out_v, out_d, strategy=COLLECT2, mode=PER_LAYER,
+        a = runner.iteration_args(gamma, qv, kvn, vvn, qd, kdn, vdn, out_v, out_d, strategy=strategy, mode=PER_LAYER,
                                   scale=scale, use_graph=not args.no_graph, phases=phases)
         with torch.cuda.stream(stream):
             for _ in range(2):
@@ -256,7 +260,7 @@ def run_ours(args, rank, world, local_rank):
     # outputs come down (copy streams, both directions at once) while step i computes.
     dev_sets = [[qv, kvn, vvn, qd, kdn, vdn, out_v, out_d],
                 [torch.empty_like(t) for t in (qv, kvn, vvn, qd, kdn, vdn, out_v, out_d)]]
-    set_args = [runner.iteration_args(gamma, *d[:6], d[6], d[7], strategy=COLLECT2, mode=PER_LAYER, scale=scale,
+    set_args = [runner.iteration_args(gamma, *d[:6], d[6], d[7], strategy=strategy, mode=PER_LAYER, scale=scale,
                                       use_graph=not args.no_graph) for d in dev_sets]
     n_e2e = args.steps + max(2, args.warmup // 2)  # warm-up covers both buffer sets (both graphs captured)
     host_in = [[t.cpu().pin_memory() for t in (qv, kvn, vvn, qd, kdn, vdn)] for _ in range(2)]
@@ -330,7 +334,7 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn, post-RoPE K/V/Q, bf16)",
         "config": {"workload": f"{args.workload}: {desc}", "global_batch": seqs_global, "seq_len": p0,
-                   "gamma": gamma, "k": k, "selection": "collect2, per-layer", "layers": L,
+                   "gamma": gamma, "k": k, "selection": f"{args.strategy}, per-layer", "layers": L,
                    "parallelism": (f"{world} GPUs: batch x KV-head shards ({B} seq x {Hkv} KV heads per GPU"
                                    + (f", NCCL per-layer score exchange over {sh.head_group} GPUs)" if comm else ")")
                                    if strong else f"dp{world} (one batch-1 replica per GPU, no collective)"),
@@ -434,6 +438,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strategy", default="collect2", choices=sorted(STRATEGIES),
+                    help="selection strategy of the iteration (the headline is collect2; the others are the "
+                         "paper's variants / baselines for the overhead comparison)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = int(os.environ.get("RANK", "0"))

@@ -64,6 +64,9 @@ typedef enum sa_dtype { SA_F32 = 0, SA_BF16 = 1 } sa_dtype;
 
 /* selection.hpp:15-22 — the logit-guided strategies on the hot path. */
 typedef enum sa_strategy {
+  SA_WINDOW = 0,          /* sink + sliding window, query-agnostic (baseline) selection.cpp:209-222 */
+  SA_QUEST_LIKE = 1,      /* page min/max bounds vs the live query, re-selected before every draft
+                             step (baseline)                                  selection.cpp:224-274 */
   SA_LAST_ACCEPTED = 2,   /* one row: a+1 (needs all rows' raw logits)        selection.cpp:198-207 */
   SA_ALL_DRAFT = 3,       /* all gamma+1 rows                                 selection.cpp:183-185 */
   SA_COLLECT2 = 4,        /* rows {1, gamma+1} (the paper's method)           selection.cpp:187-196 */
@@ -225,7 +228,9 @@ SA_API sa_status sa_draft_attention(sa_runner* r, const sa_draft_args* a, void* 
  * use_graph != 0 captures the launch sequence into a CUDA graph on first use and replays it. */
 typedef struct sa_iteration_args {
   int32_t gamma;
-  sa_strategy strategy;     /* SA_COLLECT2, SA_ALL_DRAFT, SA_LAST_ACCEPTED or SA_COLLECT2_WEIGHTS */
+  sa_strategy strategy;     /* any sa_strategy: the logit-guided ones select from the verify byproduct;
+                               SA_WINDOW selects once per iteration (sink 4, window k - 4), SA_QUEST_LIKE
+                               before every draft launch from that step's query (the baselines) */
   sa_select_mode mode;
   float scale;
   const void *qv, *kv_new, *vv_new, *qd, *kd_new, *vd_new;

@@ -6,9 +6,9 @@ thin ctypes binding used by tests/ and bench.py; it never falls back to a CPU pa
 shared library is missing or no CUDA device is present, every entry point raises.
 """
 from ._lib import (  # noqa: F401
-    ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS, LAST_ACCEPTED, PER_KV_HEAD, PER_LAYER, PHASE_DRAFT, PHASE_SELECT,
+    ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS, LAST_ACCEPTED, QUEST_LIKE, WINDOW, PER_KV_HEAD, PER_LAYER, PHASE_DRAFT, PHASE_SELECT,
     PHASE_VERIFY, Cache, Comm, Runner, SpecAttnError, build, lib, lib_path, selection_k,
 )
 
 __all__ = ["Cache", "Comm", "Runner", "SpecAttnError", "build", "lib", "lib_path", "selection_k", "COLLECT2", "ALL_DRAFT",
-           "LAST_ACCEPTED", "COLLECT2_WEIGHTS", "PER_LAYER", "PER_KV_HEAD", "PHASE_VERIFY", "PHASE_SELECT", "PHASE_DRAFT"]
+           "LAST_ACCEPTED", "COLLECT2_WEIGHTS", "QUEST_LIKE", "WINDOW", "PER_LAYER", "PER_KV_HEAD", "PHASE_VERIFY", "PHASE_SELECT", "PHASE_DRAFT"]

@@ -11,7 +11,7 @@ lib_path = os.environ.get("SA_LIB_PATH") or os.path.join(HERE, "lib", "libspecat
 SA_OK = 0
 STATUS = {0: "ok", 1: "invalid_argument", 2: "domain_error", 3: "out_of_range", 4: "length_error",
           5: "cuda_error", 6: "not_supported", 7: "nccl_error"}
-LAST_ACCEPTED, ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS = 2, 3, 4, 5
+WINDOW, QUEST_LIKE, LAST_ACCEPTED, ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS = 0, 1, 2, 3, 4, 5
 PER_LAYER, PER_KV_HEAD = 0, 1
 PHASE_VERIFY, PHASE_SELECT, PHASE_DRAFT = 1, 2, 4
 F32, BF16 = 0, 1

@@ -536,17 +536,8 @@ SA_API sa_status sa_score_weights(sa_runner* r, int32_t slot, const float* logit
   return weights_impl(r, slot, logits, ld, n_rows, mode, static_cast<cudaStream_t>(stream));
 }
 
-SA_API sa_status sa_select_quest(sa_runner* r, int32_t layer, int32_t slot, const void* q, void* stream) {
-  if (!r || !q) return fail(SA_INVALID_ARGUMENT, "null argument");
+static sa_status quest_refresh(sa_runner* r, cudaStream_t s) {  // stale summaries of the bound batch
   sa_cache* c = r->cache;
-  if (c->qpage <= 0) return fail(SA_INVALID_ARGUMENT, "select_quest: page summaries not enabled on the store");
-  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "select_quest: no batch bound");
-  if (layer < 0 || layer >= c->n_layers) return fail(SA_OUT_OF_RANGE, "select_quest: layer out of range");
-  if (slot < 0 || slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "select_quest: layer_slot");
-  const int64_t max_qp = (r->cfg.max_prefix + c->qpage - 1) / c->qpage;
-  if (max_qp > 8192) return fail(SA_NOT_SUPPORTED, "select_quest: more than 8192 summary pages (raise page_size)");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (!r->qbounds) SA_CUDA_CHECK(cudaMalloc(&r->qbounds, sizeof(double) * r->cfg.max_batch * std::max<int64_t>(1, max_qp)));
   for (int i = 0; i < r->B; ++i) {  // lazily refresh stale summaries (kv_store.cpp:127-139)
     const int seq = r->h_seq[i];
     const int64_t from = std::min(c->summ_valid[seq], r->h_p0[i] / c->qpage * c->qpage);
@@ -555,6 +546,12 @@ SA_API sa_status sa_select_quest(sa_runner* r, int32_t layer, int32_t slot, cons
     if (e != cudaSuccess) return sa::cuda_fail(e, "quest summaries");
     c->summ_valid[seq] = c->len[seq];
   }
+  return SA_OK;
+}
+
+static sa_status quest_select_impl(sa_runner* r, int32_t layer, int32_t slot, const void* q, cudaStream_t s) {
+  sa_cache* c = r->cache;
+  const int64_t max_qp = (r->cfg.max_prefix + c->qpage - 1) / c->qpage;
   cudaError_t e = sa::launch_quest_select(c->view(), c->qmin, c->qmax, static_cast<int>(c->qpage), layer, r->d_seq, r->d_p0,
                                           r->B, r->Hq, r->G, static_cast<const __nv_bfloat16*>(q), r->cfg.sparse_ratio,
                                           r->cfg.k_min, r->k_cap, r->qbounds, std::max<int64_t>(1, max_qp),
@@ -562,6 +559,26 @@ SA_API sa_status sa_select_quest(sa_runner* r, int32_t layer, int32_t slot, cons
   if (e != cudaSuccess) return sa::cuda_fail(e, "select_quest launch");
   r->slot_layout[slot] = SA_PER_LAYER;
   return SA_OK;
+}
+
+static sa_status quest_prepare(sa_runner* r) {
+  sa_cache* c = r->cache;
+  if (c->qpage <= 0) return fail(SA_INVALID_ARGUMENT, "select_quest: page summaries not enabled on the store");
+  if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "select_quest: no batch bound");
+  const int64_t max_qp = (r->cfg.max_prefix + c->qpage - 1) / c->qpage;
+  if (max_qp > 8192) return fail(SA_NOT_SUPPORTED, "select_quest: more than 8192 summary pages (raise page_size)");
+  if (!r->qbounds) SA_CUDA_CHECK(cudaMalloc(&r->qbounds, sizeof(double) * r->cfg.max_batch * std::max<int64_t>(1, max_qp)));
+  return SA_OK;
+}
+
+SA_API sa_status sa_select_quest(sa_runner* r, int32_t layer, int32_t slot, const void* q, void* stream) {
+  if (!r || !q) return fail(SA_INVALID_ARGUMENT, "null argument");
+  if (sa_status st = quest_prepare(r)) return st;
+  if (layer < 0 || layer >= r->cache->n_layers) return fail(SA_OUT_OF_RANGE, "select_quest: layer out of range");
+  if (slot < 0 || slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "select_quest: layer_slot");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (sa_status st = quest_refresh(r, s)) return st;
+  return quest_select_impl(r, layer, slot, q, s);
 }
 
 SA_API sa_status sa_select_window(sa_runner* r, int32_t slot, int64_t sink, int64_t window, void* stream) {
@@ -611,7 +628,9 @@ SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_
   const int64_t L = r->cache->n_layers;
   const uint32_t ph = a->phases ? a->phases : 7u;
   const int64_t sel_kernels = a->strategy == SA_COLLECT2_WEIGHTS ? 3 : 1;  // (+ row stats, weight scores)
-  return ((ph & SA_PHASE_VERIFY) ? L : 0) + ((ph & SA_PHASE_SELECT) ? sel_kernels * L : 0) +
+  const int64_t selects = a->strategy == SA_QUEST_LIKE ? 2 * static_cast<int64_t>(a->gamma) * L  // bounds + pick per draft
+                                                       : sel_kernels * L;
+  return ((ph & SA_PHASE_VERIFY) ? L : 0) + ((ph & SA_PHASE_SELECT) ? selects : 0) +
          ((ph & SA_PHASE_DRAFT) ? static_cast<int64_t>(a->gamma) * L : 0);
 }
 
@@ -623,6 +642,8 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
                         : a->strategy == SA_LAST_ACCEPTED ? (1u << a->accepted)
                                                            : (1u | (1u << a->gamma));
   const bool weights = a->strategy == SA_COLLECT2_WEIGHTS;  // rows {1, gamma+1}, softmax-weight metric
+  const bool quest = a->strategy == SA_QUEST_LIKE, window = a->strategy == SA_WINDOW;
+  const bool guided = !quest && !window;  // selection from the verify byproduct
   const int rows_in_score = __builtin_popcount(mask);
   const size_t qv_l = static_cast<size_t>(B) * r->Hq * R * 128, kv_l = static_cast<size_t>(B) * R * r->Hkv * 128;
   const size_t qd_l = static_cast<size_t>(B) * r->Hq * 128, kd_l = static_cast<size_t>(B) * r->Hkv * 128;
@@ -649,7 +670,7 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     v.k_new = kvn ? kvn + l * kv_l : nullptr;
     v.v_new = vvn ? vvn + l * kv_l : nullptr;
     v.scale = a->scale;
-    v.score_row_mask = weights ? 0u : mask;
+    v.score_row_mask = (weights || !guided) ? 0u : mask;
     v.score_layout = a->mode;
     if (weights) {  // LogitMatrix of the collected rows for the weights kernels
       v.logits = r->wlogits[l];
@@ -666,7 +687,9 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     sel.layer_slot = l;
     sel.mode = a->mode;
     sel.rows_in_score = rows_in_score;
-    if ((skip & 2) == 0) {
+    if ((skip & 2) == 0 && window) {  // query-agnostic: once per iteration (budget k: sink 4 + window k-4)
+      if (sa_status st = sa_select_window(r, l, 4, std::max<int64_t>(0, r->k_cap - 4), r->side)) return st;
+    } else if ((skip & 2) == 0 && guided) {
       if (weights)
         if (sa_status st = weights_impl(r, l, r->wlogits[l], r->ld, rows_in_score, a->mode, r->side)) return st;
       if (r->comm && a->mode == SA_PER_LAYER) {  // §8e exchange: sums of the other KV-head shards
@@ -691,8 +714,11 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
       d.v_new = vdn ? vdn + off * kd_l : nullptr;
       d.scale = a->scale;
       d.out = a->out_d + off * qd_l;
+      if (quest && (skip & 2) == 0)  // QuestLike re-selects before every draft forward
+        if (sa_status st = quest_select_impl(r, l, l, d.q, main)) return st;
       if ((skip & 4) == 0)
-        if (sa_status st = draft_impl(r, &d, main, /*pdl=*/(j > 1 || l > 0) && !getenv("SA_DRAFT_NOPDL"))) return st;
+        if (sa_status st = draft_impl(r, &d, main, /*pdl=*/(j > 1 || l > 0) && !quest && !getenv("SA_DRAFT_NOPDL")))
+          return st;
     }
   }
   SA_CUDA_CHECK(cudaEventRecord(r->ev_join, r->side));
@@ -704,9 +730,11 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
   if (!r || !a) return fail(SA_INVALID_ARGUMENT, "null argument");
   if (a->gamma < 0 || a->gamma + 1 > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "gamma out of range");
   if (a->gamma < 1) return fail(SA_INVALID_ARGUMENT, "DecodeParams: gamma must be >= 1");
-  if (a->strategy != SA_COLLECT2 && a->strategy != SA_ALL_DRAFT && a->strategy != SA_LAST_ACCEPTED &&
-      a->strategy != SA_COLLECT2_WEIGHTS)
-    return fail(SA_NOT_SUPPORTED, "iteration: unknown strategy");
+  if (a->strategy < SA_WINDOW || a->strategy > SA_COLLECT2_WEIGHTS) return fail(SA_NOT_SUPPORTED, "iteration: unknown strategy");
+  if (a->strategy == SA_QUEST_LIKE) {  // summaries current for the bound prefixes before capture / launch
+    if (sa_status st = quest_prepare(r)) return st;
+    if (sa_status st = quest_refresh(r, static_cast<cudaStream_t>(stream))) return st;
+  }
   if (a->strategy == SA_COLLECT2_WEIGHTS)
     if (sa_status st = ensure_weight_buffers(r)) return st;  // (outside any graph capture)
   if (a->strategy == SA_LAST_ACCEPTED && (a->accepted < 0 || a->accepted > a->gamma))

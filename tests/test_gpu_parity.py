@@ -570,3 +570,53 @@ def test_quest_and_window_selectors(cuda, ref):
     r.select_window(1, sink=4, window=150)
     idx, cnt = r.selection(1, 1)
     assert np.array_equal(idx[0, 0, : cnt[0, 0]], ref_select_window(ref, p0, 4, 150))
+
+
+@pytest.mark.parametrize("strategy", ["quest", "window"])
+def test_iteration_baseline_strategies(cuda, ref, strategy):
+    """The iteration with the paper's baselines: QuestLike re-selects before every draft launch from
+    that step's query, Window once per iteration (sink 4 + window k - 4)."""
+    torch = cuda
+    from oracle.pyoracle import ref_select_window
+    from paper_2602_07223_b200 import QUEST_LIKE, WINDOW
+    Runner, _, selection_k = _lib()
+    L, Hkv, G, gamma, p0 = 2, 2, 4, 3, 1600
+    R, Hq = gamma + 1, Hkv * G
+    m = Matched(ref, L=L, Hkv=Hkv, n_tokens=p0, seed=121, max_context=p0 + 64, page_size=128)
+    kv = m.refs[0]
+    if strategy == "quest":
+        m.cache.enable_page_summaries(8)
+        kv.enable_page_summaries(8)
+    r = Runner(m.cache, Hq, max_rows=R, max_prefix=p0, sparse_ratio=0.07, k_min=16)
+    r.set_batch([0], [p0])
+    qv = normal_bf16(122, 1, (L, 1, Hq, R, D))
+    kvn, vvn = normal_bf16(122, 2, (L, 1, R, Hkv, D)), normal_bf16(122, 3, (L, 1, R, Hkv, D))
+    qd = normal_bf16(122, 4, (gamma, L, 1, Hq, D))
+    kdn, vdn = normal_bf16(122, 5, (gamma, L, 1, Hkv, D)), normal_bf16(122, 6, (gamma, L, 1, Hkv, D))
+    out_v = torch.zeros((L, 1, Hq, R, D), dtype=torch.float32, device="cuda")
+    out_d = torch.zeros((gamma, L, 1, Hq, D), dtype=torch.float32, device="cuda")
+    dev = [to_dev_bf16(x) for x in (qv, kvn, vvn, qd, kdn, vdn)]
+    st = QUEST_LIKE if strategy == "quest" else WINDOW
+    args = r.iteration_args(gamma, *dev, out_v, out_d, strategy=st, scale=SCALE, use_graph=True)
+    for _ in range(2):
+        r.iteration(args)
+    torch.cuda.synchronize()
+    k = selection_k(0.07, p0, 16)
+    for t in range(R):
+        kv.append(kvn[:, 0, t].reshape(L * Hkv, D), vvn[:, 0, t].reshape(L * Hkv, D))
+    for layer in range(L):  # verify outputs are strategy-independent
+        o_ref, _ = kv.verify_layer(layer, Hq, qv[layer, 0], p0, R, SCALE, want_logits=False, threads=8)
+        assert rel_err_rows(out_v.cpu().numpy()[layer, 0], o_ref) < 2e-4
+    kv.truncate(p0)
+    od = out_d.cpu().numpy()
+    for j in range(1, gamma + 1):
+        kv.append(kdn[j - 1, :, 0].reshape(L * Hkv, D), vdn[j - 1, :, 0].reshape(L * Hkv, D))
+        for layer in range(L):
+            if strategy == "window":
+                T = ref_select_window(ref, p0, 4, k - 4)
+            else:  # the set the reference picks from this step's query (summaries over the store)
+                T = kv.select_quest(qd[j - 1, layer, 0], layer, p0, 0.07, 16)
+            o_ref = kv.draft_layer(layer, Hq, qd[j - 1, layer, 0], [T], p0, j, SCALE, threads=8)
+            assert rel_err_rows(od[j - 1, layer, 0], o_ref) < 2e-3, (j, layer)
+    idx, cnt = r.selection(L - 1, 1)
+    assert cnt[0, 0] == k
