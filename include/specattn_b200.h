@@ -269,6 +269,21 @@ SA_API sa_status sa_runner_set_comm(sa_runner* r, sa_comm* comm);
 /* Exchange one slot's per-layer sums on `stream` (direct-API use between verify and select). */
 SA_API sa_status sa_exchange_layer_scores(sa_runner* r, int32_t layer_slot, void* stream);
 
+/* ------------------------------------------------------- speculation glue (§8f)
+ * Verification acceptance for B sequences (SPEC-only in the reference; oracle: oracle/speculation.py):
+ * p: f32 [B][gamma+1][V] target distributions of the verify rows, q: f32 [B][gamma][V] draft
+ * distributions (NULL when greedy), draft: int32 [B][gamma] draft tokens, u: f32 [B][gamma+1]
+ * uniforms in [0,1) (u[t] for the accept test of draft t, u[gamma] for the residual / bonus sample;
+ * NULL when greedy).  Sample: accept x_t iff u_t < min(1, p_t(x_t)/q_t(x_t)); on the first rejection
+ * emit a sample of normalize(max(0, p_t - q_t)); if all accepted emit a bonus ~ p_{gamma+1}.  Greedy:
+ * accept iff x_t = argmax p_t (ties to the lower id), trailing token argmax p_{a+1}.
+ * Out (device): accepted [B], emitted [B][gamma+1] (accepted drafts then the trailing token). */
+SA_API sa_status sa_accept(const float* p, const float* q, const int32_t* draft, const float* u, int32_t B,
+                           int32_t gamma, int32_t V, int32_t greedy, int32_t* accepted, int32_t* emitted, void* stream);
+/* Commit after acceptance (kv_store.cpp:51-65): the verify rows [p0, p0+accepted] (y and
+ * the accepted drafts) stay, the store is truncated to p0 + accepted + 1 and committed. */
+SA_API sa_status sa_kv_commit_accepted(sa_cache* cache, int32_t seq, int64_t p0, int32_t accepted);
+
 /* Reference helper: selection_k (selection.cpp:63-66). */
 SA_API int64_t sa_selection_k(double sparse_ratio, int64_t prefix_len, int64_t k_min);
 

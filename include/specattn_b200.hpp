@@ -37,6 +37,12 @@ inline void check(sa_status st) {
 }
 
 // selection.hpp:48-49 / selection.cpp:63-66
+// speculation::verify acceptance over device buffers; see sa_accept.
+inline void accept(const float* p, const float* q, const int32_t* draft, const float* u, int32_t B, int32_t gamma,
+                   int32_t V, bool greedy, int32_t* accepted, int32_t* emitted, void* stream = nullptr) {
+  check(sa_accept(p, q, draft, u, B, gamma, V, greedy ? 1 : 0, accepted, emitted, stream));
+}
+
 inline int64_t selection_k(double sparse_ratio, int64_t prefix_len, int64_t k_min) {
   return sa_selection_k(sparse_ratio, prefix_len, k_min);
 }
@@ -88,6 +94,10 @@ class KvStore {
   }
   void truncate(int64_t to_len, int32_t seq = 0) { check(sa_kv_truncate(h_, seq, to_len)); }  // :51-58
   void set_committed(int64_t len, int32_t seq = 0) { check(sa_kv_set_committed(h_, seq, len)); }  // :60-65
+  // keep verify rows [p0, p0+accepted], truncate to p0+accepted+1, commit.
+  void commit_accepted(int64_t p0, int32_t accepted, int32_t seq = 0) {
+    check(sa_kv_commit_accepted(h_, seq, p0, accepted));
+  }
   // kv_store.cpp:67-88: strictly increasing indices -> (K, V) row-major fp32 copies (host).
   std::pair<std::vector<float>, std::vector<float>> gather(int64_t layer, int64_t kv_head,
                                                            const std::vector<int64_t>& indices,

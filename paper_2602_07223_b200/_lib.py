@@ -92,6 +92,8 @@ SIGNATURES = {
     "sa_dev_trace_dump": (C.c_int, [C.c_char_p]),
     "sa_score_weights": (C.c_int, [_vp, _i32, _vp, _i64, _i32, C.c_int, _vp]),
     "sa_kv_enable_page_summaries": (C.c_int, [_vp, _i64]),
+    "sa_accept": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "sa_kv_commit_accepted": (C.c_int, [_vp, _i32, _i64, _i32]),
     "sa_select_quest": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),
     "sa_select_window": (C.c_int, [_vp, _i32, _i64, _i64, _vp]),
     "sa_comm_unique_id": (C.c_int, [_vp]),
@@ -207,6 +209,10 @@ class Cache:
 
     def reserve(self, n, seq=0):
         _check(lib().sa_kv_reserve(self.h, seq, n))
+
+    def commit_accepted(self, p0, accepted, seq=0):
+        """Keep verify rows [p0, p0+accepted], truncate to p0+accepted+1 and commit."""
+        _check(lib().sa_kv_commit_accepted(self.h, seq, p0, accepted))
 
     def set_size(self, n, seq=0):
         _check(lib().sa_kv_set_size(self.h, seq, n))
@@ -384,6 +390,18 @@ class Comm:
             self.h = None
 
     __del__ = close
+
+
+def accept(p, draft, q=None, u=None, greedy=False, stream=None):
+    """Verification acceptance on the device: p [B][g+1][V], q [B][g][V] f32,
+    draft [B][g] int32, u [B][g+1] f32 -> (accepted [B], emitted [B][g+1]) int32 device tensors."""
+    import torch
+    B, g1, V = p.shape
+    acc = torch.empty((B,), dtype=torch.int32, device=p.device)
+    em = torch.full((B, g1), -1, dtype=torch.int32, device=p.device)
+    _check(lib().sa_accept(_ptr(p), _ptr(q), _ptr(draft), _ptr(u), B, g1 - 1, V, int(greedy), _ptr(acc), _ptr(em),
+                           _stream(stream)))
+    return acc, em
 
 
 def cudart_memcpy(dst: int, src: int, nbytes: int) -> None:

@@ -197,6 +197,26 @@ SA_API sa_status sa_cache_create(const sa_cache_config* cfg, sa_cache** out) {
   return SA_OK;
 }
 
+SA_API sa_status sa_accept(const float* p, const float* q, const int32_t* draft, const float* u, int32_t B,
+                           int32_t gamma, int32_t V, int32_t greedy, int32_t* accepted, int32_t* emitted, void* stream) {
+  if (!p || !draft || !accepted || !emitted || (!greedy && (!q || !u)))
+    return fail(SA_INVALID_ARGUMENT, "accept: null argument");
+  if (B < 1 || gamma < 1 || V < 1) return fail(SA_INVALID_ARGUMENT, "DecodeParams: gamma must be >= 1");
+  cudaError_t e = sa::launch_accept(p, q, draft, u, B, gamma, V, greedy, accepted, emitted,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return sa::cuda_fail(e, "accept launch");
+  return SA_OK;
+}
+
+SA_API sa_status sa_kv_commit_accepted(sa_cache* c, int32_t seq, int64_t p0, int32_t accepted) {
+  if (!c) return fail(SA_INVALID_ARGUMENT, "null cache");
+  if (seq < 0 || seq >= c->max_seqs) return fail(SA_OUT_OF_RANGE, "sequence id out of range");
+  if (accepted < 0 || p0 < 0 || p0 + accepted + 1 > c->len[seq])
+    return fail(SA_OUT_OF_RANGE, "KvStore: truncate beyond current length");
+  if (sa_status st = sa_kv_truncate(c, seq, p0 + accepted + 1)) return st;
+  return sa_kv_set_committed(c, seq, p0 + accepted + 1);
+}
+
 SA_API sa_status sa_kv_enable_page_summaries(sa_cache* c, int64_t page_size) {
   if (!c) return fail(SA_INVALID_ARGUMENT, "null cache");
   if (page_size < 1) return fail(SA_INVALID_ARGUMENT, "KvStore: page_size must be >= 1");  // kv_store.cpp:91-93

@@ -620,3 +620,92 @@ def test_iteration_baseline_strategies(cuda, ref, strategy):
             assert rel_err_rows(od[j - 1, layer, 0], o_ref) < 2e-3, (j, layer)
     idx, cnt = r.selection(L - 1, 1)
     assert cnt[0, 0] == k
+
+
+# ----------------------------------------------------------------------- speculation glue (§8f)
+
+def _spec_case(rng, B, g, V, temp=1.0):
+    z = rng.standard_normal((B, 1, V)) * 2.0
+    p = np.exp(z + temp * rng.standard_normal((B, g + 1, V)))
+    q = np.exp(z + temp * rng.standard_normal((B, g, V)))
+    p = (p / p.sum(-1, keepdims=True)).astype(np.float32)
+    q = (q / q.sum(-1, keepdims=True)).astype(np.float32)
+    cq = np.cumsum(q.astype(np.float64), -1)
+    draft = np.minimum((cq < rng.random((B, g, 1)) * cq[..., -1:]).sum(-1), V - 1).astype(np.int32)
+    u = rng.random((B, g + 1)).astype(np.float32)
+    return p, q, draft, u
+
+
+@pytest.mark.parametrize("B,g,V", [(256, 4, 1000), (8, 3, 50000), (64, 1, 7)])
+def test_accept_parity(cuda, B, g, V):
+    torch = cuda
+    from oracle.speculation import accept as ref_accept
+    from paper_2602_07223_b200 import accept
+    rng = np.random.default_rng(B + V)
+    p, q, draft, u = _spec_case(rng, B, g, V)
+    acc, em = accept(*(torch.from_numpy(x).cuda() for x in (p, draft)), q=torch.from_numpy(q).cuda(),
+                     u=torch.from_numpy(u).cuda())
+    acc, em = acc.cpu().numpy(), em.cpu().numpy()
+    seen = set()
+    for b in range(B):
+        a, e = ref_accept(p[b], draft[b], q=q[b], u=u[b])
+        assert acc[b] == a and list(em[b, :a + 1]) == e, b
+        assert np.all(em[b, a + 1:] == -1)
+        seen.add(a)
+    if B >= 64:
+        assert len(seen) >= 2  # both accept and reject paths exercised
+
+
+def test_accept_greedy_ties(cuda):
+    torch = cuda
+    from oracle.speculation import accept as ref_accept
+    from paper_2602_07223_b200 import accept
+    rng = np.random.default_rng(4)
+    B, g, V = 64, 4, 5000
+    p = rng.integers(0, 4, size=(B, g + 1, V)).astype(np.float32)  # many exact ties at the max
+    draft = np.argmax(p[:, :g], -1).astype(np.int32)
+    flip = rng.random((B, g)) < 0.3
+    draft[flip] = rng.integers(0, V, size=flip.sum())
+    acc, em = accept(torch.from_numpy(p).cuda(), torch.from_numpy(draft).cuda(), greedy=True)
+    acc, em = acc.cpu().numpy(), em.cpu().numpy()
+    for b in range(B):
+        a, e = ref_accept(p[b], draft[b], greedy=True)
+        assert acc[b] == a and list(em[b, :a + 1]) == e
+
+
+def test_accept_emission_distribution(cuda):
+    # empirical single-step emission distribution over 100000 seeded runs matches p, TV < 0.01
+    torch = cuda
+    from paper_2602_07223_b200 import accept
+    rng = np.random.default_rng(12)
+    B, V = 100000, 8
+    p1 = rng.dirichlet(np.ones(V)).astype(np.float32)
+    q1 = rng.dirichlet(np.ones(V)).astype(np.float32)
+    p = np.broadcast_to(p1, (B, 2, V)).copy()
+    q = np.broadcast_to(q1, (B, 1, V)).copy()
+    cq = np.cumsum(q1.astype(np.float64))
+    draft = np.minimum(np.searchsorted(cq / cq[-1], rng.random((B, 1)), side="right"), V - 1).astype(np.int32)
+    u = rng.random((B, 2)).astype(np.float32)
+    acc, em = accept(*(torch.from_numpy(x).cuda() for x in (p, draft)), q=torch.from_numpy(q).cuda(),
+                     u=torch.from_numpy(u).cuda())
+    first = em[:, 0].cpu().numpy()
+    freq = np.bincount(first, minlength=V) / B
+    assert 0.5 * np.abs(freq - p1).sum() < 0.01
+    rate = acc.float().mean().item()
+    assert abs(rate - np.minimum(p1, q1).sum()) < 0.01  # E[accept] = sum_x min(p, q)
+
+
+def test_commit_accepted(cuda, ref):
+    torch = cuda
+    from paper_2602_07223_b200 import Cache, SpecAttnError
+    c = Cache(1, 1, max_context=256, page_size=128)
+    try:
+        k = torch.randn(10, 1, 128, device="cuda").to(torch.bfloat16)
+        c.append(k, k.clone())
+        c.set_committed(5)
+        c.commit_accepted(5, 2)  # verify rows 5..9 = [y, x1..x4]; a = 2 keeps 5,6,7
+        assert c.size() == 8 and c.committed() == 8
+        with pytest.raises(SpecAttnError):
+            c.commit_accepted(5, 4)  # beyond the current length
+    finally:
+        c.close()

@@ -291,3 +291,66 @@ def test_window_and_quest_restatement_vs_reference(ref):
             b = quest_bounds(mins[:, :n_pages], maxs[:, :n_pages], q, 4)
             k = min(prefix, max(int(np.floor(0.3 * prefix + 0.5)), 16))
             assert np.array_equal(quest_pick(b, prefix, page, k), want)
+
+
+# ----------------------------------------------------------------- speculation glue
+# The reference ships no speculation code: the restatement (oracle/speculation.py) is pinned on the
+# SPEC's own examples here and the GPU kernel on the restatement (tests/test_gpu_parity.py).
+
+def test_residual_distribution_kats():
+    from oracle.speculation import residual_distribution
+    assert np.array_equal(residual_distribution([0.5, 0.5], [1.0, 0.0]), [0.0, 1.0])
+    assert np.array_equal(residual_distribution([0.7, 0.3], [0.3, 0.7]), [1.0, 0.0])
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        p, q = rng.dirichlet(np.ones(16)), rng.dirichlet(np.ones(16))
+        r = residual_distribution(p, q)
+        assert r.sum() == pytest.approx(1.0, abs=1e-12)
+        assert np.all(r[p <= q] == 0.0)
+    with pytest.raises(ValueError):
+        residual_distribution([0.25, 0.75], [0.25, 0.75])
+
+
+def test_accept_kats():
+    from oracle.speculation import accept
+    rng = np.random.default_rng(5)
+    # q_t = p_t for all t -> every accept probability is 1; a = gamma
+    for _ in range(20):
+        p = rng.dirichlet(np.ones(32), size=5).astype(np.float32)
+        draft = rng.integers(0, 32, size=4)
+        a, em = accept(p, draft, q=p[:4], u=rng.random(5).astype(np.float32))
+        assert a == 4 and em[:4] == list(draft) and len(em) == 5
+    # vocab {a,b}: q = (1,0), p = (0.5,0.5): accept a w.p. 0.5, on reject emit b
+    p = np.array([[0.5, 0.5], [0.5, 0.5]], np.float32)
+    q = np.array([[1.0, 0.0]], np.float32)
+    acc = 0
+    for i in range(2000):
+        a, em = accept(p, [0], q=q, u=np.array([rng.random(), rng.random()], np.float32))
+        if a == 1:
+            acc += 1
+        else:
+            assert em == [1]
+    assert abs(acc / 2000 - 0.5) < 0.05
+    # greedy: accept iff x_t = argmax p_t (ties -> lower id); corrected token = argmax
+    p = np.array([[0.1, 0.45, 0.45], [0.6, 0.2, 0.2], [0.3, 0.3, 0.4]], np.float32)
+    assert accept(p, [1, 0], greedy=True) == (2, [1, 0, 2])
+    assert accept(p, [2, 0], greedy=True) == (0, [1])
+    assert accept(p, [1, 2], greedy=True) == (1, [1, 0])
+
+
+def test_accept_emission_matches_target():
+    # single-step emission distribution equals p (modified rejection sampling is exact): Monte-Carlo
+    from oracle.speculation import accept
+    rng = np.random.default_rng(9)
+    V = 4
+    p = rng.dirichlet(np.ones(V), size=2).astype(np.float32)
+    q = rng.dirichlet(np.ones(V), size=1).astype(np.float32)
+    n = 6000
+    counts = np.zeros(V)
+    q64 = q[0].astype(np.float64)
+    q64 /= q64.sum()
+    for _ in range(n):
+        x = rng.choice(V, p=q64)
+        _, em = accept(p, [x], q=q, u=rng.random(2).astype(np.float32))
+        counts[em[0]] += 1
+    assert 0.5 * np.abs(counts / n - p[0]).sum() < 0.03
