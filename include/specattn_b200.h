@@ -284,6 +284,25 @@ SA_API sa_status sa_accept(const float* p, const float* q, const int32_t* draft,
  * the accepted drafts) stay, the store is truncated to p0 + accepted + 1 and committed. */
 SA_API sa_status sa_kv_commit_accepted(sa_cache* cache, int32_t seq, int64_t p0, int32_t accepted);
 
+/* ------------------------------------------------------- model-side producer (§8f rank 4)
+ * RMSNorm -> fused Q/K/V projection -> RoPE for the tokens of one layer, emitting exactly the bf16
+ * q / k_new / v_new buffers sa_verify_attention (rows = gamma+1) and sa_draft_attention (rows = 1)
+ * take.  Weights (caller-owned device memory, must outlive the handle): w_qkv bf16
+ * [n_layers][(Hq + 2 Hkv) * 128][d_model] = per layer the rows of wq^T, wk^T, wv^T (weights.hpp:21-23;
+ * Eigen's column-major wq is already this layout), attn_norm_gain f32 [n_layers][d_model]
+ * (weights.hpp:25).  norm_eps / rope_theta: config.hpp:32,34.  rope_style 0 = half-split pairs
+ * (i, i+64), 1 = interleaved pairs (2j, 2j+1); both rotate pair j by pos * theta^(-2j/128). */
+typedef struct sa_qkv sa_qkv;
+SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, int32_t n_layers, int32_t d_model,
+                               int32_t n_q_heads, int32_t n_kv_heads, double norm_eps, double rope_theta,
+                               int32_t rope_style, sa_qkv** out);
+SA_API sa_status sa_qkv_destroy(sa_qkv* h);
+/* x: f32 [B][rows][d_model] hidden states (device); positions: int32 [B] (device) absolute position of
+ * each sequence's row 0 (row r is at positions[b] + r); 1 <= B * rows <= 128.  Out (device, bf16):
+ * q [B][Hq][rows][128], k_new / v_new [B][rows][Hkv][128].  Stream-ordered, graph-capturable. */
+SA_API sa_status sa_qkv_project(sa_qkv* h, int32_t layer, const float* x, const int32_t* positions, int32_t B,
+                                int32_t rows, void* q, void* k_new, void* v_new, void* stream);
+
 /* Reference helper: selection_k (selection.cpp:63-66). */
 SA_API int64_t sa_selection_k(double sparse_ratio, int64_t prefix_len, int64_t k_min);
 

@@ -7,8 +7,8 @@ shared library is missing or no CUDA device is present, every entry point raises
 """
 from ._lib import (  # noqa: F401
     ALL_DRAFT, COLLECT2, COLLECT2_WEIGHTS, LAST_ACCEPTED, QUEST_LIKE, WINDOW, PER_KV_HEAD, PER_LAYER, PHASE_DRAFT, PHASE_SELECT,
-    PHASE_VERIFY, Cache, Comm, Runner, SpecAttnError, accept, build, lib, lib_path, selection_k,
+    PHASE_VERIFY, Cache, Comm, QkvProjection, Runner, SpecAttnError, accept, build, lib, lib_path, selection_k,
 )
 
-__all__ = ["accept", "Cache", "Comm", "Runner", "SpecAttnError", "build", "lib", "lib_path", "selection_k", "COLLECT2", "ALL_DRAFT",
+__all__ = ["accept", "QkvProjection", "Cache", "Comm", "Runner", "SpecAttnError", "build", "lib", "lib_path", "selection_k", "COLLECT2", "ALL_DRAFT",
            "LAST_ACCEPTED", "COLLECT2_WEIGHTS", "QUEST_LIKE", "WINDOW", "PER_LAYER", "PER_KV_HEAD", "PHASE_VERIFY", "PHASE_SELECT", "PHASE_DRAFT"]

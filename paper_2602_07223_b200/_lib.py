@@ -92,6 +92,9 @@ SIGNATURES = {
     "sa_dev_trace_dump": (C.c_int, [C.c_char_p]),
     "sa_score_weights": (C.c_int, [_vp, _i32, _vp, _i64, _i32, C.c_int, _vp]),
     "sa_kv_enable_page_summaries": (C.c_int, [_vp, _i64]),
+    "sa_qkv_create": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, C.c_double, C.c_double, _i32, C.POINTER(_vp)]),
+    "sa_qkv_destroy": (C.c_int, [_vp]),
+    "sa_qkv_project": (C.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "sa_accept": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "sa_kv_commit_accepted": (C.c_int, [_vp, _i32, _i64, _i32]),
     "sa_select_quest": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),
@@ -390,6 +393,48 @@ class Comm:
             self.h = None
 
     __del__ = close
+
+
+class QkvProjection:
+    """Model-side producer: RMSNorm -> fused QKV projection -> RoPE on the device.
+    w_qkv: bf16 [L][(Hq+2Hkv)*128][d_model] device tensor (rows of wq^T, wk^T, wv^T per layer),
+    gain: f32 [L][d_model].  The tensors are kept referenced by the handle."""
+
+    def __init__(self, w_qkv, gain, n_q_heads, n_kv_heads, norm_eps=1e-5, rope_theta=10000.0, rope_style=0):
+        import torch
+        if w_qkv.dtype != torch.bfloat16 or gain.dtype != torch.float32:
+            raise SpecAttnError(1, "QkvProjection expects bf16 weights and f32 gains")
+        self.w, self.gain = w_qkv.contiguous(), gain.contiguous()
+        self.L, _, self.d_model = self.w.shape
+        self.Hq, self.Hkv = n_q_heads, n_kv_heads
+        h = _vp()
+        _check(lib().sa_qkv_create(_ptr(self.w), _ptr(self.gain), self.L, self.d_model, n_q_heads, n_kv_heads,
+                                   norm_eps, rope_theta, rope_style, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sa_qkv_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def project(self, layer, x, positions, q=None, k_new=None, v_new=None, stream=None):
+        """x: f32 [B][rows][d_model] device, positions int32 [B] device -> (q, k_new, v_new) bf16."""
+        import torch
+        B, rows, _ = x.shape
+        dev = x.device
+        if q is None:
+            q = torch.empty((B, self.Hq, rows, 128), dtype=torch.bfloat16, device=dev)
+            k_new = torch.empty((B, rows, self.Hkv, 128), dtype=torch.bfloat16, device=dev)
+            v_new = torch.empty((B, rows, self.Hkv, 128), dtype=torch.bfloat16, device=dev)
+        _check(lib().sa_qkv_project(self.h, layer, _ptr(x), _ptr(positions), B, rows, _ptr(q), _ptr(k_new),
+                                    _ptr(v_new), _stream(stream)))
+        return q, k_new, v_new
 
 
 def accept(p, draft, q=None, u=None, greedy=False, stream=None):

@@ -28,6 +28,11 @@ sa_status cuda_fail(cudaError_t e, const char* where) {
 }
 
 bool encode_tensor_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t box_rows, std::string* err) {
+  return encode_tensor_map_2d(map, base, 128, rows, box_rows, err);
+}
+
+bool encode_tensor_map_2d(CUtensorMap* map, void* base, uint64_t cols, uint64_t rows, uint32_t box_rows,
+                          std::string* err) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -41,8 +46,8 @@ bool encode_tensor_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t box
     *err = "cuTensorMapEncodeTiled unavailable";
     return false;
   }
-  cuuint64_t dims[2] = {128, rows};
-  cuuint64_t strides[1] = {256};
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {64, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr,

@@ -23,6 +23,9 @@ sa_status cuda_fail(cudaError_t e, const char* where);
   } while (0)
 
 bool encode_tensor_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t box_rows, std::string* err);
+// bf16 [rows][cols] row-major, box {64, box_rows}, SWIZZLE_128B
+bool encode_tensor_map_2d(CUtensorMap* map, void* base, uint64_t cols, uint64_t rows, uint32_t box_rows,
+                          std::string* err);
 
 }  // namespace sa
 

@@ -709,3 +709,61 @@ def test_commit_accepted(cuda, ref):
             c.commit_accepted(5, 4)  # beyond the current length
     finally:
         c.close()
+
+
+# ----------------------------------------------------------------- model-side producer (§8f rank 4)
+
+def _bf16_round(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("D,Hq,Hkv,B,rows,style", [
+    (256, 8, 2, 1, 5, 0),       # reference toy config (config.hpp:52-54)
+    (4096, 32, 8, 1, 5, 0),     # Llama-3.1-8B shape, verify rows
+    (4096, 32, 8, 4, 1, 1),     # draft rows, interleaved RoPE
+    (1024, 8, 2, 16, 5, 0),     # 80 tokens
+    (512, 4, 4, 32, 4, 1),      # 128 tokens (the per-call maximum)
+])
+def test_qkv_projection_parity(cuda, D, Hq, Hkv, B, rows, style):
+    torch = cuda
+    from oracle.model import qkv_project
+    from paper_2602_07223_b200 import QkvProjection
+    rng = np.random.default_rng(D + B * rows + style)
+    L, n_out = 2, (Hq + 2 * Hkv) * 128
+    w = _bf16_round(rng.standard_normal((L, n_out, D)) / np.sqrt(D))  # N(0, 1/fan_in), weights.hpp:39
+    gain = (1.0 + 0.1 * rng.standard_normal((L, D))).astype(np.float32)
+    x = rng.standard_normal((B, rows, D)).astype(np.float32) * 3.0
+    pos = rng.integers(0, 131072 - rows, size=B).astype(np.int32)
+    proj = QkvProjection(torch.from_numpy(w).to(torch.bfloat16).cuda(), torch.from_numpy(gain).cuda(), Hq, Hkv,
+                         rope_style=style)
+    for layer in range(L):
+        q, k, v = proj.project(layer, torch.from_numpy(x).cuda(), torch.from_numpy(pos).cuda())
+        torch.cuda.synchronize()
+        rq, rk, rv = qkv_project(x, w[layer], gain[layer], Hq, Hkv, pos, style=style)
+        for got, ref in ((q, rq), (k, rk), (v, rv)):
+            got = got.float().cpu().numpy()
+            scale = np.sqrt(np.mean(ref * ref, axis=-1, keepdims=True))
+            err = np.abs(got - ref)
+            assert np.all(err <= 2.0 ** -8 * np.abs(ref) + 1e-5 * scale), err.max()
+            # the fp32-accurate product rounds like the exact value except within ~1e-5 of a tie
+            assert np.mean(got == _bf16_round(ref)) > 0.995
+    proj.close()
+
+
+def test_qkv_projection_deterministic_and_errors(cuda):
+    torch = cuda
+    from paper_2602_07223_b200 import QkvProjection, SpecAttnError
+    rng = np.random.default_rng(8)
+    w = torch.from_numpy(_bf16_round(rng.standard_normal((1, 12 * 128, 512)) / 23)).to(torch.bfloat16).cuda()
+    proj = QkvProjection(w, torch.ones(1, 512, device="cuda"), 8, 2)
+    x = torch.randn(2, 5, 512, device="cuda")
+    pos = torch.tensor([100, 7], dtype=torch.int32, device="cuda")
+    a = [t.clone() for t in proj.project(0, x, pos)]
+    b = proj.project(0, x, pos)
+    assert all(torch.equal(u, v) for u, v in zip(a, b))
+    with pytest.raises(SpecAttnError):
+        proj.project(1, x, pos)  # layer out of range
+    with pytest.raises(SpecAttnError):
+        proj.project(0, torch.randn(2, 65, 512, device="cuda"), pos)  # > 128 tokens
+    proj.close()

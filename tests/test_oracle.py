@@ -354,3 +354,32 @@ def test_accept_emission_matches_target():
         _, em = accept(p, [x], q=q, u=rng.random(2).astype(np.float32))
         counts[em[0]] += 1
     assert 0.5 * np.abs(counts / n - p[0]).sum() < 0.03
+
+
+# ----------------------------------------------------------------- model-side producer
+
+@pytest.mark.parametrize("style", [0, 1])
+def test_apply_rope_kats(style):
+    from oracle.model import apply_rope
+    rng = np.random.default_rng(21 + style)
+    v = rng.standard_normal(128)
+    assert np.array_equal(apply_rope(v, 0, style=style), v)  # position 0 -> identity
+    for pos in (1, 17, 4095, 131071):
+        assert abs(np.linalg.norm(apply_rope(v, pos, style=style)) - np.linalg.norm(v)) <= 1e-6 * np.linalg.norm(v)
+    for m, n in ((5, 3), (1000, 17), (40000, 39000)):  # relative-position identity
+        q, k = rng.standard_normal(128), rng.standard_normal(128)
+        lhs = apply_rope(q, m, style=style) @ apply_rope(k, n, style=style)
+        rhs = apply_rope(q, m - n, style=style) @ k
+        assert abs(lhs - rhs) <= 1e-5 * max(1.0, abs(rhs))
+    with pytest.raises(ValueError):
+        apply_rope(np.ones(7), 3)
+
+
+def test_rms_norm_and_projection_shapes():
+    from oracle.model import qkv_project, rms_norm
+    x = np.array([[3.0, 4.0]])
+    assert np.allclose(rms_norm(x, [1.0, 2.0], 0.0), [[3 / np.sqrt(12.5), 8 / np.sqrt(12.5)]])
+    rng = np.random.default_rng(2)
+    w = rng.standard_normal(((4 + 2 * 2) * 128, 64))
+    q, k, v = qkv_project(rng.standard_normal((2, 3, 64)), w, np.ones(64), 4, 2, [0, 9])
+    assert q.shape == (2, 4, 3, 128) and k.shape == (2, 3, 2, 128) and v.shape == (2, 3, 2, 128)
