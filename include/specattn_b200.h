@@ -287,7 +287,8 @@ SA_API sa_status sa_kv_commit_accepted(sa_cache* cache, int32_t seq, int64_t p0,
 /* ------------------------------------------------------- model-side producer (§8f rank 4)
  * RMSNorm -> fused Q/K/V projection -> RoPE for the tokens of one layer, emitting exactly the bf16
  * q / k_new / v_new buffers sa_verify_attention (rows = gamma+1) and sa_draft_attention (rows = 1)
- * take.  Weights (caller-owned device memory, must outlive the handle): w_qkv bf16
+ * take.  Weights (device or host memory; repacked into a handle-owned copy at create, so the caller
+ * may free them afterwards): w_qkv bf16
  * [n_layers][(Hq + 2 Hkv) * 128][d_model] = per layer the rows of wq^T, wk^T, wv^T (weights.hpp:21-23;
  * Eigen's column-major wq is already this layout), attn_norm_gain f32 [n_layers][d_model]
  * (weights.hpp:25).  norm_eps / rope_theta: config.hpp:32,34.  rope_style 0 = half-split pairs

@@ -18,12 +18,25 @@
 // product is fp32-accurate although the MMA is bf16 (~2^-17 relative input representation error);
 // the 1/rms factor is applied in the epilogue (it commutes with the projection).
 //
-// Grid: (splits, heads) with the splits of one head forming a thread-block cluster over d_model
-// (split-K, ~148 CTAs streaming at once); the partial tiles are reduced in a fixed order through
-// DSMEM (deterministic), each CTA of the cluster finishing a slice of the tokens: scale, RoPE,
-// bf16, store.  Weight tiles are streamed before griddepcontrol.wait (they do not depend on the
-// previous kernel), so under PDL the weight stream overlaps the previous kernel's tail.
+// Weights are repacked once at sa_qkv_create into [L][head][d_model/64] tiles of 128 x 64 bf16, each
+// 16 KB contiguous and already in the UMMA SWIZZLE_128B order, so one CTA's share of a layer is one
+// contiguous run read with 1-D bulk copies; the part of the run past the smem ring is prefetched into
+// L2 at CTA start.
+//
+// Grid: stream-K — one CTA per SM, each taking an equal contiguous run of the layer's (head, k-block)
+// units (a run touches at most two heads; TMEM accumulators per head, the K-steps rotating over
+// independent accumulators).  Weight streaming is bound by the chip's L2->SM rate (~40 GB/s per SM
+// with every SM pulling), so every SM must stream: a split-K cluster grid left 3-CTA clusters
+// unschedulable past 45 and ran a second wave.  Each CTA writes its per-head partial to global memory;
+// the last of a head's contributors reduces them in CTA order (deterministic) and finishes: 1/rms,
+// RoPE (cos/sin per token and pair from qkv_prepare), bf16, store.  Two launches per call: qkv_prepare
+// (1/rms, the hi/lo token planes, the RoPE table) and qkv_gemm, chained with PDL; the weight tiles of
+// the ring are loaded before griddepcontrol.wait (they depend on nothing), so they overlap the previous
+// kernel's tail.  Measured (Llama-3.1-8B shape, 5 tokens, 32-layer chain): 24 us per layer = 2.1 TB/s
+// of weights; DESIGN.md has the timeline and what bounds it.
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -31,11 +44,15 @@ struct sa_qkv {
   int L = 0, Hq = 0, Hkv = 0, D = 0, n_out = 0, nkb = 0, style = 0;
   float eps = 1e-5f;
   double theta = 10000.0;
-  const __nv_bfloat16* w = nullptr;  // [L][n_out][D] (caller-owned device memory)
-  const float* gain = nullptr;       // [L][D]
-  __nv_bfloat16* xbuf = nullptr;     // [nkb][N][64] hi/lo token planes (N <= 256)
-  float* rbuf = nullptr;             // [128] 1/rms per token
-  CUtensorMap tmap_w{}, tmap_x{};
+  __nv_bfloat16* wpack = nullptr;  // [L][heads][nkb][128][64] swizzled 16 KB tiles (owned copy)
+  float* gain = nullptr;           // [L][D] (owned copy)
+  __nv_bfloat16* xbuf = nullptr;   // [nkb][N][64] swizzled hi/lo token planes (N <= 256)
+  float* rbuf = nullptr;           // [128] 1/rms per token
+  float2* rope = nullptr;          // [128][64] (cos, sin) per token and RoPE pair
+  float* part = nullptr;           // [max grid][2][256][128] split-K partials
+  int* counters = nullptr;         // [heads]
+  int max_grid = 0;
+  unsigned long long* trace = nullptr;  // dev-only
   int device = 0, num_sms = 148;
 };
 
@@ -45,24 +62,49 @@ constexpr int kQkvMaxTokens = 128;
 constexpr int kQkvThreads = 192;  // warp 0 TMA, warp 1 MMA + TMEM, warps 2-5 epilogue
 constexpr int kQkvSmem = 200 * 1024;
 constexpr int kWTile = 128 * 64 * 2;  // 16 KB weight tile (128 output features x 64 of d_model)
+constexpr int kEpiBytes = 8 * 128 * 4;  // epilogue token-group buffer (end of the ring region)
+constexpr int kMaxStages = 12;
 
 struct QkvParams {
-  int layer, n_out, nkb, n_tok, rows, NT, N, Hq, Hkv, splits, style;
+  int layer, n_out, nkb, n_tok, rows, NT, N, Hq, Hkv, heads, style;
   float eps;
   double log2_theta;
-  const __nv_bfloat16* w;
+  const __nv_bfloat16* wpack;
   const float* x;
   const float* gain;
   const int32_t* pos0;
   __nv_bfloat16* xbuf;
   float* rbuf;
+  float2* rope;   // [128 tokens][64 pairs] (cos, sin)
+  float* part;    // [grid][2][N][128] per-CTA partial accumulators (one per head touched)
+  int* counters;  // [heads] arrivals, re-armed by the reducing CTA
+  unsigned long long* trace;  // dev-only (SA_QKV_TRACE): [layer][grid][8] globaltimer stamps
+  int dev;        // dev knobs (SA_QKV_DEV): 1 no L2 prefetch, 2 skip MMA, 4 four stages
   __nv_bfloat16* q;
   __nv_bfloat16* k_new;
   __nv_bfloat16* v_new;
 };
 
-// One CTA per padded token row: 1/rms and the hi/lo planes of x * gain in the TMA tile layout.
+// Byte offset of 16-byte chunk c (0..7) of row r in a [rows][64] bf16 tile in SWIZZLE_128B order.
+__device__ __forceinline__ uint32_t sw128(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+// One-time repack: w [L][n_out][D] (row = output feature) -> [L][head][kb] swizzled 16 KB tiles.
+__global__ void __launch_bounds__(256) qkv_pack(const __nv_bfloat16* w, int n_out, int D, __nv_bfloat16* wpack) {
+  const int tile = blockIdx.x;  // (l * heads + h) * nkb + kb
+  const int nkb = D / 64, heads = n_out / 128;
+  const int kb = tile % nkb, lh = tile / nkb, h = lh % heads, l = lh / heads;
+  const __nv_bfloat16* src = w + (static_cast<size_t>(l) * n_out + h * 128) * D + kb * 64;
+  uint8_t* dst = reinterpret_cast<uint8_t*>(wpack) + static_cast<size_t>(tile) * 16384;
+  for (int i = threadIdx.x; i < 128 * 8; i += 256) {
+    const int r = i >> 3, c = i & 7;
+    *reinterpret_cast<uint4*>(dst + sw128(r, c)) = *reinterpret_cast<const uint4*>(src + static_cast<size_t>(r) * D + c * 8);
+  }
+}
+
+// One CTA per padded token row: 1/rms and the hi/lo planes of x * gain, swizzled like the B tile.
 __global__ void __launch_bounds__(256) qkv_prepare(QkvParams p) {
+  // let the projection launch now: it streams its first weight tiles while this kernel waits and runs
+  pdl_launch_dependents();
   pdl_wait();  // x is the previous kernel's output; the previous projection's xbuf reads are done
   const int t = blockIdx.x, tid = threadIdx.x;
   const int D = p.nkb * 64;
@@ -70,17 +112,24 @@ __global__ void __launch_bounds__(256) qkv_prepare(QkvParams p) {
   const float* g = p.gain + static_cast<size_t>(p.layer) * D;
   const bool live = t < p.n_tok;
   double ss = 0.0;
-  for (int k = tid * 2; k < D; k += 512) {
-    uint32_t hi2 = 0, lo2 = 0;
+#pragma unroll 4
+  for (int k = tid * 8; k < D; k += 2048) {  // 8 consecutive elements = one 16-byte bf16 chunk
+    uint4 hi = make_uint4(0, 0, 0, 0), lo = hi;
     if (live) {
-      const float2 xv = *reinterpret_cast<const float2*>(xr + k);
-      const float2 gv = *reinterpret_cast<const float2*>(g + k);
-      ss += static_cast<double>(xv.x) * xv.x + static_cast<double>(xv.y) * xv.y;
-      split_bf16(xv.x * gv.x, xv.y * gv.y, hi2, lo2);
+      const float4 x0 = *reinterpret_cast<const float4*>(xr + k), x1 = *reinterpret_cast<const float4*>(xr + k + 4);
+      const float4 g0 = *reinterpret_cast<const float4*>(g + k), g1 = *reinterpret_cast<const float4*>(g + k + 4);
+      ss += static_cast<double>(x0.x) * x0.x + static_cast<double>(x0.y) * x0.y + static_cast<double>(x0.z) * x0.z +
+            static_cast<double>(x0.w) * x0.w + static_cast<double>(x1.x) * x1.x + static_cast<double>(x1.y) * x1.y +
+            static_cast<double>(x1.z) * x1.z + static_cast<double>(x1.w) * x1.w;
+      split_bf16(x0.x * g0.x, x0.y * g0.y, hi.x, lo.x);
+      split_bf16(x0.z * g0.z, x0.w * g0.w, hi.y, lo.y);
+      split_bf16(x1.x * g1.x, x1.y * g1.y, hi.z, lo.z);
+      split_bf16(x1.z * g1.z, x1.w * g1.w, hi.w, lo.w);
     }
-    __nv_bfloat16* dst = p.xbuf + (static_cast<size_t>(k >> 6) * p.N + t) * 64 + (k & 63);
-    *reinterpret_cast<uint32_t*>(dst) = hi2;
-    *reinterpret_cast<uint32_t*>(dst + static_cast<size_t>(p.NT) * 64) = lo2;
+    uint8_t* blk = reinterpret_cast<uint8_t*>(p.xbuf) + static_cast<size_t>(k >> 6) * p.N * 128;
+    const int c = (k & 63) >> 3;
+    *reinterpret_cast<uint4*>(blk + sw128(t, c)) = hi;
+    *reinterpret_cast<uint4*>(blk + sw128(p.NT + t, c)) = lo;
   }
   __shared__ double red[8];
 #pragma unroll
@@ -92,66 +141,101 @@ __global__ void __launch_bounds__(256) qkv_prepare(QkvParams p) {
     for (int w = 0; w < 8; ++w) s += red[w];
     p.rbuf[t] = live ? static_cast<float>(1.0 / sqrt(s / D + static_cast<double>(p.eps))) : 0.f;
   }
-  __syncthreads();
-  pdl_launch_dependents();
+  if (live && tid < 64) {  // RoPE pair j of this token: angle = pos * theta^(-2j/128), reduced in double
+    const int b = t / p.rows, r = t - b * p.rows;
+    double turns = static_cast<double>(p.pos0[b] + r) * exp2(-p.log2_theta * (2.0 * tid) / 128.0) *
+                   0.15915494309189535;
+    turns -= floor(turns);
+    double sd, cd;
+    sincospi(2.0 * turns, &sd, &cd);  // reduced argument: polynomial only, no large-angle path
+    p.rope[t * 64 + tid] = make_float2(static_cast<float>(cd), static_cast<float>(sd));
+  }
 }
 
-__global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(const __grid_constant__ CUtensorMap tmw,
-                                                            const __grid_constant__ CUtensorMap tmx, QkvParams p) {
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(src)), "r"(bytes)
+               : "memory");
+}
+
+#define QKV_STAMP(k)                                                                     \
+  do {                                                                                   \
+    if (p.trace) {                                                                       \
+      unsigned long long gt_;                                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                            \
+      p.trace[(static_cast<size_t>(p.layer) * gridDim.x + blockIdx.x) * 16 + (k)] = gt_; \
+    }                                                                                    \
+  } while (0)
+
+// First / one-past-last unit ((head, k-block) pair, head-major) of CTA c among n for U units.
+__device__ __forceinline__ int unit_begin(int c, int U, int n) { return static_cast<int>(static_cast<int64_t>(c) * U / n); }
+
+__global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int split = blockIdx.x, head = blockIdx.y;
-  const int N = p.N, NT = p.NT;
-  const uint32_t stage_bytes = kWTile + N * 128;
-  const int ring = kQkvSmem - 1024 - 256;
-  const int S = min(8, static_cast<int>(ring / stage_bytes));
+  const int N = p.N, NT = p.NT, nkb = p.nkb, n = gridDim.x, cta = blockIdx.x;
+  const int U = p.heads * nkb;
+  const int u0 = unit_begin(cta, U, n), u1 = unit_begin(cta + 1, U, n), nk = u1 - u0;
+  const int head0 = u0 / nkb, nseg = (u1 - 1) / nkb - head0 + 1;  // heads touched (1 or 2)
+  const uint32_t xbytes = N * 128;
+  const uint32_t stage_bytes = kWTile + xbytes;  // weight tile + token tile (hi/lo planes)
+  const uint32_t tx_bytes = (p.dev & 8) ? kWTile : stage_bytes;  // dev 8: X tiles not loaded
+  const int ring = kQkvSmem - 1024 - 512;
+  const int S = min((p.dev & 4) ? 4 : kMaxStages, static_cast<int>((ring - kEpiBytes) / stage_bytes));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ring);
-  uint64_t* empty = full + 8;
-  uint64_t* acc_bar = empty + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 1);
-  float* part = reinterpret_cast<float*>(smem);                   // [N][128] (after the mainloop)
-  float* fin = part + static_cast<size_t>(N) * 128;               // [slice][128]
-  const int kb0 = split * p.nkb / p.splits, kb1 = (split + 1) * p.nkb / p.splits, nk = kb1 - kb0;
-  const uint32_t tcols = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* acc_bar = empty + kMaxStages;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  // independent accumulators per head segment: consecutive MMAs of one accumulator serialise on their
+  // full latency when N is small (~0.1 us per K=16 step at N=16), so the K-steps rotate over NACC
+  const int nacc = N <= 64 ? 4 : N <= 128 ? 2 : 1;
+  const int acols = 2 * nacc * N;
+  const uint32_t tcols = acols <= 32 ? 32 : acols <= 64 ? 64 : acols <= 128 ? 128 : acols <= 256 ? 256 : 512;
 
   if (tid == 0) {
+    QKV_STAMP(0);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(acc_bar, 1);
+    mbar_init(&acc_bar[0], 1);
+    mbar_init(&acc_bar[1], 1);
     fence_mbar_init();
-    tma_prefetch_desc(&tmw);
-    tma_prefetch_desc(&tmx);
   }
   if (warp == 1) tmem_alloc(tmem_slot, tcols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // dependents (the next layer's prepare, or attention) do all their reads after griddepcontrol.wait
+  pdl_launch_dependents();
 
   if (warp == 0) {
-    if (lane == 0) {  // ------------------------------------------------ TMA producer
-      const uint64_t pol = policy_evict_first(), pol_x = policy_evict_last();
-      const int wrow = p.layer * p.n_out + head * 128;
+    if (lane == 0) {  // ------------------------------------------------ bulk-copy producer
+      // this CTA's units are one contiguous run of the packed weights
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) +
+                            (static_cast<size_t>(p.layer) * U + u0) * kWTile;
+      auto xsrc = [&](int it) {
+        return reinterpret_cast<const uint8_t*>(p.xbuf) + static_cast<size_t>((u0 + it) % nkb) * N * 128;
+      };
       const int pre = min(S, nk);
       for (int it = 0; it < pre; ++it) {  // weights do not depend on the previous kernel
-        mbar_expect_tx(&full[it], stage_bytes);
-        tma_load_2d(smem + it * stage_bytes, &tmw, &full[it], (kb0 + it) * 64, wrow, pol);
+        mbar_expect_tx(&full[it], tx_bytes);
+        bulk_load(smem + it * stage_bytes, wsrc + static_cast<size_t>(it) * kWTile, kWTile, &full[it]);
       }
+      if (nk > pre && !(p.dev & 1)) bulk_prefetch_l2(wsrc + static_cast<size_t>(pre) * kWTile, (nk - pre) * kWTile);
       pdl_wait();
-      auto load_x = [&](int it, int st) {
-        uint8_t* dst = smem + st * stage_bytes + kWTile;
-        for (int r = 0; r < N; r += 16) tma_load_2d(dst + r * 128, &tmx, &full[st], 0, (kb0 + it) * N + r, pol_x);
-      };
-      for (int it = 0; it < pre; ++it) load_x(it, it);
+      QKV_STAMP(1);
+      QKV_STAMP(11);
+      if (!(p.dev & 8))
+        for (int it = 0; it < pre; ++it) bulk_load(smem + it * stage_bytes + kWTile, xsrc(it), xbytes, &full[it]);
       for (int it = pre; it < nk; ++it) {
         const int st = it % S;
         mbar_wait(&empty[st], ((it / S) - 1) & 1);
-        mbar_expect_tx(&full[st], stage_bytes);
-        tma_load_2d(smem + st * stage_bytes, &tmw, &full[st], (kb0 + it) * 64, wrow, pol);
-        load_x(it, st);
+        mbar_expect_tx(&full[st], tx_bytes);
+        bulk_load(smem + st * stage_bytes, wsrc + static_cast<size_t>(it) * kWTile, kWTile, &full[st]);
+        if (!(p.dev & 8)) bulk_load(smem + st * stage_bytes + kWTile, xsrc(it), xbytes, &full[st]);
       }
     }
     __syncwarp();
@@ -159,50 +243,30 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(const __grid_constant
     if (lane == 0) {  // ------------------------------------------------ MMA issuer
       const uint32_t idesc = umma_idesc_bf16(N, 0, 0);
       for (int it = 0; it < nk; ++it) {
-        const int st = it % S;
+        const int st = it % S, u = u0 + it, seg = u / nkb - head0;
+        const bool first = it == 0 || u % nkb == 0;
         mbar_wait(&full[st], (it / S) & 1);
+        if (it == 0) QKV_STAMP(2);
+        if (it == S - 1) QKV_STAMP(8);
+        if (it == S) QKV_STAMP(9);
+        if (it == (S + nk) / 2) QKV_STAMP(10);
         tc_fence_after();
         const uint32_t a_base = smem_u32(smem + st * stage_bytes), b_base = a_base + kWTile;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          umma_bf16(tmem, umma_desc(a_base + kk * 32, 16, 1024, kLayoutSW128),
-                    umma_desc(b_base + kk * 32, 16, 1024, kLayoutSW128), idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          if (!(p.dev & 2))
+            umma_bf16(tmem + (seg * nacc + (kk & (nacc - 1))) * N, umma_desc(a_base + kk * 32, 16, 1024, kLayoutSW128),
+                      umma_desc(b_base + kk * 32, 16, 1024, kLayoutSW128), idesc, (!first || kk >= nacc) ? 1u : 0u);
         umma_commit(&empty[st]);
+        if (u + 1 == u1 || (u + 1) % nkb == 0) umma_commit(&acc_bar[seg]);
       }
-      umma_commit(acc_bar);
+      QKV_STAMP(3);
     }
     __syncwarp();
-  } else {  // ------------------------------------------------------------ epilogue, warps 2-5
-    pdl_wait();  // 1/rms (rbuf) and the positions are read below
-    const int quarter = warp & 3, row = quarter * 32 + lane;
-    mbar_wait(acc_bar, 0);
-    tc_fence_after();
-    for (int c = 0; c < N; c += 16) {
-      float v[16];
-      tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c, v);
-      tc_wait_ld();
-#pragma unroll
-      for (int j = 0; j < 16; ++j) part[(c + j) * 128 + row] = v[j];
-    }
-  }
-  tc_fence_before();
-  cluster_sync_all();  // every split's partial tile is in its shared memory
-
-  const int t0 = split * p.n_tok / p.splits, t1 = (split + 1) * p.n_tok / p.splits;
-  if (warp >= 2) {
-    const int row = (warp & 3) * 32 + lane;
-    const uint32_t part_addr = smem_u32(part);
-    for (int t = t0; t < t1; ++t) {
-      float hi = 0.f, lo = 0.f;
-      for (int c = 0; c < p.splits; ++c) {  // fixed order over the splits: deterministic
-        const uint32_t base = mapa_shared(part_addr, c);
-        hi += ld_dsmem_f32(base + (t * 128 + row) * 4);
-        lo += ld_dsmem_f32(base + ((NT + t) * 128 + row) * 4);
-      }
-      fin[(t - t0) * 128 + row] = (hi + lo) * p.rbuf[t];
-    }
-    named_bar_sync(1, 128);
-    const int kind = head < p.Hq ? 0 : head < p.Hq + p.Hkv ? 1 : 2;  // q / k / v head
+  } else {  // ------------------------------------------------ epilogue, warps 2-5 (128 threads)
+    pdl_wait();  // 1/rms (rbuf), positions and the head counters are read below
+    const int quarter = warp & 3, row = quarter * 32 + lane, et = tid - 64;
+    const int kind_q = p.Hq, kind_k = p.Hq + p.Hkv;
     int pair, partner;
     if (p.style == 0) {  // half-split (rotate_half): (i, i+64)
       pair = row & 63;
@@ -211,28 +275,115 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(const __grid_constant
       pair = row >> 1;
       partner = row ^ 1;
     }
-    const bool first = p.style == 0 ? row < 64 : (row & 1) == 0;
-    const double inv_freq = exp2(-p.log2_theta * (2.0 * pair) / 128.0);
-    for (int t = t0; t < t1; ++t) {
-      const int b = t / p.rows, r = t - b * p.rows;
-      float y = fin[(t - t0) * 128 + row];
-      if (kind < 2) {
-        const double ang = static_cast<double>(p.pos0[b] + r) * inv_freq;
-        const float cs = static_cast<float>(cos(ang)), sn = static_cast<float>(sin(ang));
-        const float yp = fin[(t - t0) * 128 + partner];
-        y = first ? __fsub_rn(__fmul_rn(y, cs), __fmul_rn(yp, sn)) : __fadd_rn(__fmul_rn(y, cs), __fmul_rn(yp, sn));
+    const bool first_of_pair = p.style == 0 ? row < 64 : (row & 1) == 0;
+    float* ys = reinterpret_cast<float*>(smem + ring - kEpiBytes);  // [8][128] token group
+    for (int seg = 0; seg < nseg; ++seg) {
+      const int head = head0 + seg;
+      mbar_wait(&acc_bar[seg], 0);
+      if (seg == 0 && et == 0) QKV_STAMP(4);
+      tc_fence_after();
+      float* mine = p.part + (static_cast<size_t>(cta) * 2 + seg) * N * 128;
+      const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + seg * nacc * N;
+      for (int c = 0; c < N; c += 16) {
+        float v[16], w[16];
+        tmem_ld16(lane_base + c, v);
+        for (int a = 1; a < nacc; ++a) {  // fixed order: deterministic
+          tmem_ld16(lane_base + a * N + c, w);
+          tc_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += w[j];
+        }
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mine[(c + j) * 128 + row] = v[j];
       }
-      const __nv_bfloat16 o = __float2bfloat16_rn(y);
-      if (kind == 0)
-        p.q[((static_cast<size_t>(b) * p.Hq + head) * p.rows + r) * 128 + row] = o;
-      else
-        (kind == 1 ? p.k_new : p.v_new)[((static_cast<size_t>(b) * p.rows + r) * p.Hkv + head - p.Hq -
-                                         (kind == 2 ? p.Hkv : 0)) * 128 + row] = o;
+      __threadfence();
+      named_bar_sync(1, 128);
+      if (et == 0) {
+        const int hu0 = head * nkb, hu1 = hu0 + nkb;
+        int c0 = static_cast<int>(static_cast<int64_t>(hu0) * n / U);
+        while (c0 > 0 && unit_begin(c0, U, n) > hu0) --c0;
+        while (unit_begin(c0 + 1, U, n) <= hu0) ++c0;
+        int c1 = c0;
+        while (c1 + 1 < n && unit_begin(c1 + 1, U, n) < hu1) ++c1;
+        const int contributors = c1 - c0 + 1;
+        const int prev = atomicAdd(p.counters + head, 1);
+        *last_flag = prev == contributors - 1 ? c0 : -1;
+        if (prev == contributors - 1) p.counters[head] = 0;  // re-armed for the next call
+      }
+      named_bar_sync(1, 128);
+      const int c0 = *last_flag;
+      named_bar_sync(1, 128);
+      if (et == 0) QKV_STAMP(5);
+      if (c0 < 0) continue;
+      __threadfence();
+      // last arrival: reduce every contributor's partial in CTA order (deterministic), then finish.
+      // 8 tokens x 4 contributors of loads are issued before any is used (one L2 round trip per
+      // group: under the next layer's weight stream an L2 round trip costs ~1 us).
+      const int hu1 = (head + 1) * nkb;
+      const int kind = head < kind_q ? 0 : head < kind_k ? 1 : 2;
+      int n_c = 0;
+      while (c0 + n_c < n && unit_begin(c0 + n_c, U, n) < hu1) ++n_c;
+      for (int g0 = 0; g0 < p.n_tok; g0 += 8) {
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int ci = 0; ci < n_c; ci += 4) {
+          float v[4][8][2];
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int c = c0 + ci + cc;
+            const bool ok = ci + cc < n_c;
+            const int cseg = ok && unit_begin(c, U, n) / nkb != head ? 1 : 0;
+            const float* src = p.part + (static_cast<size_t>(ok ? c : c0) * 2 + cseg) * N * 128 + row;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int t = g0 + j;
+              v[cc][j][0] = ok && t < p.n_tok ? __ldcg(src + t * 128) : 0.f;
+              v[cc][j][1] = ok && t < p.n_tok ? __ldcg(src + (NT + t) * 128) : 0.f;
+            }
+          }
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] += v[cc][j][0] + v[cc][j][1];
+        }
+        float rs[8];
+        float2 csn[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int t = min(g0 + j, p.n_tok - 1);
+            rs[j] = __ldcg(p.rbuf + t);
+            csn[j] = kind < 2 ? __ldcg(p.rope + t * 64 + pair) : make_float2(1.f, 0.f);
+          }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) ys[j * 128 + row] = acc[j] * rs[j];
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int t = g0 + j;
+          if (t >= p.n_tok) break;
+          const int b = t / p.rows, r = t - b * p.rows;
+          float y = ys[j * 128 + row];
+          if (kind < 2) {
+            const float yp = ys[j * 128 + partner];
+            y = first_of_pair ? __fsub_rn(__fmul_rn(y, csn[j].x), __fmul_rn(yp, csn[j].y))
+                              : __fadd_rn(__fmul_rn(y, csn[j].x), __fmul_rn(yp, csn[j].y));
+          }
+          const __nv_bfloat16 o = __float2bfloat16_rn(y);
+          if (kind == 0)
+            p.q[((static_cast<size_t>(b) * p.Hq + head) * p.rows + r) * 128 + row] = o;
+          else
+            (kind == 1 ? p.k_new : p.v_new)[((static_cast<size_t>(b) * p.rows + r) * p.Hkv + head - kind_q -
+                                             (kind == 2 ? p.Hkv : 0)) * 128 + row] = o;
+        }
+        named_bar_sync(1, 128);
+      }
+      if (et == 0) QKV_STAMP(6);
     }
   }
   __syncthreads();
-  pdl_launch_dependents();
-  cluster_sync_all();  // peers have finished reading this CTA's partial tile
+  if (tid == 0) QKV_STAMP(7);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, tcols);
@@ -263,23 +414,36 @@ SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, i
   h->style = rope_style;
   h->eps = static_cast<float>(norm_eps);
   h->theta = rope_theta;
-  h->w = static_cast<const __nv_bfloat16*>(w_qkv);
-  h->gain = attn_norm_gain;
   cudaGetDevice(&h->device);
   cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
-  cudaError_t e = cudaMalloc(&h->xbuf, static_cast<size_t>(h->nkb) * 2 * sa::kQkvMaxTokens * 64 * 2);
+  const size_t tiles = static_cast<size_t>(n_layers) * (n_q_heads + 2 * n_kv_heads) * h->nkb;
+  cudaError_t e = cudaMalloc(&h->wpack, tiles * sa::kWTile);
+  if (e == cudaSuccess) e = cudaMalloc(&h->gain, static_cast<size_t>(n_layers) * d_model * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&h->xbuf, static_cast<size_t>(h->nkb) * 2 * sa::kQkvMaxTokens * 64 * 2);
   if (e == cudaSuccess) e = cudaMalloc(&h->rbuf, sa::kQkvMaxTokens * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&h->rope, sa::kQkvMaxTokens * 64 * sizeof(float2));
+  const int heads = n_q_heads + 2 * n_kv_heads;
+  h->max_grid = std::max(heads, std::min(h->num_sms, heads * h->nkb));
+  if (e == cudaSuccess)
+    e = cudaMalloc(&h->part, static_cast<size_t>(h->max_grid) * 2 * 2 * sa::kQkvMaxTokens * 128 * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&h->counters, heads * sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(h->counters, 0, heads * sizeof(int));
+  if (e == cudaSuccess && std::getenv("SA_QKV_TRACE")) {
+    e = cudaMalloc(&h->trace, static_cast<size_t>(n_layers) * h->max_grid * 16 * 8);
+    if (e == cudaSuccess) e = cudaMemset(h->trace, 0, static_cast<size_t>(n_layers) * h->max_grid * 16 * 8);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpy(h->gain, attn_norm_gain, static_cast<size_t>(n_layers) * d_model * sizeof(float),
+                   cudaMemcpyDefault);
+  if (e == cudaSuccess) {
+    sa::qkv_pack<<<static_cast<unsigned>(tiles), 256>>>(static_cast<const __nv_bfloat16*>(w_qkv), h->n_out, d_model,
+                                                         h->wpack);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     sa_qkv_destroy(h);
-    return sa::cuda_fail(e, "qkv buffers");
-  }
-  std::string err;
-  if (!sa::encode_tensor_map_2d(&h->tmap_w, const_cast<__nv_bfloat16*>(h->w), static_cast<uint64_t>(d_model),
-                                static_cast<uint64_t>(n_layers) * h->n_out, 128, &err) ||
-      !sa::encode_tensor_map_2d(&h->tmap_x, h->xbuf, 64, static_cast<uint64_t>(h->nkb) * 2 * sa::kQkvMaxTokens, 16,
-                                &err)) {
-    sa_qkv_destroy(h);
-    return sa::fail(SA_CUDA_ERROR, err);
+    return sa::cuda_fail(e, "qkv create");
   }
   *out = h;
   return SA_OK;
@@ -287,8 +451,23 @@ SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, i
 
 SA_API sa_status sa_qkv_destroy(sa_qkv* h) {
   if (!h) return SA_OK;
+  if (h->trace) {  // dev-only: dump the stamps of the last call per layer
+    std::vector<unsigned long long> t(static_cast<size_t>(h->L) * h->max_grid * 16);
+    if (cudaMemcpy(t.data(), h->trace, t.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+      if (FILE* f = std::fopen("/tmp/sa_qkv_trace.bin", "wb")) {
+        std::fwrite(t.data(), 8, t.size(), f);
+        std::fclose(f);
+      }
+    }
+    cudaFree(h->trace);
+  }
+  cudaFree(h->wpack);
+  cudaFree(h->gain);
   cudaFree(h->xbuf);
   cudaFree(h->rbuf);
+  cudaFree(h->rope);
+  cudaFree(h->part);
+  cudaFree(h->counters);
   delete h;
   return SA_OK;
 }
@@ -310,29 +489,31 @@ SA_API sa_status sa_qkv_project(sa_qkv* h, int32_t layer, const float* x, const 
   p.Hq = h->Hq;
   p.Hkv = h->Hkv;
   const int heads = h->Hq + 2 * h->Hkv;
-  p.splits = std::max(1, std::min({h->num_sms / heads, 8, h->nkb}));
+  p.heads = heads;
   p.style = h->style;
   p.eps = h->eps;
   p.log2_theta = std::log2(h->theta);
-  p.w = h->w;
+  p.wpack = h->wpack;
   p.x = x;
   p.gain = h->gain;
   p.pos0 = positions;
   p.xbuf = h->xbuf;
   p.rbuf = h->rbuf;
+  p.rope = h->rope;
+  p.part = h->part;
+  p.counters = h->counters;
+  p.trace = h->trace;
+  if (const char* e = std::getenv("SA_QKV_DEV")) p.dev = std::atoi(e);
   p.q = static_cast<__nv_bfloat16*>(q);
   p.k_new = static_cast<__nv_bfloat16*>(k_new);
   p.v_new = static_cast<__nv_bfloat16*>(v_new);
-  // the epilogue overlays [N][128] partials + the token slice on the (drained) stage ring
-  const int slice = (p.n_tok + p.splits - 1) / p.splits;
-  if ((p.N + slice) * 128 * 4 > sa::kQkvSmem - 1024 - 256) return sa::fail(SA_INVALID_ARGUMENT, "qkv: too many tokens");
   auto s = static_cast<cudaStream_t>(stream);
   static bool attr_set = false;
   if (!attr_set) {
     SA_CUDA_CHECK(cudaFuncSetAttribute(sa::qkv_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, sa::kQkvSmem));
     attr_set = true;
   }
-  cudaLaunchAttribute pdl[2];
+  cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t c1{};
@@ -342,18 +523,14 @@ SA_API sa_status sa_qkv_project(sa_qkv* h, int32_t layer, const float* x, const 
   c1.attrs = pdl;
   c1.numAttrs = 1;
   SA_CUDA_CHECK(cudaLaunchKernelEx(&c1, sa::qkv_prepare, p));
-  pdl[1].id = cudaLaunchAttributeClusterDimension;
-  pdl[1].val.clusterDim.x = p.splits;
-  pdl[1].val.clusterDim.y = 1;
-  pdl[1].val.clusterDim.z = 1;
   cudaLaunchConfig_t c2{};
-  c2.gridDim = dim3(p.splits, heads);
+  c2.gridDim = dim3(h->max_grid);  // stream-K: every SM takes an equal run of (head, k-block) units
   c2.blockDim = dim3(sa::kQkvThreads);
   c2.dynamicSmemBytes = sa::kQkvSmem;
   c2.stream = s;
   c2.attrs = pdl;
-  c2.numAttrs = 2;
-  SA_CUDA_CHECK(cudaLaunchKernelEx(&c2, sa::qkv_gemm, h->tmap_w, h->tmap_x, p));
+  c2.numAttrs = 1;
+  SA_CUDA_CHECK(cudaLaunchKernelEx(&c2, sa::qkv_gemm, p));
   return SA_OK;
 }
 
