@@ -358,7 +358,77 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_extras:
+        result["next_rows"] = next_rows(dev, B, gamma, hbm_peak)
     return result
+
+
+def next_rows(dev, B, gamma, hbm_peak):
+    """SURVEY.md §8f rows measured beside the headline (not part of `value`): the model-side producer
+    (RMSNorm + fused QKV projection + RoPE, Llama-3.1-8B shape, a 32-layer PDL chain in one graph) for
+    the verify rows and a draft row, and the speculation acceptance kernel at the Llama-3 vocabulary."""
+    import torch
+
+    from paper_2602_07223_b200 import QkvProjection, accept
+    L, Dm, Hq, Hkv = 32, 4096, 32, 8
+    n_out = (Hq + 2 * Hkv) * 128
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    w = (torch.randn((L, n_out, Dm), generator=g, device=dev) / 64).to(torch.bfloat16)
+    proj = QkvProjection(w, torch.ones((L, Dm), device=dev), Hq, Hkv)
+    del w
+    out = {}
+    s = torch.cuda.Stream(device=dev)
+    for name, rows in (("verify_rows", gamma + 1), ("draft_row", 1)):
+        x = torch.randn((B, rows, Dm), generator=g, device=dev)
+        pos = torch.full((B,), 32768, dtype=torch.int32, device=dev)
+        q = torch.empty((B, Hq, rows, 128), dtype=torch.bfloat16, device=dev)
+        kn = torch.empty((B, rows, Hkv, 128), dtype=torch.bfloat16, device=dev)
+        vn = torch.empty_like(kn)
+        with torch.cuda.stream(s):
+            for l in range(L):
+                proj.project(l, x, pos, q, kn, vn, stream=s)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=s):
+                for l in range(L):
+                    proj.project(l, x, pos, q, kn, vn, stream=s)
+            for _ in range(3):
+                gr.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(10):
+                gr.replay()
+            e1.record(s)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (10 * L)
+        nbytes = n_out * Dm * 2 + B * rows * (Dm * 4 + n_out * 2)
+        gbs = nbytes / us / 1e3
+        out[name] = {"tokens": B * rows, "us_per_layer": round(us, 2), "bytes_per_layer": nbytes,
+                     "achieved_gbs": round(gbs, 1), "frac": round(gbs / hbm_peak, 4)}
+    proj.close()
+    res = {"producer": dict(out, kernel="qkv_prepare + qkv_gemm (tcgen05, stream-K)", shape="Llama-3.1-8B layer",
+                            chain="32 layers, one CUDA graph, PDL")}
+    V = 128256
+    p = torch.softmax(torch.randn((B, gamma + 1, V), generator=g, device=dev), -1)
+    qd = torch.softmax(torch.randn((B, gamma, V), generator=g, device=dev), -1)
+    draft = torch.randint(0, V, (B, gamma), generator=g, device=dev, dtype=torch.int32)
+    u = torch.rand((B, gamma + 1), generator=g, device=dev)
+    res_out = (torch.empty(B, dtype=torch.int32, device=dev), torch.empty((B, gamma + 1), dtype=torch.int32, device=dev))
+    with torch.cuda.stream(s):  # a graph of 20 calls: device time, not Python launch overhead
+        accept(p, draft, q=qd, u=u, stream=s, out=res_out)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=s):
+            for _ in range(20):
+                accept(p, draft, q=qd, u=u, stream=s, out=res_out)
+        gr.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        gr.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    res["accept"] = {"us_per_call": round(e0.elapsed_time(e1) * 1e3 / 20, 2), "vocab": V, "gamma": gamma, "batch": B,
+                     "mode": "modified rejection sampling"}
+    return res
 
 
 # --------------------------------------------------------------------------------------------- CPU
@@ -438,6 +508,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the §8f next-row measurements")
     ap.add_argument("--strategy", default="collect2", choices=sorted(STRATEGIES),
                     help="selection strategy of the iteration (the headline is collect2; the others are the "
                          "paper's variants / baselines for the overhead comparison)")

@@ -277,7 +277,7 @@ SA_API sa_status sa_exchange_layer_scores(sa_runner* r, int32_t layer_slot, void
  * NULL when greedy).  Sample: accept x_t iff u_t < min(1, p_t(x_t)/q_t(x_t)); on the first rejection
  * emit a sample of normalize(max(0, p_t - q_t)); if all accepted emit a bonus ~ p_{gamma+1}.  Greedy:
  * accept iff x_t = argmax p_t (ties to the lower id), trailing token argmax p_{a+1}.
- * Out (device): accepted [B], emitted [B][gamma+1] (accepted drafts then the trailing token). */
+ * Out (device): accepted [B], emitted [B][gamma+1] (accepted drafts, the trailing token, then -1). */
 SA_API sa_status sa_accept(const float* p, const float* q, const int32_t* draft, const float* u, int32_t B,
                            int32_t gamma, int32_t V, int32_t greedy, int32_t* accepted, int32_t* emitted, void* stream);
 /* Commit after acceptance (kv_store.cpp:51-65): the verify rows [p0, p0+accepted] (y and

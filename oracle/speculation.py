@@ -6,9 +6,11 @@ restates the SPEC contract speculation::verify (SPEC.md:391-405) and residual_di
  and is pinned on the SPEC's own known-answer examples (tests/test_oracle.py).
 
 The sampling arithmetic mirrors accept.cu exactly so GPU parity is bit-exact: ratios and
-max(0, p - q) in fp32, prefix sums in float64 over ceil(V/1024)-token chunks (sequential inside a
-chunk, then over chunk totals in order), target = u * total, smallest token whose inclusive
-prefix exceeds the target.
+max(0, p - q) in fp32, prefix sums in float64 in block_sample's fixed order (32 contiguous ranges,
+each summed by a warp in rounds of 32 - lane sums over rounds, butterfly to the range total - and
+totalled in order; the picked range split again into 32 sub-ranges the same way; the picked
+sub-range rescanned with an inclusive warp scan), target = u * total, smallest token whose
+inclusive prefix exceeds the target.
 
 Only tests/, __graft_entry__.smoke() and bench.py may import this module.
 """
@@ -16,7 +18,7 @@ from __future__ import annotations
 
 import numpy as np
 
-THREADS = 1024  # accept.cu kAccThreads: the chunking of the prefix sums
+WARPS = 32  # accept.cu: 1024 threads = 32 warps, each owning a contiguous range of the vocabulary
 
 
 def residual_distribution(p, q):
@@ -30,37 +32,81 @@ def residual_distribution(p, q):
     return r / s
 
 
+def _butterfly_sum(x):
+    """Sum of 32 lane values in the order of a __shfl_xor butterfly (offsets 16, 8, 4, 2, 1)."""
+    v = list(x)
+    for off in (16, 8, 4, 2, 1):
+        v = [v[l] + v[l ^ off] for l in range(32)]
+    return v[0]
+
+
+def _warp_scan(x):
+    """Inclusive Hillis-Steele scan of 32 lane values (shfl_up offsets 1, 2, 4, 8, 16)."""
+    v = list(x)
+    for off in (1, 2, 4, 8, 16):
+        v = [v[l] + v[l - off] if l >= off else v[l] for l in range(32)]
+    return v
+
+
+def _range_sum(w, lo, hi):
+    lanes = [0.0] * 32
+    for i in range(lo, hi):
+        lanes[(i - lo) % 32] += float(w[i])
+    return _butterfly_sum(lanes)
+
+
+def _pick(part, run, target):
+    run0 = run
+    for t, x in enumerate(part):
+        if run + x > target:
+            return t, run
+        run += x
+    c = 0
+    for t, x in enumerate(part):
+        if x > 0.0:
+            c = t
+    run = run0
+    for x in part[:c]:
+        run += x
+    return c, run
+
+
+def _ceil32(n):
+    return (n + 31) // 32 * 32
+
+
 def inverse_cdf(w, u):
     """accept.cu block_sample: w float64 weights >= 0, u in [0,1)."""
     w = np.asarray(w, dtype=np.float64)
     V = w.shape[0]
-    per = -(-V // THREADS)
-    chunks = [w[t * per:min(V, (t + 1) * per)] for t in range(THREADS) if t * per < V]
-    part = [float(np.cumsum(c)[-1]) if len(c) else 0.0 for c in chunks]
-    part += [0.0] * (THREADS - len(part))
+    per1 = _ceil32(-(-V // WARPS))
+    part = [_range_sum(w, min(V, k * per1), min(V, k * per1 + per1)) for k in range(WARPS)]
     total = 0.0
     for x in part:
         total += x
     target = u * total
-    run, c = 0.0, -1
-    for t, x in enumerate(part):
-        if run + x > target:
-            c = t
-            break
-        run += x
-    if c < 0:
-        c = max(t for t, x in enumerate(part) if x > 0.0)
-        run = 0.0
-        for x in part[:c]:
-            run += x
-    r = -1
-    for i in range(c * per, min(V, (c + 1) * per)):
-        run += w[i]
-        if w[i] > 0.0:
-            r = i
-        if run > target:
-            return i
-    return r
+    c1, base = _pick(part, 0.0, target)
+    lo1, hi1 = c1 * per1, min(V, c1 * per1 + per1)
+    per2 = _ceil32(-(-per1 // WARPS))
+    part2 = []
+    for k in range(WARPS):
+        lo = min(hi1, lo1 + k * per2)
+        part2.append(_range_sum(w, lo, min(hi1, lo + per2)))
+    c2, base = _pick(part2, base, target)
+    lo = min(hi1, lo1 + c2 * per2)
+    hi = min(hi1, lo + per2)
+    last_mass = -1
+    for i0 in range(lo, hi, 32):
+        e = [float(w[i]) if i < hi else 0.0 for i in range(i0, i0 + 32)]
+        v = _warp_scan(e)
+        for l in range(32):
+            if e[l] > 0.0:
+                last_mass = i0 + l
+        for l in range(32):
+            if base + v[l] > target:
+                return i0 + l
+        base += v[31]
+    return last_mass
 
 
 def argmax_lower(row):

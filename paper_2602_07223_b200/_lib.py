@@ -437,13 +437,17 @@ class QkvProjection:
         return q, k_new, v_new
 
 
-def accept(p, draft, q=None, u=None, greedy=False, stream=None):
+def accept(p, draft, q=None, u=None, greedy=False, stream=None, out=None):
     """Verification acceptance on the device: p [B][g+1][V], q [B][g][V] f32,
-    draft [B][g] int32, u [B][g+1] f32 -> (accepted [B], emitted [B][g+1]) int32 device tensors."""
+    draft [B][g] int32, u [B][g+1] f32 -> (accepted [B], emitted [B][g+1]) int32 device tensors
+    (emitted: accepted drafts, the trailing token, then -1).  out: optional preallocated pair."""
     import torch
     B, g1, V = p.shape
-    acc = torch.empty((B,), dtype=torch.int32, device=p.device)
-    em = torch.full((B, g1), -1, dtype=torch.int32, device=p.device)
+    if out is not None:
+        acc, em = out
+    else:
+        acc = torch.empty((B,), dtype=torch.int32, device=p.device)
+        em = torch.empty((B, g1), dtype=torch.int32, device=p.device)
     _check(lib().sa_accept(_ptr(p), _ptr(q), _ptr(draft), _ptr(u), B, g1 - 1, V, int(greedy), _ptr(acc), _ptr(em),
                            _stream(stream)))
     return acc, em

@@ -10,7 +10,7 @@
 //
 // One CTA (1024 threads) per sequence; distributions are fp32 rows of V entries.  Samples use inverse
 // CDF sampling with one uniform per sequence (u[gamma]): the smallest token i whose inclusive
-// prefix sum (double, fixed order: 1024 contiguous chunks, then a scan over chunks) exceeds u * total.
+// prefix sum (double, the fixed order of block_sample) exceeds u * total.
 #include "internal.h"
 
 namespace sa {
@@ -18,7 +18,7 @@ namespace sa {
 constexpr int kAccThreads = 1024;
 
 struct AccShared {
-  double part[kAccThreads];
+  double part[32];
   double base, target;
   float fmax[32];
   int imax[32];
@@ -67,55 +67,98 @@ __device__ int block_argmax(const float* row, int V, AccShared& sh) {
   return r;
 }
 
+// Sum of w over [lo, hi) by one warp in a fixed order: coalesced rounds of 32, lane sums over rounds,
+// then a __shfl_xor butterfly (every lane ends with the same value).
+template <typename W>
+__device__ __forceinline__ double warp_range_sum(int lo, int hi, int lane, W& w) {
+  double s = 0.0;
+#pragma unroll 8
+  for (int i = lo + lane; i < hi; i += 32) s += w(i);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
+// Thread 0: first of 32 sums whose running total (from `run`) exceeds target; the last range with
+// mass if rounding left none.  Returns the index; *base = running total before it.
+__device__ __forceinline__ int pick_range(const double* part, double run, double target, double* base) {
+  const double run0 = run;
+  for (int t = 0; t < 32; ++t) {
+    if (run + part[t] > target) {
+      *base = run;
+      return t;
+    }
+    run += part[t];
+  }
+  int c = 0;
+  for (int t = 0; t < 32; ++t)
+    if (part[t] > 0.0) c = t;
+  run = run0;
+  for (int t = 0; t < c; ++t) run += part[t];
+  *base = run;
+  return c;
+}
+
 // Inverse-CDF sample of weights w(i) >= 0 (unnormalised): the smallest i whose inclusive prefix sum
-// exceeds u * total.  Prefix sums in double in a fixed order: contiguous chunks of ceil(V/1024)
-// tokens per thread, then the chunk totals in thread order (oracle/speculation.py restates it).
+// exceeds u * total, in double with a fixed summation order (oracle/speculation.py restates it).
+// Level 1: warp w sums the contiguous range [w*per1, (w+1)*per1) (per1 = ceil(V/32) rounded up to
+// 32); thread 0 totals them in warp order and picks the range the target falls in.  Level 2: the
+// 32 warps split that range into sub-ranges of per2 = ceil(per1/32) rounded up to 32, same sums and
+// pick.  Level 3: one warp rescans the picked sub-range in rounds of 32 with an inclusive
+// (Hillis-Steele) warp scan on top of the running base.
 template <typename W>
 __device__ int block_sample(int V, double u, W w, AccShared& sh) {
-  const int tid = threadIdx.x;
-  const int per = (V + kAccThreads - 1) / kAccThreads;
-  const int lo = tid * per, hi = min(V, lo + per);
-  double loc = 0.0;
-  for (int i = lo; i < hi; ++i) loc += w(i);
-  sh.part[tid] = loc;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per1 = ((V + 31) / 32 + 31) / 32 * 32;
+  {
+    const int lo = warp * per1, hi = min(V, lo + per1);
+    const double s = warp_range_sum(lo, hi, lane, w);
+    if (lane == 0) sh.part[warp] = s;
+  }
   __syncthreads();
   if (tid == 0) {
     double total = 0.0;
-    for (int t = 0; t < kAccThreads; ++t) total += sh.part[t];
-    const double target = u * total;
-    double run = 0.0;
-    int c = -1;
-    for (int t = 0; t < kAccThreads; ++t) {
-      if (run + sh.part[t] > target) {
-        c = t;
-        break;
-      }
-      run += sh.part[t];
-    }
-    if (c < 0) {  // u * total rounded up to the total: the last chunk with mass
-      run = 0.0;
-      for (int t = 0; t < kAccThreads; ++t)
-        if (sh.part[t] > 0.0) c = t;
-      for (int t = 0; t < c; ++t) run += sh.part[t];
-    }
-    sh.base = run;
-    sh.target = target;
-    sh.pick = c;
+    for (int t = 0; t < 32; ++t) total += sh.part[t];
+    sh.target = u * total;
+    sh.pick = pick_range(sh.part, 0.0, sh.target, &sh.base);
   }
   __syncthreads();
-  if (tid == sh.pick) {
-    double run = sh.base;
-    int r = -1;
-    for (int i = lo; i < hi; ++i) {
-      const double wi = w(i);
-      run += wi;
-      if (wi > 0.0) r = i;  // fallback: the last token with mass
-      if (run > sh.target) {
-        r = i;
+  const int lo1 = sh.pick * per1, hi1 = min(V, lo1 + per1);
+  const int per2 = ((per1 + 31) / 32 + 31) / 32 * 32;
+  const double base1 = sh.base;
+  __syncthreads();
+  {
+    const int lo = min(hi1, lo1 + warp * per2), hi = min(hi1, lo + per2);
+    const double s = warp_range_sum(lo, hi, lane, w);
+    if (lane == 0) sh.part[warp] = s;
+  }
+  __syncthreads();
+  if (tid == 0) sh.pick = pick_range(sh.part, base1, sh.target, &sh.base);
+  __syncthreads();
+  if (warp == 0) {
+    const int lo = min(hi1, lo1 + sh.pick * per2), hi = min(hi1, lo + per2);
+    double base = sh.base;
+    const double target = sh.target;
+    int r = -1, last_mass = -1;
+    for (int i0 = lo; i0 < hi; i0 += 32) {
+      const int i = i0 + lane;
+      const double e = i < hi ? w(i) : 0.0;
+      double v = e;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double o = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += o;
+      }
+      const unsigned cross = __ballot_sync(0xffffffffu, base + v > target);
+      const unsigned mass = __ballot_sync(0xffffffffu, e > 0.0);
+      if (mass) last_mass = i0 + 31 - __clz(mass);
+      if (cross) {
+        r = i0 + __ffs(cross) - 1;
         break;
       }
+      base += __shfl_sync(0xffffffffu, v, 31);
     }
-    sh.res = r;
+    if (lane == 0) sh.res = r >= 0 ? r : last_mass;  // fallback: the last token with mass
   }
   __syncthreads();
   const int r = sh.res;
@@ -163,6 +206,7 @@ __global__ void __launch_bounds__(kAccThreads) accept_kernel(const float* p, con
   }
   if (threadIdx.x == 0) {
     eb[a] = trailing;
+    for (int j = a + 1; j <= gamma; ++j) eb[j] = -1;
     accepted[b] = a;
   }
 }
