@@ -479,8 +479,9 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
 }
 
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_mask{0};
+  int dev = 0;
+  if (func_attrs_needed(attr_mask, &dev)) {
     cudaError_t e = cudaFuncSetAttribute(draft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg::kSmem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(draft_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -489,7 +490,7 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(draft_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    func_attrs_done(attr_mask, dev);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,18 @@ sa_status cuda_fail(cudaError_t e, const char* where);
     cudaError_t _e = (expr);                                        \
     if (_e != cudaSuccess) return ::sa::cuda_fail(_e, #expr);       \
   } while (0)
+
+// Kernel function attributes (max dynamic smem, non-portable clusters) are per device: `mask` holds one
+// bit per device ordinal on which they were set.  Setting them twice is harmless, so races are benign.
+inline bool func_attrs_needed(std::atomic<uint64_t>& mask, int* dev_out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  *dev_out = dev;
+  return dev >= 64 || !(mask.load(std::memory_order_relaxed) & (uint64_t{1} << dev));
+}
+inline void func_attrs_done(std::atomic<uint64_t>& mask, int dev) {
+  if (dev < 64) mask.fetch_or(uint64_t{1} << dev, std::memory_order_relaxed);
+}
 
 bool encode_tensor_map(CUtensorMap* map, void* base, uint64_t rows, uint32_t box_rows, std::string* err);
 // bf16 [rows][cols] row-major, box {64, box_rows}, SWIZZLE_128B

@@ -508,10 +508,11 @@ SA_API sa_status sa_qkv_project(sa_qkv* h, int32_t layer, const float* x, const 
   p.k_new = static_cast<__nv_bfloat16*>(k_new);
   p.v_new = static_cast<__nv_bfloat16*>(v_new);
   auto s = static_cast<cudaStream_t>(stream);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_mask{0};
+  int dev = 0;
+  if (sa::func_attrs_needed(attr_mask, &dev)) {
     SA_CUDA_CHECK(cudaFuncSetAttribute(sa::qkv_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, sa::kQkvSmem));
-    attr_set = true;
+    sa::func_attrs_done(attr_mask, dev);
   }
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -232,11 +232,12 @@ cudaError_t launch_quest_select(const CacheView& c, const __nv_bfloat16* qmin, c
   int npow = 1;
   while (npow < max_qpages) npow <<= 1;
   const size_t smem = static_cast<size_t>(npow) * 12 + static_cast<size_t>(max_qpages) * 4 + 16;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr_mask{0};
+  int dev = 0;
+  if (func_attrs_needed(attr_mask, &dev)) {
     e = cudaFuncSetAttribute(quest_pick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
+    func_attrs_done(attr_mask, dev);
   }
   quest_pick_kernel<<<B, 1024, smem, s>>>(p0, qpage, bounds, max_qpages, ratio, k_min, k_cap, idx, k_out);
   return cudaGetLastError();

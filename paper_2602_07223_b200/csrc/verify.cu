@@ -282,11 +282,12 @@ template <int MT, int TG>
 static cudaError_t launch_mt(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s) {
   using Cfg = VCfg<MT, TG>;
   auto kern = verify_kernel<MT, TG>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_mask{0};
+  int dev = 0;
+  if (func_attrs_needed(attr_mask, &dev)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    func_attrs_done(attr_mask, dev);
   }
   dim3 grid(p.n_splits, p.Hkv, p.B);
   kern<<<grid, Cfg::kThreads, Cfg::kSmem, s>>>(tk, tv, p);

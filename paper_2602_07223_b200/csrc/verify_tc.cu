@@ -877,11 +877,12 @@ __global__ void __launch_bounds__(384, 1)
 template <int N>
 static cudaError_t launch_n(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s) {
   auto kern = verify_tc_kernel<N>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_mask{0};
+  int dev = 0;
+  if (func_attrs_needed(attr_mask, &dev)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TCfg<N>::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    func_attrs_done(attr_mask, dev);
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);
