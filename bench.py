@@ -428,6 +428,24 @@ def next_rows(dev, B, gamma, hbm_peak):
     torch.cuda.synchronize()
     res["accept"] = {"us_per_call": round(e0.elapsed_time(e1) * 1e3 / 20, 2), "vocab": V, "gamma": gamma, "batch": B,
                      "mode": "modified rejection sampling"}
+    # the CPU restatements timed beside them (host cores of this box; the reference ships no code here)
+    import numpy as np
+
+    from oracle.model import qkv_project
+    from oracle.speculation import accept as ref_accept
+    rng = np.random.default_rng(3)
+    wn = rng.standard_normal((n_out, Dm)).astype(np.float32)
+    xn = rng.standard_normal((B, gamma + 1, Dm)).astype(np.float32)
+    t0 = time.perf_counter()
+    qkv_project(xn, wn, np.ones(Dm, np.float32), Hq, Hkv, [32768] * B)
+    res["producer"]["cpu_port"] = {"us_per_layer": round((time.perf_counter() - t0) * 1e6, 1),
+                                   "kind": "port (oracle/model.py, numpy float64)", "tokens": B * (gamma + 1),
+                                   "cores": os.cpu_count()}
+    pn, qn = p[0].cpu().numpy(), qd[0].cpu().numpy()
+    t0 = time.perf_counter()
+    ref_accept(pn, draft[0].cpu().numpy(), q=qn, u=u[0].cpu().numpy())
+    res["accept"]["cpu_port"] = {"us_per_call": round((time.perf_counter() - t0) * 1e6, 1),
+                                 "kind": "port (oracle/speculation.py, scalar Python)", "batch": 1, "cores": 1}
     return res
 
 

@@ -79,7 +79,11 @@ struct QkvParams {
   float* part;    // [grid][2][N][128] per-CTA partial accumulators (one per head touched)
   int* counters;  // [heads] arrivals, re-armed by the reducing CTA
   unsigned long long* trace;  // dev-only (SA_QKV_TRACE): [layer][grid][8] globaltimer stamps
-  int dev;        // dev knobs (SA_QKV_DEV): 1 no L2 prefetch, 2 skip MMA, 4 four stages
+  // dev knobs (SA_QKV_DEV, timing experiments only; results are wrong with 2/8/64/1024): 1 no L2
+  // prefetch, 2 skip the MMAs, 4 four stages, 8 no token tiles, 64 MMA without waits, 128 no per-stage
+  // commits, 256 plain arrive instead of tcgen05.commit, 512 test_wait spin, 1024 token tiles from a
+  // stale buffer
+  int dev;
   __nv_bfloat16* q;
   __nv_bfloat16* k_new;
   __nv_bfloat16* v_new;
@@ -162,7 +166,7 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
     if (p.trace) {                                                                       \
       unsigned long long gt_;                                                            \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                            \
-      p.trace[(static_cast<size_t>(p.layer) * gridDim.x + blockIdx.x) * 16 + (k)] = gt_; \
+      p.trace[(static_cast<size_t>(p.layer) * gridDim.x + blockIdx.x) * 32 + (k)] = gt_; \
     }                                                                                    \
   } while (0)
 
@@ -217,7 +221,9 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(p.wpack) +
                             (static_cast<size_t>(p.layer) * U + u0) * kWTile;
       auto xsrc = [&](int it) {
-        return reinterpret_cast<const uint8_t*>(p.xbuf) + static_cast<size_t>((u0 + it) % nkb) * N * 128;
+        const uint8_t* xb = (p.dev & 1024) ? reinterpret_cast<const uint8_t*>(p.wpack)  // dev: stale source
+                                           : reinterpret_cast<const uint8_t*>(p.xbuf);
+        return xb + static_cast<size_t>((u0 + it) % nkb) * N * 128;
       };
       const int pre = min(S, nk);
       for (int it = 0; it < pre; ++it) {  // weights do not depend on the previous kernel
@@ -245,8 +251,14 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
       for (int it = 0; it < nk; ++it) {
         const int st = it % S, u = u0 + it, seg = u / nkb - head0;
         const bool first = it == 0 || u % nkb == 0;
-        mbar_wait(&full[st], (it / S) & 1);
+        if (p.dev & 512) {  // dev: spin with test_wait (no try_wait suspend)
+          while (!mbar_test(&full[st], (it / S) & 1)) {
+          }
+        } else if (!(p.dev & 64) || it == 0) {
+          mbar_wait(&full[st], (it / S) & 1);  // dev 64: MMA issue rate only
+        }
         if (it == 0) QKV_STAMP(2);
+        if (it < 16) QKV_STAMP(16 + it);  // dev: per-iteration issue times
         if (it == S - 1) QKV_STAMP(8);
         if (it == S) QKV_STAMP(9);
         if (it == (S + nk) / 2) QKV_STAMP(10);
@@ -257,7 +269,8 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
           if (!(p.dev & 2))
             umma_bf16(tmem + (seg * nacc + (kk & (nacc - 1))) * N, umma_desc(a_base + kk * 32, 16, 1024, kLayoutSW128),
                       umma_desc(b_base + kk * 32, 16, 1024, kLayoutSW128), idesc, (!first || kk >= nacc) ? 1u : 0u);
-        umma_commit(&empty[st]);
+        if (p.dev & 256) mbar_arrive(&empty[st]);  // dev: plain arrive instead of tcgen05.commit
+        else if (!(p.dev & 128)) umma_commit(&empty[st]);
         if (u + 1 == u1 || (u + 1) % nkb == 0) umma_commit(&acc_bar[seg]);
       }
       QKV_STAMP(3);
@@ -429,8 +442,8 @@ SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, i
   if (e == cudaSuccess) e = cudaMalloc(&h->counters, heads * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(h->counters, 0, heads * sizeof(int));
   if (e == cudaSuccess && std::getenv("SA_QKV_TRACE")) {
-    e = cudaMalloc(&h->trace, static_cast<size_t>(n_layers) * h->max_grid * 16 * 8);
-    if (e == cudaSuccess) e = cudaMemset(h->trace, 0, static_cast<size_t>(n_layers) * h->max_grid * 16 * 8);
+    e = cudaMalloc(&h->trace, static_cast<size_t>(n_layers) * h->max_grid * 32 * 8);
+    if (e == cudaSuccess) e = cudaMemset(h->trace, 0, static_cast<size_t>(n_layers) * h->max_grid * 32 * 8);
   }
   if (e == cudaSuccess)
     e = cudaMemcpy(h->gain, attn_norm_gain, static_cast<size_t>(n_layers) * d_model * sizeof(float),
@@ -452,7 +465,7 @@ SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, i
 SA_API sa_status sa_qkv_destroy(sa_qkv* h) {
   if (!h) return SA_OK;
   if (h->trace) {  // dev-only: dump the stamps of the last call per layer
-    std::vector<unsigned long long> t(static_cast<size_t>(h->L) * h->max_grid * 16);
+    std::vector<unsigned long long> t(static_cast<size_t>(h->L) * h->max_grid * 32);
     if (cudaMemcpy(t.data(), h->trace, t.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
       if (FILE* f = std::fopen("/tmp/sa_qkv_trace.bin", "wb")) {
         std::fwrite(t.data(), 8, t.size(), f);

@@ -37,7 +37,7 @@ with torch.cuda.stream(s):
         g.replay()
 torch.cuda.synchronize()
 proj.close()
-t = np.fromfile("/tmp/sa_qkv_trace.bin", dtype=np.uint64).reshape(L, -1, 16).astype(np.int64)
+t = np.fromfile("/tmp/sa_qkv_trace.bin", dtype=np.uint64).reshape(L, -1, 32).astype(np.int64)
 names = ["start", "pdl", "first", "mma_end", "acc0", "counted", "reduced", "exit", "pre_last", "post_first", "mid"]
 prev_exit = None
 for l in range(L):
@@ -50,3 +50,5 @@ for l in range(L):
     gap = f" gap_from_prev_exit={(t0 - prev_exit) / 1e3:6.2f}" if prev_exit is not None else ""
     prev_exit = a[:, 7].max()
     print(f"L{l}: span={(a[:, 7].max() - t0) / 1e3:6.2f}us " + " ".join(cols) + gap)
+    land = [np.median(a[:, 16 + i][a[:, 16 + i] > 0] - t0) / 1e3 for i in range(16) if (a[:, 16 + i] > 0).any()]
+    print("     MMA iteration (median us): " + " ".join(f"{x:.2f}" for x in land))
