@@ -64,6 +64,7 @@ constexpr int kQkvSmem = 200 * 1024;
 constexpr int kWTile = 128 * 64 * 2;  // 16 KB weight tile (128 output features x 64 of d_model)
 constexpr int kEpiBytes = 8 * 128 * 4;  // epilogue token-group buffer (end of the ring region)
 constexpr int kMaxStages = 12;
+constexpr uint32_t kXResMax = 64 * 1024;  // resident token tiles up to this size
 
 struct QkvParams {
   int layer, n_out, nkb, n_tok, rows, NT, N, Hq, Hkv, heads, style;
@@ -79,10 +80,10 @@ struct QkvParams {
   float* part;    // [grid][2][N][128] per-CTA partial accumulators (one per head touched)
   int* counters;  // [heads] arrivals, re-armed by the reducing CTA
   unsigned long long* trace;  // dev-only (SA_QKV_TRACE): [layer][grid][8] globaltimer stamps
-  // dev knobs (SA_QKV_DEV, timing experiments only; results are wrong with 2/8/64/1024): 1 no L2
-  // prefetch, 2 skip the MMAs, 4 four stages, 8 no token tiles, 64 MMA without waits, 128 no per-stage
-  // commits, 256 plain arrive instead of tcgen05.commit, 512 test_wait spin, 1024 token tiles from a
-  // stale buffer
+  // dev knobs (SA_QKV_DEV, timing experiments only; results are wrong with 2/8/1024/32768): 1 no L2
+  // prefetch, 2 skip the MMAs, 4 four stages, 8 no token tiles, 1024 token tiles from a stale buffer,
+  // 2048 token tiles per stage even when they fit resident, 4096 at most 4 accumulators, 8192 wait for
+  // every preloaded stage before the loop, 16384 no per-iteration stamps, 32768 no refills
   int dev;
   __nv_bfloat16* q;
   __nv_bfloat16* k_new;
@@ -181,19 +182,26 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
   const int U = p.heads * nkb;
   const int u0 = unit_begin(cta, U, n), u1 = unit_begin(cta + 1, U, n), nk = u1 - u0;
   const int head0 = u0 / nkb, nseg = (u1 - 1) / nkb - head0 + 1;  // heads touched (1 or 2)
+  // Token tiles: each bulk copy costs about as much of the SM's copy stream as a 16 KB weight tile,
+  // so when the CTA's whole run of token tiles fits (xres) it is loaded with one copy per head
+  // segment right after the dependency wait and stays resident; otherwise each stage carries one.
   const uint32_t xbytes = N * 128;
-  const uint32_t stage_bytes = kWTile + xbytes;  // weight tile + token tile (hi/lo planes)
-  const uint32_t tx_bytes = (p.dev & 8) ? kWTile : stage_bytes;  // dev 8: X tiles not loaded
+  const bool xres = static_cast<uint32_t>(nk) * xbytes <= kXResMax && !(p.dev & 2048);
+  const uint32_t stage_bytes = kWTile + (xres ? 0u : xbytes);
+  const uint32_t tx_bytes = (p.dev & 8) || xres ? kWTile : stage_bytes;  // dev 8: X tiles not loaded
   const int ring = kQkvSmem - 1024 - 512;
-  const int S = min((p.dev & 4) ? 4 : kMaxStages, static_cast<int>((ring - kEpiBytes) / stage_bytes));
+  const int ring_w = (ring - kEpiBytes - (xres ? nk * static_cast<int>(xbytes) : 0)) & ~1023;
+  uint8_t* xsm = smem + ring_w;  // resident token tiles [nk][N][64] (1 KB aligned for SWIZZLE_128B)
+  const int S = min((p.dev & 4) ? 4 : kMaxStages, static_cast<int>(ring_w / stage_bytes));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ring);
   uint64_t* empty = full + kMaxStages;
   uint64_t* acc_bar = empty + kMaxStages;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_bar + 2);
+  uint64_t* x_bar = acc_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(x_bar + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  // independent accumulators per head segment: consecutive MMAs of one accumulator serialise on their
-  // full latency when N is small (~0.1 us per K=16 step at N=16), so the K-steps rotate over NACC
-  const int nacc = N <= 64 ? 4 : N <= 128 ? 2 : 1;
+  // independent accumulators per head segment: consecutive MMAs into one accumulator serialise on the
+  // MMA latency, which dominates at small N, so the K=16 steps rotate over nacc accumulators
+  const int nacc = (p.dev & 4096) ? (N <= 64 ? 4 : N <= 128 ? 2 : 1) : max(1, min(16, 256 / N));
   const int acols = 2 * nacc * N;
   const uint32_t tcols = acols <= 32 ? 32 : acols <= 64 ? 64 : acols <= 128 ? 128 : acols <= 256 ? 256 : 512;
 
@@ -205,6 +213,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
     }
     mbar_init(&acc_bar[0], 1);
     mbar_init(&acc_bar[1], 1);
+    mbar_init(x_bar, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, tcols);
@@ -234,44 +243,67 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
       pdl_wait();
       QKV_STAMP(1);
       QKV_STAMP(11);
-      if (!(p.dev & 8))
+      if (xres) {
+        const int n0 = min(nk, nkb - u0 % nkb);  // units of the first head segment (contiguous k-blocks)
+        mbar_expect_tx(x_bar, nk * xbytes);
+        bulk_load(xsm, xsrc(0), n0 * xbytes, x_bar);
+        if (nk > n0) bulk_load(xsm + n0 * xbytes, xsrc(n0), (nk - n0) * xbytes, x_bar);
+      } else if (!(p.dev & 8)) {
         for (int it = 0; it < pre; ++it) bulk_load(smem + it * stage_bytes + kWTile, xsrc(it), xbytes, &full[it]);
-      for (int it = pre; it < nk; ++it) {
+      }
+      for (int it = pre; it < ((p.dev & 32768) ? pre : nk); ++it) {  // dev 32768: no refills
         const int st = it % S;
         mbar_wait(&empty[st], ((it / S) - 1) & 1);
         mbar_expect_tx(&full[st], tx_bytes);
         bulk_load(smem + st * stage_bytes, wsrc + static_cast<size_t>(it) * kWTile, kWTile, &full[st]);
-        if (!(p.dev & 8)) bulk_load(smem + st * stage_bytes + kWTile, xsrc(it), xbytes, &full[st]);
+        if (!xres && !(p.dev & 8)) bulk_load(smem + st * stage_bytes + kWTile, xsrc(it), xbytes, &full[st]);
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {  // ------------------------------------------------ MMA issuer
-      const uint32_t idesc = umma_idesc_bf16(N, 0, 0);
-      for (int it = 0; it < nk; ++it) {
-        const int st = it % S, u = u0 + it, seg = u / nkb - head0;
-        const bool first = it == 0 || u % nkb == 0;
-        if (p.dev & 512) {  // dev: spin with test_wait (no try_wait suspend)
-          while (!mbar_test(&full[st], (it / S) & 1)) {
-          }
-        } else if (!(p.dev & 64) || it == 0) {
-          mbar_wait(&full[st], (it / S) & 1);  // dev 64: MMA issue rate only
-        }
+  } else if (warp == 1) {  // --------------------------------------- MMA issuer: the whole warp loops,
+    // waits are warp-wide and lane 0 issues the tcgen05 instructions
+    const uint32_t idesc = umma_idesc_bf16(N, 0, 0);
+    if (xres) mbar_wait(x_bar, 0);
+    if (p.dev & 8192) {  // dev: wait until every preloaded stage landed, then time the loop over them
+      for (int i = 0; i < min(S, nk); ++i) mbar_wait(&full[i], 0);
+      if (lane == 0) QKV_STAMP(12);
+    }
+    const int nk_mma = (p.dev & 32768) ? min(S, nk) : nk;
+    const int n0 = min(nk, nkb - u0 % nkb);  // units of the first head segment
+    int st = 0;
+    uint32_t phase = 0;
+    for (int it = 0; it < nk_mma; ++it) {
+      const int seg = it < n0 ? 0 : 1, seg_it = it < n0 ? it : it - n0;
+      mbar_wait(&full[st], phase);
+      tc_fence_after();
+      if (lane == 0) {
         if (it == 0) QKV_STAMP(2);
-        if (it < 16) QKV_STAMP(16 + it);  // dev: per-iteration issue times
+        if (it < 16 && !(p.dev & 16384)) QKV_STAMP(16 + it);  // dev: per-iteration issue times
         if (it == S - 1) QKV_STAMP(8);
         if (it == S) QKV_STAMP(9);
         if (it == (S + nk) / 2) QKV_STAMP(10);
-        tc_fence_after();
-        const uint32_t a_base = smem_u32(smem + st * stage_bytes), b_base = a_base + kWTile;
+        const uint32_t a_base = smem_u32(smem + st * stage_bytes);
+        const uint32_t b_base = xres ? smem_u32(xsm + it * xbytes) : a_base + kWTile;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
+        for (int kk = 0; kk < 4; ++kk) {
+          const int m = seg_it * 4 + kk;  // MMA index within the segment: accumulator m % nacc
           if (!(p.dev & 2))
-            umma_bf16(tmem + (seg * nacc + (kk & (nacc - 1))) * N, umma_desc(a_base + kk * 32, 16, 1024, kLayoutSW128),
-                      umma_desc(b_base + kk * 32, 16, 1024, kLayoutSW128), idesc, (!first || kk >= nacc) ? 1u : 0u);
-        if (p.dev & 256) mbar_arrive(&empty[st]);  // dev: plain arrive instead of tcgen05.commit
-        else if (!(p.dev & 128)) umma_commit(&empty[st]);
-        if (u + 1 == u1 || (u + 1) % nkb == 0) umma_commit(&acc_bar[seg]);
+            umma_bf16(tmem + (seg * nacc + (m & (nacc - 1))) * N, umma_desc(a_base + kk * 32, 16, 1024, kLayoutSW128),
+                      umma_desc(b_base + kk * 32, 16, 1024, kLayoutSW128), idesc, m >= nacc ? 1u : 0u);
+        }
+        umma_commit(&empty[st]);
+        if (it + 1 == nk || it + 1 == n0) umma_commit(&acc_bar[seg]);
+      }
+      __syncwarp();
+      if (++st == S) {
+        st = 0;
+        phase ^= 1u;
+      }
+    }
+    if (lane == 0) {
+      if ((p.dev & 32768) && nk_mma < nk) {  // dev: release the epilogue (results meaningless)
+        umma_commit(&acc_bar[0]);
+        if (nseg > 1) umma_commit(&acc_bar[1]);
       }
       QKV_STAMP(3);
     }
@@ -297,10 +329,12 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
       tc_fence_after();
       float* mine = p.part + (static_cast<size_t>(cta) * 2 + seg) * N * 128;
       const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + seg * nacc * N;
+      const int seg_units = seg == 0 ? min(nk, nkb - u0 % nkb) : nk - (nkb - u0 % nkb);
+      const int used = min(nacc, 4 * seg_units);  // accumulators this segment wrote
       for (int c = 0; c < N; c += 16) {
         float v[16], w[16];
         tmem_ld16(lane_base + c, v);
-        for (int a = 1; a < nacc; ++a) {  // fixed order: deterministic
+        for (int a = 1; a < used; ++a) {  // fixed order: deterministic
           tmem_ld16(lane_base + a * N + c, w);
           tc_wait_ld();
 #pragma unroll

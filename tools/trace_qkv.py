@@ -38,7 +38,7 @@ with torch.cuda.stream(s):
 torch.cuda.synchronize()
 proj.close()
 t = np.fromfile("/tmp/sa_qkv_trace.bin", dtype=np.uint64).reshape(L, -1, 32).astype(np.int64)
-names = ["start", "pdl", "first", "mma_end", "acc0", "counted", "reduced", "exit", "pre_last", "post_first", "mid"]
+names = ["start", "pdl", "first", "mma_end", "acc0", "counted", "reduced", "exit", "pre_last", "post_first", "mid", "pdl2", "allpre"]
 prev_exit = None
 for l in range(L):
     a = t[l]
