@@ -162,7 +162,7 @@ struct DCfg {
   // r+1 is gathered while round r is computed (one CTA per SM)
   static constexpr int kOffBuf1 = (kOffBar + 16 + 1023) / 1024 * 1024;
   static constexpr int kSmemStream = kOffBuf1 + 2 * kMaxTiles * kTileBytes + 1024;
-  static_assert(kMaxWarps * 8 * 128 * 4 <= kOffPart, "warp partials must fit in the tile buffers");
+  static_assert(kMaxWarps * 8 * 132 * 4 <= kOffPart, "warp partials must fit in the tile buffers");
   static_assert(kMaxTiles * kTile * 8 >= kMaxWarps * 16 * 4, "warp (m, l) table fits the row-source area");
   static_assert(kSmem <= 113 * 1024, "two CTAs per SM: the next PDL launch co-resides");
   static_assert(kSmemStream <= 227 * 1024, "streaming mode fits one CTA per SM");
@@ -360,93 +360,74 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   w.finalize_l();
   dtrace(p, 3);
 
-  // in-CTA merge of the warps' partials (only the G real query rows), fused with the push:
-  //  (1) every warp publishes its per-row (m, l); (2) every warp rescales its O fragments to the
-  //  CTA-wide row max and stores them; one thread per row forms (m*, l); (3) each thread sums the
-  //  warps' float4 groups and pushes the result straight into the owner's inbox with st.async.
-  float* wps = reinterpret_cast<float*>(smem);             // [nwarps][G x 128] rescaled partials
+  // in-CTA merge of the warps' partials (only the G real query rows), fused with the push: every
+  // warp stores its raw O fragments and (m, l); after one barrier each thread rescales the warps'
+  // float4 groups of its output to the CTA-wide row max, sums them in warp order (deterministic)
+  // and pushes the result straight into the owner's inbox with st.async; the first thread of each
+  // row also pushes the row's (m*, l*).
+  constexpr int kWs = 132;  // padded row stride of a warp partial (floats): conflict-free stores
+  float* wps = reinterpret_cast<float*>(smem);             // [nwarps][G][kWs] raw partials
   float* wml = reinterpret_cast<float*>(smem + DCfg::kOffRow);  // [kMaxWarps][16]: m[8], l[8]
   __syncthreads();  // every warp done reading K/V tiles (wps aliases them) and src_row
   dtrace(p, 8);
   const int gid = lane >> 2, t4 = lane & 3;
-  if (gid == 0) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      wml[warp * 16 + 2 * t4 + e] = w.m[e];
-      wml[warp * 16 + 8 + 2 * t4 + e] = w.l[e];
-    }
-  }
-  __syncthreads();
-  dtrace(p, 9);
   {
-    float* wp = wps + warp * (p.G * 128);
+    float* wp = wps + warp * (p.G * kWs);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int row = 2 * t4 + e;
       if (row < p.G) {
-        float mq[DCfg::kMaxWarps];  // independent loads, then a max tree (no serial smem chain)
-#pragma unroll
-        for (int q = 0; q < DCfg::kMaxWarps; ++q) mq[q] = q < nwarps ? wml[q * 16 + row] : -INFINITY;
-        float mstar = -INFINITY;
-#pragma unroll
-        for (int q = 0; q < DCfg::kMaxWarps; ++q) mstar = fmaxf(mstar, mq[q]);
-        const float f = (w.m[e] == -INFINITY) ? 0.f : fast_exp2(w.m[e] - mstar);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-          wp[row * 128 + 16 * jj + gid] = w.o[jj][e] * f;
-          wp[row * 128 + 16 * jj + gid + 8] = w.o[jj][2 + e] * f;
+          wp[row * kWs + 16 * jj + gid] = w.o[jj][e];
+          wp[row * kWs + 16 * jj + gid + 8] = w.o[jj][2 + e];
+        }
+        if (gid == 0) {
+          wml[warp * 16 + row] = w.m[e];
+          wml[warp * 16 + 8 + row] = w.l[e];
         }
       }
     }
   }
-  dtrace(p, 10);
-  if (tid < p.G) {  // CTA-wide (m*, l) of row tid
-    float mq[DCfg::kMaxWarps], lq[DCfg::kMaxWarps];
-#pragma unroll
-    for (int q = 0; q < DCfg::kMaxWarps; ++q) {
-      mq[q] = q < nwarps ? wml[q * 16 + tid] : -INFINITY;
-      lq[q] = q < nwarps ? wml[q * 16 + 8 + tid] : 0.f;
-    }
-    float mstar = -INFINITY;
-#pragma unroll
-    for (int q = 0; q < DCfg::kMaxWarps; ++q) mstar = fmaxf(mstar, mq[q]);
-    float lsum = 0.f;
-#pragma unroll
-    for (int q = 0; q < DCfg::kMaxWarps; ++q) lsum += mq[q] == -INFINITY ? 0.f : lq[q] * fast_exp2(mq[q] - mstar);
-    part[1024 + tid] = mstar;
-    part[1024 + 8 + tid] = lsum;
-  }
-  dtrace(p, 11);
   __syncthreads();
   dtrace(p, 5);
   cluster_wait_acquire();  // every owner's inbox barrier is initialised
   if (tid == 0) {
     const int my_vals = my_hi - my_lo;
-    mbar_arrive_expect_tx(inbox_bar, static_cast<uint32_t>(CS) * (my_vals + 16) * 4u);
+    mbar_arrive_expect_tx(inbox_bar, static_cast<uint32_t>(CS) * (my_vals + 2 * p.G) * 4u);
   }
   const uint32_t inbox_addr = smem_u32(inbox), bar_addr = smem_u32(inbox_bar);
   for (int q4 = tid; q4 < n_out / 4; q4 += nthr) {
-    float4 x[DCfg::kMaxWarps];
+    const int e = q4 * 4, row = e >> 7, col = e & 127;
+    float mq[DCfg::kMaxWarps];
 #pragma unroll
-    for (int q = 0; q < DCfg::kMaxWarps; ++q)
-      x[q] = q < nwarps ? reinterpret_cast<const float4*>(wps + q * (p.G * 128))[q4] : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 v = x[0];
+    for (int q = 0; q < DCfg::kMaxWarps; ++q) mq[q] = q < nwarps ? wml[q * 16 + row] : -INFINITY;
+    float mstar = -INFINITY;
 #pragma unroll
-    for (int q = 1; q < DCfg::kMaxWarps; ++q) {  // fixed warp order: deterministic
-      v.x += x[q].x;
-      v.y += x[q].y;
-      v.z += x[q].z;
-      v.w += x[q].w;
+    for (int q = 0; q < DCfg::kMaxWarps; ++q) mstar = fmaxf(mstar, mq[q]);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    float lsum = 0.f;
+#pragma unroll
+    for (int q = 0; q < DCfg::kMaxWarps; ++q) {  // fixed warp order: deterministic
+      if (q < nwarps) {
+        const float f = mq[q] == -INFINITY ? 0.f : fast_exp2(mq[q] - mstar);
+        const float4 x = *reinterpret_cast<const float4*>(wps + (q * p.G + row) * kWs + col);
+        v.x += x.x * f;
+        v.y += x.y * f;
+        v.z += x.z * f;
+        v.w += x.w * f;
+        if (col == 0) lsum += wml[q * 16 + 8 + row] * f;
+      }
     }
-    const int e = q4 * 4, owner = e / per;
+    const int owner = e / per;
     st_async_v4(mapa_shared(inbox_addr + (split * rstride + (e - owner * per)) * 4, owner), v,
                 mapa_shared(bar_addr, owner));
-  }
-  for (int t = tid; t < CS * 4; t += nthr) {
-    const int owner = t >> 2, q = t & 3;
-    const float4 v = *reinterpret_cast<const float4*>(part + 1024 + 4 * q);  // m[0..7], l[0..7]
-    st_async_v4(mapa_shared(inbox_addr + (split * rstride + per + 4 * q) * 4, owner), v,
-                mapa_shared(bar_addr, owner));
+    if (col == 0)  // this row's (m*, l*) to every owner
+      for (int o = 0; o < CS; ++o) {
+        const uint32_t ob = mapa_shared(bar_addr, o);
+        st_async_f32(mapa_shared(inbox_addr + (split * rstride + per + row) * 4, o), mstar, ob);
+        st_async_f32(mapa_shared(inbox_addr + (split * rstride + per + 8 + row) * 4, o), lsum, ob);
+      }
   }
   // combine my slice once every sender's contribution has landed
   dtrace(p, 6);
