@@ -760,6 +760,7 @@ __global__ void __launch_bounds__(384, 1)
     named_bar_sync(bar_wg, 128);
     if (ts < N) ltot[wg * 64 + ts] = red[ts] + red[64 + ts] + red[128 + ts] + red[192 + ts];
     named_bar_sync(1, 256);  // both warpgroups' (mref, ltot) final
+    if (wg == 0 && ts == 0) SA_TSTAMP(10);
     const bool single = p.n_splits == 1;  // this CTA owns the whole unit: normalise in place
     float* po = p.part_o + static_cast<size_t>(unit) * p.n_splits * N * 128;
     float* pml = p.part_ml + static_cast<size_t>(unit) * p.n_splits * N * 2;
@@ -780,6 +781,7 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
     named_bar_sync(1, 256);
+    if (wg == 0 && ts == 0) SA_TSTAMP(11);
     // merge the two warpgroups' O^T: warpgroup 0 takes even 16-column chunks, warpgroup 1 odd ones;
     // only the M real rows are stored (partial rows keep the N-row stride)
     for (int c16 = wg; c16 < N / 16; c16 += 2) {
@@ -808,6 +810,7 @@ __global__ void __launch_bounds__(384, 1)
         else my_o[m * 128 + tk] = acc;
       }
     }
+    if (wg == 0 && ts == 0) SA_TSTAMP(12);
     tc_fence_before();
     if (single) {
       if (wg == 0 && ts == 0) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
