@@ -166,6 +166,7 @@ cudaError_t launch_window(const int32_t* p0, int B, int64_t sink, int64_t window
                           int32_t* k_out, cudaStream_t s);
 cudaError_t launch_accept(const float* p, const float* q, const int32_t* draft, const float* u, int B, int gamma, int V,
                           int greedy, int32_t* accepted, int32_t* emitted, cudaStream_t s);
+constexpr int kWeightParts = 8;  // Collect2Weights row statistics: CTAs per logit row
 cudaError_t launch_weights(const float* logits, int64_t ld, const int32_t* p0, int B, int Hq, int G, int n_rows,
                            double scale, float2* stats, int n_sets, long long* fx, float* scores, int64_t ld_scores,
                            int64_t max_p, cudaStream_t s);

@@ -505,7 +505,7 @@ static sa_status ensure_weight_buffers(sa_runner* r) {  // lazily: only the weig
   const size_t bytes = sizeof(float) * r->cfg.max_batch * r->Hq * 2 * r->ld;
   for (auto& w : r->wlogits)
     if (!w) SA_CUDA_CHECK(cudaMalloc(&w, bytes));
-  if (!r->wstats) SA_CUDA_CHECK(cudaMalloc(&r->wstats, sizeof(float2) * r->cfg.max_batch * r->Hq * r->cfg.max_rows));
+  if (!r->wstats) SA_CUDA_CHECK(cudaMalloc(&r->wstats, sizeof(float2) * sa::kWeightParts * r->cfg.max_batch * r->Hq * r->cfg.max_rows));
   return SA_OK;
 }
 
@@ -517,7 +517,7 @@ static sa_status weights_impl(sa_runner* r, int32_t slot, const float* logits, i
   if (n_rows < 1 || n_rows > r->cfg.max_rows) return fail(SA_INVALID_ARGUMENT, "score_columns_weights: empty row subset");
   if (ld < r->p_max) return fail(SA_INVALID_ARGUMENT, "score_weights: ld_logits < prefix");
   if (mode != SA_PER_LAYER && mode != SA_PER_KV_HEAD) return fail(SA_INVALID_ARGUMENT, "score_weights: mode");
-  if (!r->wstats) SA_CUDA_CHECK(cudaMalloc(&r->wstats, sizeof(float2) * r->cfg.max_batch * r->Hq * r->cfg.max_rows));
+  if (!r->wstats) SA_CUDA_CHECK(cudaMalloc(&r->wstats, sizeof(float2) * sa::kWeightParts * r->cfg.max_batch * r->Hq * r->cfg.max_rows));
   const int n_sets = mode == SA_PER_LAYER ? 1 : r->Hkv;
   long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, slot, nullptr));
   float* scores = sa_runner_scores(r, slot, nullptr);

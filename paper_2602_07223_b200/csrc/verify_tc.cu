@@ -52,7 +52,7 @@ struct TCfg {
   //       | tile_pos[kPosRing] | producer ring pring[32]
   static constexpr int kBtMax = 1024;                  // block-table entries staged in smem
   static constexpr int kMiscBytes = 16 + (2 + 2 + 2 + 1 + 1) * 64 * 4 + 2 * 4 * 64 * 4 + kPosRing * 4 + 32 * 4 +
-                                    kBtMax * 4;
+                                    kBtMax * 4 + 64 * 4;
   static constexpr int kSmem = kOffMisc + kMiscBytes + 1024;
   static constexpr int kThreads = 384;
   // TMEM columns: S[2] (N each) then O[2] (kNP each: O_hi | O_lo)
@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(384, 1)
   int* tile_pos = reinterpret_cast<int*>(red_all + 512);                 // [kPosRing]
   int* pring = tile_pos + C::kPosRing;                                   // [32] producer-private
   int* bt = pring + 32;                                                  // [kBtMax] this sequence's pages
+  int* loff = bt + C::kBtMax;  // [64] raw-logit output offset of row m (LogitMatrix path), -1: not collected
   int* ntiles_wg = flag + 1;                                             // [2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -351,6 +352,11 @@ __global__ void __launch_bounds__(384, 1)
     mref_all[64 + tid] = -INFINITY;
     lim[tid] = tid < M ? p0 + tid % R : -1;  // last key position row m may see (causal window)
     wsc[tid] = (tid < M && ((p.score_mask >> (tid % R)) & 1u)) ? 1.f : 0.f;
+    const int r = tid % R;
+    loff[tid] = (p.logits && tid < M && ((p.collect_mask >> r) & 1u))
+                    ? ((g * p.G + tid / R) * p.n_collect + __popc(p.collect_mask & ((1u << r) - 1u))) *
+                          static_cast<int>(p.ld_logits)
+                    : -1;
   }
   if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
@@ -627,14 +633,12 @@ __global__ void __launch_bounds__(384, 1)
         else
           score_out[pos] = sc;
       }
-      if (p.logits && pos < p0) {  // debug / variant path: raw prefix logits
+      if (p.logits && pos < p0) {  // LogitMatrix path (Collect2Weights, debug): raw prefix logits
+        float* lb = p.logits + static_cast<size_t>(b) * Hq * p.n_collect * p.ld_logits + pos;
 #pragma unroll
         for (int m = 0; m < N; ++m) {
-          if (m >= M) continue;
-          const int r = m % R;
-          if (!((p.collect_mask >> r) & 1u)) continue;
-          const int ci = __popc(p.collect_mask & ((1u << r) - 1u));
-          p.logits[((static_cast<size_t>(b) * Hq + g * p.G + m / R) * p.n_collect + ci) * p.ld_logits + pos] = s[m];
+          const int o = loff[m];  // smem broadcast, precomputed per CTA
+          if (o >= 0) lb[o] = s[m];
         }
       }
       // pass 1: does any logit exceed the lazy reference by more than 2^8?  (mref held in registers:
