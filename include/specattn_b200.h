@@ -281,7 +281,9 @@ SA_API sa_status sa_exchange_layer_scores(sa_runner* r, int32_t layer_slot, void
 SA_API sa_status sa_accept(const float* p, const float* q, const int32_t* draft, const float* u, int32_t B,
                            int32_t gamma, int32_t V, int32_t greedy, int32_t* accepted, int32_t* emitted, void* stream);
 /* Commit after acceptance (kv_store.cpp:51-65): the verify rows [p0, p0+accepted] (y and
- * the accepted drafts) stay, the store is truncated to p0 + accepted + 1 and committed. */
+ * the accepted drafts, written by sa_verify_attention's fused append) stay; the store's length and
+ * committed mark become p0 + accepted + 1.  OUT_OF_RANGE if p0 is past the current length or the
+ * kept rows were never reserved. */
 SA_API sa_status sa_kv_commit_accepted(sa_cache* cache, int32_t seq, int64_t p0, int32_t accepted);
 
 /* ------------------------------------------------------- model-side producer (§8f rank 4)

@@ -216,10 +216,15 @@ SA_API sa_status sa_accept(const float* p, const float* q, const int32_t* draft,
 SA_API sa_status sa_kv_commit_accepted(sa_cache* c, int32_t seq, int64_t p0, int32_t accepted) {
   if (!c) return fail(SA_INVALID_ARGUMENT, "null cache");
   if (seq < 0 || seq >= c->max_seqs) return fail(SA_OUT_OF_RANGE, "sequence id out of range");
-  if (accepted < 0 || p0 < 0 || p0 + accepted + 1 > c->len[seq])
-    return fail(SA_OUT_OF_RANGE, "KvStore: truncate beyond current length");
-  if (sa_status st = sa_kv_truncate(c, seq, p0 + accepted + 1)) return st;
-  return sa_kv_set_committed(c, seq, p0 + accepted + 1);
+  // The verify rows p0.. were written by the verify kernel's fused append into pages reserved for
+  // them (sa_runner_set_batch), whether or not the host length was advanced: keep p0 .. p0+accepted.
+  const int64_t keep = p0 + accepted + 1;
+  if (accepted < 0 || p0 < 0 || p0 > c->len[seq] || keep > (c->pages_of_seq[seq] << c->page_shift))
+    return fail(SA_OUT_OF_RANGE, "KvStore: commit beyond the appended verify rows");
+  c->summaries_stale_from(seq, std::min(c->len[seq], p0));
+  c->len[seq] = keep;
+  c->committed[seq] = keep;
+  return SA_OK;
 }
 
 SA_API sa_status sa_kv_enable_page_summaries(sa_cache* c, int64_t page_size) {

@@ -706,7 +706,7 @@ def test_commit_accepted(cuda, ref):
         c.commit_accepted(5, 2)  # verify rows 5..9 = [y, x1..x4]; a = 2 keeps 5,6,7
         assert c.size() == 8 and c.committed() == 8
         with pytest.raises(SpecAttnError):
-            c.commit_accepted(5, 4)  # beyond the current length
+            c.commit_accepted(200, 100)  # beyond the reserved rows
     finally:
         c.close()
 
@@ -766,4 +766,57 @@ def test_qkv_projection_deterministic_and_errors(cuda):
         proj.project(1, x, pos)  # layer out of range
     with pytest.raises(SpecAttnError):
         proj.project(0, torch.randn(2, 65, 512, device="cuda"), pos)  # > 128 tokens
+    proj.close()
+
+
+def test_producer_feeds_verify_and_commit(cuda, ref):
+    """The §8f producer's q / k_new / v_new drive the verify kernel directly (layouts end to end), the
+    acceptance kernel decides, and commit_accepted leaves the cache at p0 + a + 1."""
+    torch = cuda
+    from oracle.model import qkv_project
+    from oracle.speculation import accept as ref_accept
+    from paper_2602_07223_b200 import QkvProjection, accept
+    Runner, _, _ = _lib()
+    Hkv, G, R, p0, Dm = 2, 4, 5, 300, 256
+    Hq = Hkv * G
+    m = Matched(ref, L=2, Hkv=Hkv, n_tokens=p0, seed=41, max_context=p0 + R + 64, page_size=128)
+    rng = np.random.default_rng(41)
+    w = rng.standard_normal((2, (Hq + 2 * Hkv) * 128, Dm)).astype(np.float32) / 16
+    w = torch.from_numpy(w).to(torch.bfloat16)
+    gain = (1 + 0.1 * rng.standard_normal((2, Dm))).astype(np.float32)
+    proj = QkvProjection(w.cuda(), torch.from_numpy(gain).cuda(), Hq, Hkv)
+    x = rng.standard_normal((1, R, Dm)).astype(np.float32)
+    q, kn, vn = proj.project(1, torch.from_numpy(x).cuda(), torch.tensor([p0], dtype=torch.int32, device="cuda"))
+    r = Runner(m.cache, Hq, max_rows=R, max_prefix=p0)
+    r.set_batch([0], [p0])
+    out = torch.zeros((1, Hq, R, D), dtype=torch.float32, device="cuda")
+    r.verify(1, q, out, kn, vn, SCALE, score_row_mask=1 | (1 << (R - 1)))
+    torch.cuda.synchronize()
+    # producer outputs vs the float64 restatement (half a bf16 ulp + fp32 slack)
+    rq, rk, _ = qkv_project(x, w[1].float().numpy(), gain[1], Hq, Hkv, [p0])
+    assert np.all(np.abs(q.float().cpu().numpy() - rq) <= 2.0 ** -8 * np.abs(rq) + 1e-4)
+    assert np.all(np.abs(kn.float().cpu().numpy() - rk) <= 2.0 ** -8 * np.abs(rk) + 1e-4)
+    # verify over the producer's exact bf16 values vs the reference TUs
+    qh, kh, vh = (t.float().cpu().numpy() for t in (q, kn, vn))
+    kv = m.refs[0]
+    for t in range(R):
+        kk = np.zeros((2 * Hkv, D), np.float32)
+        vv = np.zeros((2 * Hkv, D), np.float32)
+        kk[Hkv:], vv[Hkv:] = kh[0, t], vh[0, t]
+        kv.append(kk, vv)
+    o_ref, _ = kv.verify_layer(1, Hq, qh[0], p0, R, SCALE, threads=8)
+    assert rel_err_rows(out.cpu().numpy()[0], o_ref) < 2e-4
+    # acceptance on the device, then commit: the store keeps [y, x_1..x_a] and drops the rest
+    V = 64
+    pp = rng.dirichlet(np.ones(V), size=(1, R)).astype(np.float32)
+    qq = rng.dirichlet(np.ones(V), size=(1, R - 1)).astype(np.float32)
+    xx = rng.integers(0, V, size=(1, R - 1)).astype(np.int32)
+    uu = rng.random((1, R)).astype(np.float32)
+    acc, em = accept(*(torch.from_numpy(a_).cuda() for a_ in (pp, xx)), q=torch.from_numpy(qq).cuda(),
+                     u=torch.from_numpy(uu).cuda())
+    a_ref, e_ref = ref_accept(pp[0], xx[0], q=qq[0], u=uu[0])
+    a = int(acc.item())
+    assert a == a_ref and list(em.cpu().numpy()[0, :a + 1]) == e_ref
+    m.cache.commit_accepted(p0, a)
+    assert m.cache.size() == p0 + a + 1 and m.cache.committed() == p0 + a + 1
     proj.close()
