@@ -10,9 +10,10 @@
 // min / max of bf16 keys are exact in bf16).  quest_summarize recomputes a token range's quest pages
 // (the cache refreshes lazily: rows changed by appends / fused appends / truncation mark pages
 // stale, the next Quest selection recomputes them first).  quest_bounds: one warp per quest page.
-// quest_pick: one CTA per sequence, bitonic sort of the (bound, page) pairs in shared memory, a
-// block scan of the pages' token counts in rank order, then a scan in page order writes the
-// ascending position list.
+// quest_pick: one CTA per sequence: a radix select finds the key of the last page that can be
+// needed (rank ceil(k/qpage)+1), only the pages at or above it are sorted (bitonic, shared memory),
+// a block scan of their token counts in rank order decides what is taken, then a scan in page order
+// writes the ascending position list.
 #include "internal.h"
 
 namespace sa {
@@ -72,28 +73,33 @@ __global__ void __launch_bounds__(256) quest_bounds_kernel(CacheView c, const __
   const int64_t n_qp = (p0 + qpage - 1) / qpage;
   if (qp >= n_qp) return;
   const int seq = seq_ids[b];
+  // each lane owns 4 dims: its per-head partials (fp32 over 4 dims) accumulate in double across the
+  // heads, and one butterfly reduces the lanes (the reference's per-head fp32 sum over d is an
+  // unpinned Eigen order; this order differs from it at the 1e-7 level, far inside the tie band)
   double acc = 0.0;
+#pragma unroll 4
   for (int g = 0; g < c.n_kv_heads; ++g) {
     const int64_t o = qsum_row(c, qpage, seq, layer, g, qp * qpage) * 128 + lane * 4;
-    float mn[4], mx[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      mn[e] = __bfloat162float(qmin[o + e]);
-      mx[e] = __bfloat162float(qmax[o + e]);
-    }
+    const uint2 mnr = *reinterpret_cast<const uint2*>(qmin + o), mxr = *reinterpret_cast<const uint2*>(qmax + o);
+    const float2 mn01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&mnr.x));
+    const float2 mn23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&mnr.y));
+    const float2 mx01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&mxr.x));
+    const float2 mx23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&mxr.y));
+    const float mn[4] = {mn01.x, mn01.y, mn23.x, mn23.y}, mx[4] = {mx01.x, mx01.y, mx23.x, mx23.y};
+#pragma unroll 4
     for (int hh = 0; hh < G; ++hh) {
-      const __nv_bfloat16* qh = q + (static_cast<size_t>(b) * Hq + g * G + hh) * 128 + lane * 4;
+      const uint2 qr = __ldg(reinterpret_cast<const uint2*>(q + (static_cast<size_t>(b) * Hq + g * G + hh) * 128 + lane * 4));
+      const float2 q01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qr.x));
+      const float2 q23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qr.y));
+      const float qv[4] = {q01.x, q01.y, q23.x, q23.y};
       float t = 0.f;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float qv = __bfloat162float(qh[e]);
-        t += fmaxf(qv * mn[e], qv * mx[e]);
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+      for (int e = 0; e < 4; ++e) t += fmaxf(qv[e] * mn[e], qv[e] * mx[e]);
       acc += static_cast<double>(t);
     }
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) bounds[static_cast<size_t>(b) * ld + qp] = acc;
 }
 
@@ -115,43 +121,113 @@ __global__ void __launch_bounds__(1024) quest_pick_kernel(const int32_t* p0s, in
   int npow = 1;
   while (npow < n_qp) npow <<= 1;
   unsigned long long* key = qsm;                                   // [npow]
-  int* pg = reinterpret_cast<int*>(qsm + npow);                    // [npow]
-  int* take = pg + npow;                                           // [n_qp] tokens taken per page
+  int* take = reinterpret_cast<int*>(qsm + npow);                  // [n_qp] tokens taken per page
   __shared__ int wsum[32];
   __shared__ int s_rank, s_before;
   long long k = llround(ratio * static_cast<double>(p0));
   k = min(static_cast<long long>(p0), max(k, static_cast<long long>(k_min)));
   if (k > k_cap) k = k_cap;
-  for (int i = tid; i < npow; i += 1024) {
-    key[i] = i < n_qp ? dkey(bounds[static_cast<size_t>(b) * ld + i]) : 0ull;  // padding sorts last
-    pg[i] = i;
-  }
+  for (int i = tid; i < n_qp; i += 1024) key[i] = dkey(bounds[static_cast<size_t>(b) * ld + i]);
   for (int i = tid; i < n_qp; i += 1024) take[i] = 0;
   __syncthreads();
-  // bitonic sort: descending key, ties -> ascending page
-  for (int size = 2; size <= npow; size <<= 1)
+  // (1) radix select (8-bit digits, MSB first) of T = the m_need-th largest key: only pages ranked
+  // before it can be taken (m_need covers k tokens even if the partial last page ranks among them)
+  const int m_need = static_cast<int>(min(static_cast<long long>(n_qp), (k + qpage - 1) / qpage + 1));
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_rem, s_nc;
+  if (tid == 0) {
+    s_prefix = 0ull;
+    s_rem = m_need;
+    s_nc = 0;
+  }
+  unsigned long long mask = 0ull;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    if (tid < 256) hist[tid] = 0u;
+    __syncthreads();
+    const unsigned long long prefix = s_prefix;
+    for (int i = tid; i < n_qp; i += 1024)
+      if ((key[i] & mask) == prefix) atomicAdd(&hist[(key[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    if (tid < 32) {  // lane l owns bins 255-8l .. 248-8l (descending)
+      unsigned int cnt[8], sum = 0u;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        cnt[e] = hist[255 - 8 * tid - e];
+        sum += cnt[e];
+      }
+      unsigned int incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (tid >= off) incl += t;
+      }
+      const int rem = s_rem;
+      const unsigned int hit = __ballot_sync(0xffffffffu, incl >= static_cast<unsigned int>(rem));
+      const int l = __ffs(hit) - 1;  // first lane whose bins reach the remaining rank
+      if (tid == l) {
+        unsigned int above = incl - sum;
+        int d = 255 - 8 * l;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (above + cnt[e] >= static_cast<unsigned int>(rem)) {
+            d = 255 - 8 * l - e;
+            break;
+          }
+          above += cnt[e];
+        }
+        s_prefix = prefix | (static_cast<unsigned long long>(d) << shift);
+        s_rem = rem - static_cast<int>(above);
+      }
+    }
+    mask |= 0xFFull << shift;
+    __syncthreads();
+  }
+  const unsigned long long T = s_prefix;
+  // (2) candidates: every page with key >= T (ties with T included), compacted, then sorted
+  unsigned long long* ckey = reinterpret_cast<unsigned long long*>(take + n_qp + (n_qp & 1));  // [npow]
+  int* cpg = reinterpret_cast<int*>(ckey + npow);                                                // [npow]
+  for (int i = tid; i < n_qp; i += 1024)
+    if (key[i] >= T) {
+      const int slot = atomicAdd(&s_nc, 1);
+      ckey[slot] = key[i];
+      cpg[slot] = i;
+    }
+  __syncthreads();
+  const int nc = s_nc;
+  int cpow = 1;
+  while (cpow < nc) cpow <<= 1;
+  for (int i = nc + tid; i < cpow; i += 1024) {
+    ckey[i] = 0ull;  // padding sorts last
+    cpg[i] = 0x7fffffff;
+  }
+  __syncthreads();
+  // bitonic sort of the candidates: descending key, ties -> ascending page
+  for (int size = 2; size <= cpow; size <<= 1)
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < npow / 2; i += 1024) {
+      for (int i = tid; i < cpow / 2; i += 1024) {
         const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const bool up = (lo & size) == 0;  // this block sorts "before-first" order
-        const unsigned long long ka = key[lo], kb = key[hi];
-        const int ia = pg[lo], ib = pg[hi];
+        const bool up = (lo & size) == 0;
+        const unsigned long long ka = ckey[lo], kb = ckey[hi];
+        const int ia = cpg[lo], ib = cpg[hi];
         const bool a_first = ka > kb || (ka == kb && ia < ib);
         if (a_first != up) {
-          key[lo] = kb;
-          key[hi] = ka;
-          pg[lo] = ib;
-          pg[hi] = ia;
+          ckey[lo] = kb;
+          ckey[hi] = ka;
+          cpg[lo] = ib;
+          cpg[hi] = ia;
         }
       }
       __syncthreads();
     }
+  int* pg_r = cpg;          // pages in rank order (the first nc ranks)
+  const int n_rank = nc;
   // rank order: cumulative token counts; rank r* = first rank where the running total reaches k
-  const int per = (n_qp + 1023) / 1024;
+  const int per_r = (n_rank + 1023) / 1024;
   int loc = 0;
-  for (int q = 0; q < per; ++q) {
-    const int r = tid * per + q;
-    if (r < n_qp) loc += min(qpage, p0 - pg[r] * qpage);
+  for (int q = 0; q < per_r; ++q) {
+    const int r = tid * per_r + q;
+    if (r < n_rank) loc += min(qpage, p0 - pg_r[r] * qpage);
   }
   const int lane = tid & 31, warp = tid >> 5;
   int incl = loc;
@@ -175,14 +251,15 @@ __global__ void __launch_bounds__(1024) quest_pick_kernel(const int32_t* p0s, in
   }
   __syncthreads();
   int run = wsum[warp] + incl - loc;  // tokens in ranks before this thread's first rank
-  for (int q = 0; q < per && k > 0; ++q) {
-    const int r = tid * per + q;
-    if (r >= n_qp) break;
-    const int c = min(qpage, p0 - pg[r] * qpage);
-    if (run < k) take[pg[r]] = static_cast<int>(min(static_cast<long long>(c), k - run));
+  for (int q = 0; q < per_r && k > 0; ++q) {
+    const int r = tid * per_r + q;
+    if (r >= n_rank) break;
+    const int c = min(qpage, p0 - pg_r[r] * qpage);
+    if (run < k) take[pg_r[r]] = static_cast<int>(min(static_cast<long long>(c), k - run));
     run += c;
   }
   __syncthreads();
+  const int per = (n_qp + 1023) / 1024;
   // page order: positions p*qpage .. p*qpage + take[p) - 1, ascending
   loc = 0;
   for (int q = 0; q < per; ++q) {
@@ -231,7 +308,8 @@ cudaError_t launch_quest_select(const CacheView& c, const __nv_bfloat16* qmin, c
   if (e != cudaSuccess) return e;
   int npow = 1;
   while (npow < max_qpages) npow <<= 1;
-  const size_t smem = static_cast<size_t>(npow) * 12 + static_cast<size_t>(max_qpages) * 4 + 16;
+  const size_t smem = static_cast<size_t>(npow) * 8 + (static_cast<size_t>(max_qpages) + 1) * 4 +
+                      static_cast<size_t>(npow) * 12 + 16;
   static std::atomic<uint64_t> attr_mask{0};
   int dev = 0;
   if (func_attrs_needed(attr_mask, &dev)) {
