@@ -102,109 +102,6 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
       p.trace[(e) * 64 + (t)] = clock64();                                                      \
   } while (0)  // log2 units: p <= 2^8 before a forced max update
 
-// Merge `cnt` split partials of one unit (O rows [N][128] unnormalised, (m, l) per row, both in the
-// partial layout at src_o / src_ml with per-partial strides N*128 / N*2 floats) with bulk copies into
-// the idle ring buffers.  normalize: rows O/l -> dst_o (row stride 128);  else the merged partial
-// (O, m*, l) -> dst_o / dst_ml in the same partial layout (the next merge level reads it).
-// Called by the 256 softmax threads (t256); `bar` / `parity` is this use of the merge mbarrier.
-__device__ __forceinline__ void merge_partials(uint8_t* smem, uint32_t smem_cap, uint64_t* bar, uint32_t parity,
-                                               const float* src_o, const float* src_ml, int cnt, int N, int M,
-                                               bool normalize, float* dst_o, float* dst_ml, int t256,
-                                               unsigned long long* tr = nullptr) {
-  auto stamp = [&](int k) {  // dev trace (SA_TRACE): this CTA's phase slots
-    if (tr && t256 == 0) {
-      unsigned long long gt;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-      tr[k] = gt;
-    }
-  };
-  const uint32_t obytes = static_cast<uint32_t>(M) * 512u;
-  const uint32_t mlbytes = static_cast<uint32_t>(cnt) * N * 8u;
-  (void)smem_cap;
-  if (t256 == 0) {
-    fence_proxy_async();  // generic writes of the other CTAs (acquired by the caller) -> async-proxy reads
-    mbar_expect_tx(bar, cnt * obytes + mlbytes);
-    for (int s2 = 0; s2 < cnt; ++s2) bulk_load(smem + s2 * obytes, src_o + static_cast<size_t>(s2) * N * 128, obytes, bar);
-    bulk_load(smem + cnt * obytes, src_ml, mlbytes, bar);
-  }
-  mbar_wait(bar, parity);
-  stamp(12);
-  const float4* so = reinterpret_cast<const float4*>(smem);
-  float2* sml = reinterpret_cast<float2*>(smem + cnt * obytes);  // [partial][N] (m, l)
-  if (normalize) {
-    // every thread forms its own row's weights on the fly (broadcast (m, l) loads, MUFU exp2): no
-    // separate weights pass by a few threads and no barrier before the combine
-    stamp(13);
-    stamp(14);
-    for (int it = t256; it < M * 32; it += 256) {
-      const int row = it >> 5, c4 = it & 31;
-      float mstar = -INFINITY;
-      for (int s0 = 0; s0 < cnt; s0 += 8) {
-        float mm[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) mm[u] = s0 + u < cnt ? sml[(s0 + u) * N + row].x : -INFINITY;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) mstar = fmaxf(mstar, mm[u]);
-      }
-      float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-      float lsum = 0.f;
-      for (int s0 = 0; s0 < cnt; s0 += 8) {  // 8 independent smem loads per batch
-        float4 v[8];
-        float2 ml[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const bool ok = s0 + u < cnt;
-          v[u] = ok ? so[((s0 + u) * M + row) * 32 + c4] : make_float4(0.f, 0.f, 0.f, 0.f);
-          ml[u] = ok ? sml[(s0 + u) * N + row] : make_float2(-INFINITY, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const float w = ml[u].x == -INFINITY ? 0.f : fast_exp2(ml[u].x - mstar);
-          lsum = fmaf(ml[u].y, w, lsum);
-          float4& a = acc[u & 1];
-          a.x = fmaf(v[u].x, w, a.x);
-          a.y = fmaf(v[u].y, w, a.y);
-          a.z = fmaf(v[u].z, w, a.z);
-          a.w = fmaf(v[u].w, w, a.w);
-        }
-      }
-      const float inv = 1.f / lsum;
-      reinterpret_cast<float4*>(dst_o + static_cast<size_t>(row) * 128)[c4] =
-          make_float4((acc[0].x + acc[1].x) * inv, (acc[0].y + acc[1].y) * inv, (acc[0].z + acc[1].z) * inv,
-                      (acc[0].w + acc[1].w) * inv);
-    }
-  } else {  // merged partial for the next level: weights pass, then the combine
-    if (t256 < M) {
-      float mstar = -INFINITY;
-      for (int s2 = 0; s2 < cnt; ++s2) mstar = fmaxf(mstar, sml[s2 * N + t256].x);
-      float lsum = 0.f;
-      for (int s2 = 0; s2 < cnt; ++s2) {
-        const float2 v = sml[s2 * N + t256];
-        const float f = v.x == -INFINITY ? 0.f : fast_exp2(v.x - mstar);
-        lsum += v.y * f;
-        sml[s2 * N + t256].x = f;
-      }
-      dst_ml[t256 * 2] = mstar;
-      dst_ml[t256 * 2 + 1] = lsum;
-    }
-    named_bar_sync(1, 256);
-    for (int it = t256; it < M * 32; it += 256) {
-      const int row = it >> 5, c4 = it & 31;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int s2 = 0; s2 < cnt; ++s2) {
-        const float4 v = so[(s2 * M + row) * 32 + c4];
-        const float w = sml[s2 * N + row].x;
-        acc.x = fmaf(v.x, w, acc.x);
-        acc.y = fmaf(v.y, w, acc.y);
-        acc.z = fmaf(v.z, w, acc.z);
-        acc.w = fmaf(v.w, w, acc.w);
-      }
-      reinterpret_cast<float4*>(dst_o + static_cast<size_t>(row) * 128)[c4] = acc;
-    }
-  }
-  stamp(15);
-}
-
 // Rows [r_lo, r_hi) of one unit's output from its `cnt` split partials (O rows [N][128]
 // unnormalised and (m, l) per row at src_o / src_ml, per-partial strides N*128 / N*2 floats): the
 // partial rows and the (m, l) table are bulk-copied into the idle ring buffers, then every thread
