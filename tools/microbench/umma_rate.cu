@@ -18,7 +18,7 @@ __device__ __forceinline__ uint32_t idesc(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) | (8u << 24);
 }
 
-__global__ void k(int n, int iters, int nacc, unsigned long long* out) {
+__global__ void k(int n, int iters, int nacc, int a_tmem, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t{1023});
   __shared__ uint32_t tslot;
@@ -46,11 +46,18 @@ __global__ void k(int n, int iters, int nacc, unsigned long long* out) {
       for (int i = 0; i < iters; ++i) {
         const int kk = i & 3;
         const uint32_t acc = (i % nacc) * n;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm + acc),
-            "l"(desc(a + kk * 32)), "l"(desc(b + kk * 32)), "r"(idesc(n)), "r"(i >= nacc ? 1 : 0)
-            : "memory");
+        if (a_tmem)  // A from TMEM columns [384, 512) (garbage contents: timing only)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + acc),
+              "r"(tm + 384 + kk * 8), "l"(desc(b + kk * 32)), "r"(idesc(n)), "r"(i >= nacc ? 1 : 0)
+              : "memory");
+        else
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm + acc),
+              "l"(desc(a + kk * 32)), "l"(desc(b + kk * 32)), "r"(idesc(n)), "r"(i >= nacc ? 1 : 0)
+              : "memory");
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar))
                    : "memory");
@@ -69,18 +76,19 @@ int main() {
   cudaMalloc(&d, 148 * 8);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   unsigned long long h[148];
+  for (int at = 0; at < 2; ++at)
   for (int n : {16, 32, 64, 128, 256})
     for (int nacc : {1, 4}) {
-      if (n * nacc > 512) continue;
+      if (n * nacc > (at ? 384 : 512)) continue;
       const int iters = 256;
-      k<<<148, 128, 64 * 1024>>>(n, iters, nacc, d);
-      k<<<148, 128, 64 * 1024>>>(n, iters, nacc, d);
+      k<<<148, 128, 64 * 1024>>>(n, iters, nacc, at, d);
+      k<<<148, 128, 64 * 1024>>>(n, iters, nacc, at, d);
       cudaDeviceSynchronize();
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
       double sum = 0;
       for (int i = 0; i < 148; ++i) sum += h[i];
       const double ns = sum / 148 / iters;
-      printf("N=%3d nacc=%d: %.1f ns per MMA (M128 K16) -> %.2f TFLOP/s chip  err=%s\n", n, nacc, ns,
+      printf("A=%s N=%3d nacc=%d: %.1f ns per MMA (M128 K16) -> %.2f TFLOP/s chip  err=%s\n", at ? "tmem" : "smem", n, nacc, ns,
              2.0 * 128 * 16 * n * 148 / ns / 1e3, cudaGetErrorString(cudaGetLastError()));
     }
   return 0;
