@@ -303,14 +303,6 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   cp_async_commit();
   DraftWarp w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
-  // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45)
-  if (split == 0 && p.k_new && tid < 32) {
-    const int which = tid >> 4, ch = tid & 15;
-    const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128;
-    const int64_t row = cache_row(p.cache, seq, p.layer, g, new_pos);
-    __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + row * 128;
-    reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
-  }
   const int n_rounds = max(1, (n + kRoundRows - 1) / kRoundRows);
   const bool dbuf = kStream && n_rounds > 1;  // double-buffered rounds (streaming mode)
   auto issue_round = [&](int round, int buf) {  // every row of a later round (after the wait)
@@ -428,6 +420,16 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
         st_async_f32(mapa_shared(inbox_addr + (split * rstride + per + row) * 4, o), mstar, ob);
         st_async_f32(mapa_shared(inbox_addr + (split * rstride + per + 8 + row) * 4, o), lsum, ob);
       }
+  }
+  // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45), off the
+  // critical path: this launch reads the row from k_new / v_new; later steps of this layer gather it
+  // from the cache either before their own dependency wait (launches >= L back, complete) or after it
+  if (split == CS - 1 && p.k_new && tid < 32) {
+    const int which = tid >> 4, ch = tid & 15;
+    const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128;
+    const int64_t row = cache_row(p.cache, seq, p.layer, g, new_pos);
+    __nv_bfloat16* dst = (which ? p.cache.v : p.cache.k) + row * 128;
+    reinterpret_cast<uint4*>(dst)[ch] = __ldg(reinterpret_cast<const uint4*>(src) + ch);
   }
   // combine my slice once every sender's contribution has landed
   dtrace(p, 6);

@@ -84,3 +84,21 @@ if v_st:
     print(f"verify layer0 start -> last verify end {(max(v_en) - min(v_st)) / 1e3:.1f} us; last verify end -> first "
           f"draft start {(d_first - max(v_en)) / 1e3:.1f} us; drafts {(d_last - d_first) / 1e3:.1f} us; "
           f"total {(d_last - min(v_st)) / 1e3:.1f} us")
+
+# per split index: median (over launches) of each CTA's 'computed' and 'gathered' stamps relative to
+# its launch's median (which split is the straggler)
+CS = int(os.environ.get("CS_HINT", 12))
+rel_c, rel_g = {}, {}
+for j in range(gamma):
+    for l in range(2, L):
+        blk = dr[j, l]
+        live = np.nonzero(blk[:, 0] > 0)[0]
+        if len(live) < CS:
+            continue
+        med_c, med_g = np.median(blk[live, 3]), np.median(blk[live, 2])
+        for c in live:
+            s_ = int(c % CS)
+            rel_c.setdefault(s_, []).append((blk[c, 3] - med_c) / 1e3)
+            rel_g.setdefault(s_, []).append((blk[c, 2] - med_g) / 1e3)
+print("split: computed-vs-median (us) / gathered-vs-median (us)")
+print(" ".join(f"{s_}:{np.median(rel_c[s_]):+.2f}/{np.median(rel_g[s_]):+.2f}" for s_ in sorted(rel_c)))
