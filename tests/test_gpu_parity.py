@@ -820,3 +820,31 @@ def test_producer_feeds_verify_and_commit(cuda, ref):
     m.cache.commit_accepted(p0, a)
     assert m.cache.size() == p0 + a + 1 and m.cache.committed() == p0 + a + 1
     proj.close()
+
+
+def test_quest_all_bounds_tied(cuda, ref):
+    """Every page bound equal (constant keys): the candidate set is every page and the reference's
+    tie rule (lower page first) decides alone; a partial last page included."""
+    torch = cuda
+    Runner, _, selection_k = _lib()
+    from paper_2602_07223_b200 import Cache
+    L, Hkv, G, p0, page = 2, 2, 4, 1003, 8
+    Hq = Hkv * G
+    K = np.full((p0, L * Hkv, D), 0.5, np.float32)
+    V = normal_bf16(5, 2, (p0, L * Hkv, D))
+    kv = ref.kv(L, Hkv, D, p0 + 64)
+    for t in range(p0):
+        kv.append(K[t], V[t])
+    kv.enable_page_summaries(page)
+    c = Cache(L, Hkv, D, p0 + 64, page_size=128)
+    c.append(torch.from_numpy(K).cuda(), torch.from_numpy(V).cuda())
+    c.enable_page_summaries(page)
+    r = Runner(c, Hq, max_rows=5, max_prefix=p0, sparse_ratio=0.1, k_min=16)
+    r.set_batch([0], [p0])
+    q = normal_bf16(9, 1, (1, Hq, D))
+    r.select_quest(1, to_dev_bf16(q))
+    idx, cnt = r.selection(1, 1)
+    want = kv.select_quest(q[0], 1, p0, 0.1, 16)
+    assert cnt[0, 0] == selection_k(0.1, p0, 16) == len(want)
+    assert np.array_equal(idx[0, 0, : cnt[0, 0]], want)
+    c.close()
