@@ -668,13 +668,18 @@ __global__ void __launch_bounds__(384, 1)
     float* my_o = po + static_cast<size_t>(split) * N * 128;
     float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
     float* fin_l = red_all;  // [64] per-row sum of this CTA (both warpgroups, common max)
+    float* wgfac = red_all + 64;  // [2][64] per-row rescale of each warpgroup's O to the common max
     const bool has0 = ntiles_wg[0] > 0, has1 = ntiles_wg[1] > 0;
     if (wg == 0 && ts < N) {
       const float m0 = mref_all[ts], m1 = mref_all[64 + ts];
       const float ms = fmaxf(m0, m1);
+      const float f0 = (has0 && m0 != -INFINITY) ? fast_exp2(m0 - ms) : 0.f;
+      const float f1 = (has1 && m1 != -INFINITY) ? fast_exp2(m1 - ms) : 0.f;
+      wgfac[ts] = f0;
+      wgfac[64 + ts] = f1;
       float lsum = 0.f;
-      if (m0 != -INFINITY) lsum += ltot[ts] * fast_exp2(m0 - ms);
-      if (m1 != -INFINITY) lsum += ltot[64 + ts] * fast_exp2(m1 - ms);
+      if (m0 != -INFINITY) lsum += ltot[ts] * f0;
+      if (m1 != -INFINITY) lsum += ltot[64 + ts] * f1;
       fin_l[ts] = lsum;
       if (!single) {
         pml[(split * N + ts) * 2] = (has0 || has1) ? ms : -INFINITY;
@@ -702,11 +707,9 @@ __global__ void __launch_bounds__(384, 1)
       for (int j = 0; j < 16; ++j) {
         const int m = 16 * c16 + j;
         if (m >= M) break;
-        const float m0 = mref_all[m], m1 = mref_all[64 + m];
-        const float ms = fmaxf(m0, m1);
-        float acc = 0.f;
-        if (has0 && m0 != -INFINITY) acc += (o0[j] + t0[j]) * fast_exp2(m0 - ms);
-        if (has1 && m1 != -INFINITY) acc += (o1[j] + t1[j]) * fast_exp2(m1 - ms);
+        float acc = 0.f;  // factors precomputed per row (0 for an empty warpgroup / masked row)
+        if (has0) acc += (o0[j] + t0[j]) * wgfac[m];
+        if (has1) acc += (o1[j] + t1[j]) * wgfac[64 + m];
         if (single) out_unit[m * 128 + tk] = acc / fin_l[m];
         else my_o[m * 128 + tk] = acc;
       }
