@@ -77,6 +77,44 @@ __device__ __forceinline__ void warp_allreduce_max(float (&x)[N]) {
 #pragma unroll
   for (int m = 0; m < N; ++m) x[m] = ord2f(__reduce_max_sync(0xffffffffu, f2ord(x[m])));
 }
+// Sum N per-lane values over the 32 lanes with a transposing butterfly: each level halves the values
+// a lane keeps (the upper half when the level's lane bit is set) and adds its partner's other half,
+// so 31 shuffles do what N x 5 would.  Lane l ends with the sum of row l (N = 32), rows 2l, 2l+1
+// (N = 64, values past N are zero padding) or row l >> 1 (N = 16); they go to out[row].
+template <int N>
+__device__ __forceinline__ void warp_transpose_sum_store(const float (&x)[N], int lane, float* out) {
+  constexpr int NP = N <= 16 ? 16 : N <= 32 ? 32 : 64;
+  float v[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) v[i] = i < N ? x[i] : 0.f;
+  int cnt = NP;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    if (cnt > 1) {
+      const int half = cnt >> 1;
+      const bool upper = (lane & off) != 0;
+#pragma unroll
+      for (int i = 0; i < NP / 2; ++i) {
+        if (i < half) {
+          const float keep = upper ? v[half + i] : v[i];
+          const float send = upper ? v[i] : v[half + i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      cnt = half;
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+    }
+  }
+  if (NP == 32) {
+    out[lane] = v[0];
+  } else if (NP == 64) {
+    out[2 * lane] = v[0];
+    out[2 * lane + 1] = v[1];
+  } else if ((lane & 1) == 0) {
+    out[lane >> 1] = v[0];
+  }
+}
 template <int N>
 __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
 #pragma unroll
@@ -652,12 +690,7 @@ __global__ void __launch_bounds__(384, 1)
       tc_fence_after();
     }
     if (wg == 0 && ts == 0) SA_TSTAMP(4);
-    warp_allreduce_sum<N>(l);
-    if (lane == 0) {
-#pragma unroll
-      for (int m = 0; m < N; m += 4)
-        *reinterpret_cast<float4*>(&red[q4 * 64 + m]) = make_float4(l[m], l[m + 1], l[m + 2], l[m + 3]);
-    }
+    warp_transpose_sum_store<N>(l, lane, red + q4 * 64);  // per-warp row sums of l -> red[q4][row]
     named_bar_sync(bar_wg, 128);
     if (ts < N) ltot[wg * 64 + ts] = red[ts] + red[64 + ts] + red[128 + ts] + red[192 + ts];
     named_bar_sync(1, 256);  // both warpgroups' (mref, ltot) final
