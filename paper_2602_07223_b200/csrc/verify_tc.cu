@@ -282,6 +282,9 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sq = smem + C::kOffQ;
   for (int i = tid; i < ((p0 + R + (1 << p.cache.page_shift) - 1) >> p.cache.page_shift); i += C::kThreads)
     bt[i] = __ldg(p.cache.block_table + static_cast<int64_t>(seq) * p.cache.max_pages_per_seq + i);
+  __shared__ int s_go;  // this unit's merge generation before any arrival of this launch
+  if (tid == 0 && p.n_splits > 1)  // final value of the previous use (complete by the PDL transitivity)
+    asm volatile("ld.relaxed.gpu.s32 %0, [%1];" : "=r"(s_go) : "l"(p.counters + unit * 4 + 1) : "memory");
   if (tid < 64) {
     mref_all[tid] = -INFINITY;
     mref_all[64 + tid] = -INFINITY;
@@ -754,10 +757,13 @@ __global__ void __launch_bounds__(384, 1)
     } else {
       // Split merge by the last-arriving CTAs of the unit, each normalising a slice of the rows.
       // Arrival: one acq_rel atomic per CTA after the CTA-wide barrier (release of this CTA's
-      // partial stores).  The last arrival has acquired every partial; it releases `go`, which the
-      // other mergers (the few arrivals before it, still resident) acquire before reading partials.
+      // partial stores).  The last arrival has acquired every partial; it re-arms the arrival and
+      // chunk counters (every CTA of the unit has claimed its last chunk and arrived) and releases the
+      // next `go` generation, which the other mergers (the few arrivals before it, still resident)
+      // acquire before reading partials.  `go` only ever increases, so nobody waits for the
+      // mergers to finish before the unit's counters are ready for their next use.
       const int t256 = wg * 128 + ts;
-      int* ctr = p.counters + unit * 4;  // [0] arrivals, [1] go, [2] mergers done
+      int* ctr = p.counters + unit * 4;  // [0] arrivals, [1] go generation
       named_bar_sync(1, 256);
       if (t256 == 0) {
         SA_TSTAMP(5);
@@ -772,13 +778,17 @@ __global__ void __launch_bounds__(384, 1)
       if (arrival >= p.n_splits - nm) {
         const int part = arrival - (p.n_splits - nm);  // the last arrival takes the last slice
         if (arrival == p.n_splits - 1) {
-          if (t256 == 0 && nm > 1) asm volatile("st.release.gpu.s32 [%0], 1;" ::"l"(ctr + 1) : "memory");
+          if (t256 == 0) {
+            ctr[0] = 0;
+            p.chunk_ctr[unit] = 0;
+            if (nm > 1) asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(ctr + 1), "r"(s_go + 1) : "memory");
+          }
         } else {
           if (t256 == 0) {
             int go = 0;
             while (true) {
               asm volatile("ld.acquire.gpu.s32 %0, [%1];" : "=r"(go) : "l"(ctr + 1) : "memory");
-              if (go) break;
+              if (go != s_go) break;
               __nanosleep(64);
             }
           }
@@ -787,18 +797,7 @@ __global__ void __launch_bounds__(384, 1)
         const int per = (M + nm - 1) / nm;
         merge_rows(smem, merge_bar, po, pml, p.n_splits, N, min(M, part * per), min(M, (part + 1) * per), out_unit,
                    t256);
-        named_bar_sync(1, 256);
-        if (t256 == 0) {
-          SA_TSTAMP(9);
-          int done = nm - 1;
-          if (nm > 1) asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(done) : "l"(ctr + 2) : "memory");
-          if (done == nm - 1) {  // the last merger re-arms the unit's counters for the next use
-            ctr[0] = 0;
-            ctr[1] = 0;
-            ctr[2] = 0;
-            p.chunk_ctr[unit] = 0;
-          }
-        }
+        if (t256 == 0) SA_TSTAMP(9);
       }
     }
   }
