@@ -124,6 +124,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     L, Hq_full, Hkv_full, ctx, gamma, B_total, desc = WORKLOADS[args.workload]
+    if args.gamma:  # config 5: gamma sweep at the workload's context
+        gamma = args.gamma
     G = Hq_full // Hkv_full
     strong = args.workload in ("config3", "config4")
     if strong:  # fixed global batch: batch x KV-head shards, shard.plan
@@ -137,7 +139,8 @@ def run_ours(args, rank, world, local_rank):
     Hq = G * Hkv
     R = gamma + 1
     p0 = ctx
-    k = selection_k(RATIO, p0, K_MIN)
+    ratio, k_min = (0.0, args.k) if args.k else (RATIO, K_MIN)  # config 5: fixed budget k
+    k = selection_k(ratio, p0, k_min)
     scale = 1.0 / math.sqrt(D)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
@@ -157,7 +160,7 @@ def run_ours(args, rank, world, local_rank):
     if args.strategy == "quest":
         cache.enable_page_summaries(8)  # SelectorConfig::page_size default (selection.hpp:36)
     torch.cuda.synchronize()
-    runner = Runner(cache, Hq, max_rows=R, max_prefix=p0, max_batch=B, sparse_ratio=RATIO, k_min=K_MIN)
+    runner = Runner(cache, Hq, max_rows=R, max_prefix=p0, max_batch=B, sparse_ratio=ratio, k_min=k_min)
     runner.set_batch(list(range(B)), [p0] * B)
     comm = None
     if sh is not None and sh.needs_score_exchange:  # KV heads of a layer on several GPUs: NCCL exchange
@@ -333,7 +336,9 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
         "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn, post-RoPE K/V/Q, bf16)",
-        "config": {"workload": f"{args.workload}: {desc}", "global_batch": seqs_global, "seq_len": p0,
+        "config": {"workload": (f"config5 sweep point (gamma {gamma}, k {k}) on {args.workload}'s shape"
+                                if args.gamma or args.k else f"{args.workload}: {desc}"),
+                   "global_batch": seqs_global, "seq_len": p0,
                    "gamma": gamma, "k": k, "selection": f"{args.strategy}, per-layer", "layers": L,
                    "parallelism": (f"{world} GPUs: batch x KV-head shards ({B} seq x {Hkv} KV heads per GPU"
                                    + (f", NCCL per-layer score exchange over {sh.head_group} GPUs)" if comm else ")")
@@ -553,6 +558,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--gamma", type=int, default=0, help="override the workload's gamma (config 5 sweep)")
+    ap.add_argument("--k", type=int, default=0, help="fixed selection budget k instead of selection_k(0.07, p, 16)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the §8f next-row measurements")
