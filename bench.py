@@ -139,7 +139,7 @@ def run_ours(args, rank, world, local_rank):
     Hq = G * Hkv
     R = gamma + 1
     p0 = ctx
-    ratio, k_min = (0.0, args.k) if args.k else (RATIO, K_MIN)  # config 5: fixed budget k
+    ratio, k_min = (1e-9, args.k) if args.k else (RATIO, K_MIN)  # config 5: fixed budget k (ratio must be > 0)
     k = selection_k(ratio, p0, k_min)
     scale = 1.0 / math.sqrt(D)
     g = torch.Generator(device=dev)

@@ -848,3 +848,77 @@ def test_quest_all_bounds_tied(cuda, ref):
     assert cnt[0, 0] == selection_k(0.1, p0, 16) == len(want)
     assert np.array_equal(idx[0, 0, : cnt[0, 0]], want)
     c.close()
+
+
+# ------------------------------------------------------------------- full-size cases (BASELINE configs)
+
+def _bf16_round(x):
+    """float32 -> nearest-even bf16-representable float32 (the device stores these bits losslessly)."""
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    u = (u + (0x7FFF + ((u >> 16) & 1))) & 0xFFFF0000
+    return u.view(np.float32)
+
+
+FULL_CASES = [
+    # (Hkv, G, R, p0, k)   k = None: selection_k(0.07, p0, 16) as in configs 2-4
+    (8, 4, 5, 32768, None),   # config 2: one Llama-3.1-8B layer at 32K, gamma 4, k = 2294
+    (1, 8, 5, 131072, None),  # config 4 per-GPU shard: one KV head (+ its 8 q-heads) at 128K, k = 9175
+    (8, 4, 9, 32768, 4096),   # config 5 corner: gamma 8, k 4096
+    (8, 4, 3, 32768, 64),     # config 5 corner: gamma 2, k 64
+]
+
+
+@pytest.mark.parametrize("Hkv,G,R,p0,kfix", FULL_CASES)
+def test_full_size_verify_select_draft(cuda, ref, Hkv, G, R, p0, kfix):
+    """One layer at the BASELINE configs' full context: verify (outputs + fused Collect-2 scores),
+    per-layer top-k and the gamma draft steps over the selected rows, each against the reference's own
+    CPU code (oracle/_ref) on the same bf16-representable inputs (numpy Philox, not CounterRng, to keep
+    the 10^8-element generation fast; the parity contract is on identical inputs either way)."""
+    torch = cuda
+    Runner, _, selection_k = _lib()
+    from paper_2602_07223_b200 import Cache
+    rng = np.random.default_rng(p0 + 97 * R + Hkv)
+    Hq = Hkv * G
+    ratio, k_min = (1e-9, kfix) if kfix else (0.07, 16)
+    k = selection_k(ratio, p0, k_min)
+    K = _bf16_round(rng.standard_normal((p0, Hkv, D), np.float32))
+    V = _bf16_round(rng.standard_normal((p0, Hkv, D), np.float32))
+    cache = Cache(1, Hkv, D, p0 + R + 64, page_size=256)
+    for c0 in range(0, p0, 8192):
+        cache.append(torch.from_numpy(K[c0:c0 + 8192]).cuda(), torch.from_numpy(V[c0:c0 + 8192]).cuda())
+    kv = ref.kv(1, Hkv, D, p0 + R + 64)
+    for t in range(p0):
+        kv.append(K[t], V[t])
+    r = Runner(cache, Hq, max_rows=R, max_prefix=p0, sparse_ratio=ratio, k_min=k_min)
+    r.set_batch([0], [p0])
+    q = _bf16_round(rng.standard_normal((1, Hq, R, D), np.float32))
+    kn = _bf16_round(rng.standard_normal((1, R, Hkv, D), np.float32))
+    vn = _bf16_round(rng.standard_normal((1, R, Hkv, D), np.float32))
+    out = torch.zeros((1, Hq, R, D), dtype=torch.float32, device="cuda")
+    r.verify(0, to_dev_bf16(q), out, to_dev_bf16(kn), to_dev_bf16(vn), SCALE, score_row_mask=1 | (1 << (R - 1)))
+    idx, cnt = _gpu_select(r, 0, 0, 1, 2)
+    for t in range(R):
+        kv.append(kn[0, t], vn[0, t])
+    o_ref, l_ref = kv.verify_layer(0, Hq, q[0], p0, R, SCALE, threads=8)
+    got = out.cpu().numpy()[0]
+    assert rel_err_rows(got, o_ref) < 2e-4, rel_err_rows(got, o_ref)
+    assert rel_err_elem(got, o_ref) < 2e-3
+    # selection: |T| = k, bit-exact outside the 2e-3 tie band (north star)
+    ref_scores = ref.score_columns(l_ref, list(range(1, R + 1)), [1, R])
+    assert cnt[0, 0] == k
+    sel = idx[0, 0, :k].astype(np.int64)
+    check_selection(sel, ref_scores, k)
+    # draft chain over the GPU's selection (drafts read T; parity of attention given T)
+    kv.truncate(p0)
+    cache.set_size(p0)
+    for step in range(1, R):
+        qd = _bf16_round(rng.standard_normal((1, Hq, D), np.float32))
+        kd = _bf16_round(rng.standard_normal((1, Hkv, D), np.float32))
+        vd = _bf16_round(rng.standard_normal((1, Hkv, D), np.float32))
+        o = torch.zeros((1, Hq, D), dtype=torch.float32, device="cuda")
+        r.draft(0, step, to_dev_bf16(qd), o, to_dev_bf16(kd), to_dev_bf16(vd), mode=0, scale=SCALE)
+        kv.append(kd[0], vd[0])
+        o_ref = kv.draft_layer(0, Hq, qd[0], [sel], p0, step, SCALE, threads=8)
+        got = o.cpu().numpy()[0]
+        assert rel_err_rows(got, o_ref) < 2e-4, (step, rel_err_rows(got, o_ref))
+        assert rel_err_elem(got, o_ref) < 2e-3
