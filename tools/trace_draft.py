@@ -24,7 +24,8 @@ cache = Cache(L, Hkv, D, p0 + R + 64, page_size=256)
 for s in range(0, p0, 2048):
     kk = torch.randn((2048, L * Hkv, D), device="cuda").to(torch.bfloat16)
     cache.append(kk, kk)
-r = Runner(cache, Hq, max_rows=R, max_prefix=p0)
+KFIX = int(os.environ.get("K_FIX", 0))  # fixed budget k (config 5 sweep points)
+r = Runner(cache, Hq, max_rows=R, max_prefix=p0, **({"sparse_ratio": 1e-9, "k_min": KFIX} if KFIX else {}))
 r.set_batch([0], [p0])
 
 
