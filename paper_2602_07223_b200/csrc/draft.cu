@@ -16,6 +16,8 @@
 // produces in the previous layer) are read after it.
 #include "attn_core.cuh"
 #include <algorithm>
+#include <map>
+#include <mutex>
 
 #include "internal.h"
 
@@ -151,7 +153,8 @@ struct DCfg {
   static constexpr int kPartFloats = 8 * 128 + 16;  // CTA partial: O[8 rows][128], m[8], l[8]
   static constexpr int kOffPart = 2 * kMaxTiles * kTileBytes;
   static constexpr int kOffRow = kOffPart + kPartFloats * 4;      // int64 source rows of the round
-  static constexpr int kOffRecv = kOffRow + kMaxTiles * kTile * 8;  // merge inbox [kMaxCS][kRecvFloats]
+  static constexpr int kRowRounds = 3;  // rounds whose source rows are resolved before the dependency wait
+  static constexpr int kOffRecv = kOffRow + kRowRounds * kMaxTiles * kTile * 8;  // merge inbox [kMaxCS][kRecvFloats]
   static constexpr int kRecvFloats = 8 * 128 / 1 + 16;            // worst case (CS = 1) slice + (m, l)
   static constexpr int kRecvPerSender = 64 + 16;                  // CS = 16, G = 8: 64-float slice + (m, l)
   static constexpr int kRecvBytes = kMaxCS * kRecvPerSender * 4 > kRecvFloats * 4 ? kMaxCS * kRecvPerSender * 4
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   int64_t* src_row = reinterpret_cast<int64_t*>(smem + DCfg::kOffRow);  // -1: new row (k_new), -2: zero fill
   // pre: true -> rows that exist before this launch (gathered ahead of the dependency wait)
   auto is_pre = [&](int v) { return v < k || (v == new_v ? !p.k_new : old_tail_ready); };
-  auto resolve = [&](int r0, int rows, bool pre_pass) {
+  auto resolve = [&](int r0, int rows, bool pre_pass, int64_t* src_row) {
     for (int r = tid; r < rows; r += nthr) {
       const int v = v_begin + r0 + r;
       if (v >= v_end) {  // zero fill: known before the dependency
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
       src_row[r] = (p.k_new && pos == new_pos) ? -1 : cache_row(p.cache, seq, p.layer, g, pos);
     }
   };
-  auto gather = [&](int r0, int rows, bool pre_pass, int buf = 0) {
+  auto gather = [&](int r0, int rows, bool pre_pass, int buf, const int64_t* src_row) {
     uint8_t* const base = buf ? smem + DCfg::kOffBuf1 : smem;
     for (int i = tid; i < rows * 16; i += nthr) {
       const int r = i >> 4, ch = i & 15;
@@ -275,12 +278,32 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   };
 
   constexpr int kRoundRows = DCfg::kMaxTiles * DCfg::kTile;
+  const int n_rounds = max(1, (n + kRoundRows - 1) / kRoundRows);
+  // two-CTA-per-SM mode with several rounds (a few units, large k): every round's pre-existing source
+  // rows are resolved before the dependency wait (own src_row area per round) and the rows of rounds
+  // >= 1 are prefetched into L2, so a later round costs one L2 gather instead of index + block-table
+  // + HBM round trips after the previous round's compute
+  const bool early = !kStream && n_rounds > 1 && n_rounds <= DCfg::kRowRounds;
+  auto round_src = [&](int round) { return early ? src_row + round * kRoundRows : src_row; };
+  auto round_pad = [&](int round) { return (min(kRoundRows, n - round * kRoundRows) + 15) & ~15; };
   {  // round 0, pre-existing rows: independent of the previous kernel
     const int rows0 = (min(kRoundRows, n) + 15) & ~15;
-    resolve(0, rows0, true);
+    resolve(0, rows0, true, src_row);
+    if (early)
+      for (int rd = 1; rd < n_rounds; ++rd) resolve(rd * kRoundRows, round_pad(rd), true, round_src(rd));
     __syncthreads();
-    gather(0, rows0, true);
+    gather(0, rows0, true, 0, src_row);
     cp_async_commit();
+    if (early)
+      for (int rd = 1; rd < n_rounds; ++rd) {
+        const int64_t* sr = round_src(rd);
+        const int rp = round_pad(rd);
+        for (int i = tid; i < 2 * rp; i += nthr) {
+          const int64_t row = sr[i >> 1];
+          if (row >= 0 && is_pre(v_begin + rd * kRoundRows + (i >> 1)))
+            prefetch_l2_bulk(((i & 1) ? p.cache.v : p.cache.k) + row * 128, 256);
+        }
+      }
   }
   pdl_wait();  // previous layer complete: q and this step's new row are valid
   pdl_launch_dependents();
@@ -291,9 +314,9 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   const int rows0_pad = (min(kRoundRows, n) + 15) & ~15;
   if (!old_tail_ready) {
     __syncthreads();  // src_row of the pre pass consumed by every thread
-    resolve(0, rows0_pad, false);
+    resolve(0, rows0_pad, false, src_row);
     __syncthreads();
-    gather(0, rows0_pad, false);
+    gather(0, rows0_pad, false, 0, src_row);
   } else if (p.k_new && warp == nwarps - 1 && new_v >= v_begin && new_v < v_begin + rows0_pad && new_v < v_end) {
     const int r = new_v - v_begin, ch = lane & 15;
     const uint32_t off = (r >> 6) * DCfg::kTileBytes + swz(r & 63, ch, DCfg::kHalf);
@@ -303,17 +326,17 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   cp_async_commit();
   DraftWarp w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
-  const int n_rounds = max(1, (n + kRoundRows - 1) / kRoundRows);
   const bool dbuf = kStream && n_rounds > 1;  // double-buffered rounds (streaming mode)
   auto issue_round = [&](int round, int buf) {  // every row of a later round (after the wait)
     const int rr0 = round * kRoundRows;
     const int rp = (min(kRoundRows, n - rr0) + 15) & ~15;
     __syncthreads();  // buffer `buf` and src_row free
-    resolve(rr0, rp, true);
-    resolve(rr0, rp, false);
+    int64_t* sr = round_src(round);
+    if (!early) resolve(rr0, rp, true, sr);
+    resolve(rr0, rp, false, sr);
     __syncthreads();
-    gather(rr0, rp, true, buf);
-    gather(rr0, rp, false, buf);
+    gather(rr0, rp, true, buf, sr);
+    gather(rr0, rp, false, buf, sr);
     cp_async_commit();
   };
   if (dbuf) issue_round(1, 1);
@@ -461,7 +484,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   dtrace(p, 4);
 }
 
-cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
+static cudaError_t draft_set_attrs() {
   static std::atomic<uint64_t> attr_mask{0};
   int dev = 0;
   if (func_attrs_needed(attr_mask, &dev)) {
@@ -475,6 +498,46 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     func_attrs_done(attr_mask, dev);
   }
+  return cudaSuccess;
+}
+
+// How many clusters of `cs` CTAs (full 8-warp blocks) the device runs at once in the given mode:
+// clusters must fit inside one GPC, so on 148 SMs e.g. eight 16-CTA clusters of the one-CTA-per-SM
+// streaming mode do NOT all fit and a second wave would follow.  Cached per (device, mode, cs).
+int draft_max_active_clusters(int stream, int cs) {
+  static std::mutex mu;
+  static std::map<int, int> memo;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int key = (dev * 2 + (stream ? 1 : 0)) * 64 + cs;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  int n = 0;
+  if (draft_set_attrs() == cudaSuccess) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs, 1, 1);
+    cfg.blockDim = dim3(DCfg::kMaxThreads);
+    cfg.dynamicSmemBytes = stream ? DCfg::kSmemStream : DCfg::kSmem;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cs;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    if ((stream ? cudaOccupancyMaxActiveClusters(&n, draft_kernel<true>, &cfg)
+                : cudaOccupancyMaxActiveClusters(&n, draft_kernel<false>, &cfg)) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+  }
+  memo[key] = n;
+  return n;
+}
+
+cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
+  if (cudaError_t e = draft_set_attrs()) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);
   // one warp per 16-row sub-block of the CTA's chunk (<= 9 warps, two CTAs per SM)

@@ -176,6 +176,7 @@ cudaError_t launch_verify_tc(const VerifyParams& p, const CUtensorMap& tk, const
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s);
 int draft_max_splits();
 int draft_round_rows();
+int draft_max_active_clusters(int stream, int cs);
 cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
 size_t verify_smem_bytes(int MT);
 int verify_tc_merge_capacity(int M);  // bytes of smem a merge may fill (tcgen05 verify, rows M)

@@ -464,15 +464,58 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
         break;
       }
     p.stream = 0;
-    if (cs < 0 || units * cs > 2 * r->num_sms) {
+    static const int multi_round_max = [] {  // dev knob: rounds allowed in the two-CTA-per-SM mode
+      const char* e = std::getenv("SA_DRAFT_MULTI_ROUNDS");
+      return e ? std::atoi(e) : 3;
+    }();
+    // a few units with a large budget (config 5 k = 4096, config 4's per-GPU shard): several rounds in
+    // the two-CTA-per-SM mode, round 0 gathered before the dependency wait and later rounds reusing its
+    // buffer.  Fewest rounds first, with a penalty when two successive launches' clusters cannot
+    // co-reside (the next launch's pre-wait gathers would then start late); the one-CTA-per-SM
+    // streaming mode would need two waves of 16-CTA clusters here.
+    int multi_cs = -1;
+    double multi_score = 0.0;
+    for (int c : {16, 12, 8}) {
+      if (cs > 0) break;  // one round fits: the single-round rule above
+      const int act = sa::draft_max_active_clusters(0, c);
+      const int64_t rounds = ((m + c - 1) / c + round_rows - 1) / round_rows;
+      if (act < units || rounds > multi_round_max) continue;
+      const double score = static_cast<double>(rounds) + (2 * units > act ? 1.5 : 0.0);
+      if (multi_cs < 0 || score < multi_score) {
+        multi_cs = c;
+        multi_score = score;
+      }
+    }
+    if (cs < 0 && multi_cs > 0) {
+      cs = multi_cs;
+    } else if (cs < 0 || units * cs > 2 * r->num_sms) {
+      // cost ~ waves x (rows per CTA + a fixed per-CTA overhead of one 64-row tile), where the wave
+      // count comes from the occupancy API: 16-CTA clusters of one CTA per SM do not all fit on
+      // 148 SMs (a cluster lives inside one GPC), and a second wave costs a whole launch
       p.stream = 1;
-      const int64_t fit = std::max<int64_t>(1, r->num_sms / units);
       cs = 1;
-      for (int c : {2, 4, 8, 12, 16})
-        if (c <= fit && (m + c - 1) / c >= round_rows) cs = c;  // keep >= one full round per CTA
+      int64_t best = -1;
+      for (int c : {1, 2, 4, 8, 12, 16}) {
+        const int act = sa::draft_max_active_clusters(1, c);
+        if (act <= 0) continue;
+        const int64_t waves = (units + act - 1) / act;
+        const int64_t cost = waves * ((m + c - 1) / c + 64);
+        if (best < 0 || cost < best) {
+          best = cost;
+          cs = c;
+        }
+      }
     }
     p.n_splits = cs;
     p.chunk = static_cast<int>(((m + cs - 1) / cs + 15) / 16 * 16);
+    static const bool dbg = std::getenv("SA_DRAFT_DEBUG") != nullptr;
+    if (dbg) {
+      std::fprintf(stderr, "draft: units %lld m %lld -> stream %d cs %d chunk %d | active clusters (stream/non):",
+                   static_cast<long long>(units), static_cast<long long>(m), p.stream, cs, p.chunk);
+      for (int c : {1, 2, 4, 8, 12, 16})
+        std::fprintf(stderr, " %d:%d/%d", c, sa::draft_max_active_clusters(1, c), sa::draft_max_active_clusters(0, c));
+      std::fprintf(stderr, "\n");
+    }
   }
   p.part_o = r->d_po;
   p.part_ml = r->d_pml;
