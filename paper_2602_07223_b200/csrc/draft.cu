@@ -164,7 +164,9 @@ struct DCfg {
   // streaming mode (chunks of several rounds): a second K/V buffer after everything else, so round
   // r+1 is gathered while round r is computed (one CTA per SM)
   static constexpr int kOffBuf1 = (kOffBar + 16 + 1023) / 1024 * 1024;
-  static constexpr int kSmemStream = kOffBuf1 + 2 * kMaxTiles * kTileBytes + 1024;
+  static constexpr int kOffBt = kOffBuf1 + 2 * kMaxTiles * kTileBytes;  // streaming: block table in smem
+  static constexpr int kBtMax = 2048;
+  static constexpr int kSmemStream = kOffBt + kBtMax * 4 + 1024;
   static_assert(kMaxWarps * 8 * 132 * 4 <= kOffPart, "warp partials must fit in the tile buffers");
   static_assert(kMaxTiles * kTile * 8 >= kMaxWarps * 16 * 4, "warp (m, l) table fits the row-source area");
   static_assert(kSmem <= 113 * 1024, "two CTAs per SM: the next PDL launch co-resides");
@@ -324,6 +326,20 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
     cp_async_16(smem + (lane < 16 ? 0 : DCfg::kOffV) + off, src, 16);
   }
   cp_async_commit();
+  // streaming mode: the sequence's block table staged in shared memory and each thread's T entry of
+  // the next round loaded one round ahead, so resolving a round's source rows costs no dependent
+  // global round trip between two rounds' compute
+  int* bt_s = reinterpret_cast<int*>(smem + DCfg::kOffBt);
+  const int n_pages_seq = ((p0 + j) >> p.cache.page_shift) + 1;
+  const bool bt_smem = kStream && n_pages_seq <= DCfg::kBtMax;
+  int tq = 0;
+  if (kStream) {
+    if (bt_smem)
+      for (int i = tid; i < n_pages_seq; i += nthr)
+        bt_s[i] = __ldg(p.cache.block_table + static_cast<int64_t>(seq) * p.cache.max_pages_per_seq + i);
+    const int v2 = v_begin + kRoundRows + tid;
+    if (tid < kRoundRows && v2 < min(v_end, k)) tq = __ldg(T + v2);
+  }
   DraftWarp w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
   const bool dbuf = kStream && n_rounds > 1;  // double-buffered rounds (streaming mode)
@@ -332,8 +348,30 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
     const int rp = (min(kRoundRows, n - rr0) + 15) & ~15;
     __syncthreads();  // buffer `buf` and src_row free
     int64_t* sr = round_src(round);
-    if (!early) resolve(rr0, rp, true, sr);
-    resolve(rr0, rp, false, sr);
+    if (kStream) {
+      if (tid < rp) {
+        const int v = v_begin + rr0 + tid;
+        int64_t row = -2;
+        if (v < v_end) {
+          const int pos = v < k ? tq : p0 + (v - k);
+          if (p.k_new && pos == new_pos) {
+            row = -1;
+          } else {
+            const int page = bt_smem ? bt_s[pos >> p.cache.page_shift]
+                                     : __ldg(p.cache.block_table + static_cast<int64_t>(seq) * p.cache.max_pages_per_seq +
+                                             (pos >> p.cache.page_shift));
+            row = ((((int64_t)p.layer * p.cache.num_pages + page) * p.cache.n_kv_heads + g) << p.cache.page_shift) +
+                  (pos & ((1 << p.cache.page_shift) - 1));
+          }
+        }
+        sr[tid] = row;
+      }
+      const int v2 = v_begin + rr0 + kRoundRows + tid;  // the next round's T entry, one round ahead
+      tq = (tid < kRoundRows && v2 < min(v_end, k)) ? __ldg(T + v2) : 0;
+    } else {
+      if (!early) resolve(rr0, rp, true, sr);
+      resolve(rr0, rp, false, sr);
+    }
     __syncthreads();
     gather(rr0, rp, true, buf, sr);
     gather(rr0, rp, false, buf, sr);
