@@ -458,8 +458,19 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
     const int64_t m = r->k_cap + a->step;
     const int round_rows = sa::draft_round_rows();
     int cs = -1;
+    // at least 4 CTAs per unit while two launches still co-reside at two CTAs per SM: shorter
+    // per-CTA chains beat the larger merge (k = 64: 4.27 -> 3.25 us, k = 256: 3.68 -> 3.32 us per
+    // launch with CS 1/2 -> 4; CS 8-12 is slower again)
+    static const int min_cs_env = [] {  // dev knob
+      const char* e = std::getenv("SA_DRAFT_MIN_CS");
+      return e ? std::atoi(e) : 0;
+    }();
+    int min_cs = 1;
+    for (int c : {2, 4})
+      if (units * c <= r->num_sms) min_cs = c;
+    if (min_cs_env) min_cs = min_cs_env;
     for (int c : {1, 2, 4, 8, 12, 16})
-      if ((m + c - 1) / c <= round_rows) {
+      if (c >= min_cs && (m + c - 1) / c <= round_rows) {
         cs = c;
         break;
       }
