@@ -37,6 +37,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "internal.h"
 
@@ -437,6 +438,227 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Decode-size producer (<= 8 tokens): one fused launch on mma.sync instead of tcgen05.
+//
+// Measured on this chip: a tcgen05.mma instruction (M = 128, K = 16) costs ~78 ns whatever N is, so
+// with 2 x 8 token columns the swap-AB projection is bound by the instruction count (~0.39 us per
+// 16 KB weight tile) and needs split-K across CTAs plus a separate prepare kernel.  For <= 8 tokens
+// the warp-level m16n8k16 MMA (A = 16 weight rows x 16 of d_model, B = the 8 token columns as bf16
+// hi / lo planes) does the same fp32-accurate product at a fraction of the tensor time, and every
+// CTA owns whole output rows over the full d_model, so there is no split-K reduction and no second
+// launch:
+//   * CTA c owns RoPE pairs [c*P/grid, (c+1)*P/grid) (P = n_out / 2; both rows of a pair, so the
+//     rotation happens in registers), in 16-row tiles: rows 0-7 = first rows of 8 pairs, 8-15 = their
+//     partners — exactly the C-fragment rows gid / gid+8 of one lane;
+//   * warp w owns the 32-wide k-blocks w, w+16, ... of d_model; the 16-byte chunk a lane loads
+//     (8 consecutive k of one weight row, straight from the packed SWIZZLE_128B tiles) IS its A
+//     fragment of two k16 steps once k is permuted inside the block (A and B use the same
+//     permutation: logical k 2t4+e / 2t4+8+e of step s = physical 8t4+4s+e / 8t4+4s+2+e);
+//   * x * gain is staged once per CTA in shared memory (fp32, padded rows), and 1/rms (double sum of
+//     squares, like qkv_prepare) comes from the same pass; B fragments are split to hi / lo per block;
+//   * the 16 warps' partial C fragments are summed in warp order through shared memory
+//     (deterministic), then the tile's warp applies 1/rms and RoPE (fp32, angle reduced in double as in
+//     qkv_prepare) and stores bf16.
+// Pre-dependency: the CTA's weight rows are prefetched into L2 (they depend on nothing).
+// (a, b) -> three bf16 planes with a ~= hi + mid + lo to ~2^-24 relative (each residual is exact in fp32)
+__device__ __forceinline__ void split3_bf16(float a, float b, uint32_t& hi, uint32_t& mid, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  const float2 hf = __bfloat1622float2(h);
+  const float ra = a - hf.x, rb = b - hf.y;
+  const __nv_bfloat162 m = __floats2bfloat162_rn(ra, rb);
+  const float2 mf = __bfloat1622float2(m);
+  const __nv_bfloat162 l = __floats2bfloat162_rn(ra - mf.x, rb - mf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  mid = *reinterpret_cast<const uint32_t*>(&m);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+constexpr int kGemvThreads = 512;
+constexpr int kGemvWarps = kGemvThreads / 32;
+constexpr int kGemvTiles = 3;  // 16-row tiles per CTA (24 RoPE pairs; Llama-3.1-8B: 3072 pairs / 148 CTAs)
+
+__global__ void __launch_bounds__(kGemvThreads, 1) qkv_gemv(QkvParams p) {
+  extern __shared__ __align__(16) float gsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gid = lane >> 2, t4 = lane & 3;
+  const int D = p.nkb * 64, T = p.n_tok;
+  const int xs_ld = D + 4;                       // padded fp32 row (conflict-free LDS.128 per gid)
+  float* xs = gsm;                               // [T][xs_ld] x * gain
+  float* red = xs + T * xs_ld;                   // [kGemvWarps][kGemvTiles][32][4] partial C fragments
+  __shared__ double ssq[kGemvWarps][8];
+  const int P = p.n_out / 2, grid = gridDim.x;
+  const int pr0 = static_cast<int>(static_cast<int64_t>(blockIdx.x) * P / grid);
+  const int pr1 = static_cast<int>(static_cast<int64_t>(blockIdx.x + 1) * P / grid);
+  // physical weight row (0..n_out) of tile row rr (0..15) of tile t; -1 if past the CTA's pairs
+  auto row_of = [&](int t, int rr) {
+    const int pp = pr0 + t * 8 + (rr & 7);
+    if (pp >= pr1) return -1;
+    const int h = pp >> 6, j = pp & 63;
+    const int first = p.style == 0 ? j : 2 * j, second = p.style == 0 ? j + 64 : 2 * j + 1;
+    return h * 128 + (rr < 8 ? first : second);
+  };
+  const size_t layer_base = static_cast<size_t>(p.layer) * p.heads * p.nkb;
+  // address of the 16-byte chunk holding k = 8c .. 8c+7 of weight row `row` in the packed tiles
+  auto wchunk = [&](int row, int c) {
+    const int h = row >> 7, rr = row & 127, kt = c >> 3;
+    return reinterpret_cast<const uint4*>(p.wpack + ((layer_base + static_cast<size_t>(h) * p.nkb + kt) * 128 + rr) * 64) +
+           ((c & 7) ^ (rr & 7));
+  };
+  float acc[kGemvTiles][4];
+#pragma unroll
+  for (int t = 0; t < kGemvTiles; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+  int rowA[kGemvTiles], rowB[kGemvTiles];
+#pragma unroll
+  for (int t = 0; t < kGemvTiles; ++t) {
+    rowA[t] = row_of(t, gid);
+    rowB[t] = row_of(t, gid + 8);
+  }
+  const int nblk = D / 32;
+  uint4 wa[2][kGemvTiles], wb[2][kGemvTiles];
+  auto load_w = [&](const int buf, int blk) {
+    const int c = blk * 4 + t4;
+#pragma unroll
+    for (int t = 0; t < kGemvTiles; ++t) {
+      (buf ? wa[1] : wa[0])[t] = rowA[t] >= 0 ? __ldcs(wchunk(rowA[t], c)) : make_uint4(0, 0, 0, 0);
+      (buf ? wb[1] : wb[0])[t] = rowB[t] >= 0 ? __ldcs(wchunk(rowB[t], c)) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  // pre-dependency (weights depend on nothing): the warp's first two k-blocks into registers.  (An L2
+  // prefetch of the rest, one 128-byte bulk prefetch per row and k tile, measured slower: 20.9 vs
+  // 16.4 us per layer; dev bit 1 turns it on.)
+  if (warp < nblk) load_w(0, warp);
+  if (warp + kGemvWarps < nblk) load_w(1, warp + kGemvWarps);
+  if (p.dev & 1)
+    for (int i = tid; i < kGemvTiles * 16 * p.nkb; i += kGemvThreads) {
+      const int t = i / (16 * p.nkb), rr = (i / p.nkb) & 15, kt = i % p.nkb;
+      const int row = row_of(t, rr);
+      if (row >= 0 && kt >= 4)
+        bulk_prefetch_l2(p.wpack + ((layer_base + static_cast<size_t>(row >> 7) * p.nkb + kt) * 128 + (row & 127)) * 64,
+                         128);
+    }
+  pdl_wait();  // x and positions are the previous kernel's outputs
+  pdl_launch_dependents();
+  // each warp stages x * gain for its own k-blocks (no CTA barrier before the main loop) and keeps
+  // per-lane partial sums of squares (double, like qkv_prepare) for the epilogue's 1/rms
+  const float* g = p.gain + static_cast<size_t>(p.layer) * D;
+  double ss[2] = {0.0, 0.0};  // tokens lane/8 and lane/8 + 4
+  {
+    const int kq = 4 * (lane & 7), t0 = lane >> 3;
+    for (int blk = warp; blk < nblk; blk += kGemvWarps) {
+      const int k = blk * 32 + kq;
+      const float4 gg = __ldg(reinterpret_cast<const float4*>(g + k));
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int t = t0 + 4 * e;
+        if (t < T) {
+          const float4 xv = __ldg(reinterpret_cast<const float4*>(p.x + static_cast<size_t>(t) * D + k));
+          ss[e] += static_cast<double>(xv.x) * xv.x + static_cast<double>(xv.y) * xv.y +
+                   static_cast<double>(xv.z) * xv.z + static_cast<double>(xv.w) * xv.w;
+          *reinterpret_cast<float4*>(xs + t * xs_ld + k) = make_float4(xv.x * gg.x, xv.y * gg.y, xv.z * gg.z, xv.w * gg.w);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  auto compute = [&](const uint4 (&wA)[kGemvTiles], const uint4 (&wB)[kGemvTiles], int blk) {
+    // B fragments of token gid at k = 32 blk + 8 t4 .. + 7 (hi / lo planes)
+    const float* xr = xs + gid * xs_ld + blk * 32 + 8 * t4;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 x0 = gid < T ? *reinterpret_cast<const float4*>(xr) : z4;
+    const float4 x1 = gid < T ? *reinterpret_cast<const float4*>(xr + 4) : z4;
+    // three bf16 planes (hi + mid + lo represent x * gain to ~2^-24): the product is as accurate as
+    // an fp32 one, so outputs round like the exact value except within fp32 noise of a tie
+    uint32_t hi[4], mid[4], lo[4];
+    split3_bf16(x0.x, x0.y, hi[0], mid[0], lo[0]);
+    split3_bf16(x0.z, x0.w, hi[1], mid[1], lo[1]);
+    split3_bf16(x1.x, x1.y, hi[2], mid[2], lo[2]);
+    split3_bf16(x1.z, x1.w, hi[3], mid[3], lo[3]);
+#pragma unroll
+    for (int t = 0; t < kGemvTiles; ++t) {
+      const uint32_t a0[4] = {wA[t].x, wB[t].x, wA[t].y, wB[t].y}, a1[4] = {wA[t].z, wB[t].z, wA[t].w, wB[t].w};
+      mma_bf16(acc[t], a0, lo[0], lo[1]);
+      mma_bf16(acc[t], a1, lo[2], lo[3]);
+      mma_bf16(acc[t], a0, mid[0], mid[1]);
+      mma_bf16(acc[t], a1, mid[2], mid[3]);
+      mma_bf16(acc[t], a0, hi[0], hi[1]);
+      mma_bf16(acc[t], a1, hi[2], hi[3]);
+    }
+  };
+  // two register buffers with compile-time indices (unrolled by two blocks); blocks 0 and 1 of the
+  // warp were loaded before the dependency wait
+  for (int blk = warp; blk < nblk; blk += 2 * kGemvWarps) {
+    const bool has1 = blk + kGemvWarps < nblk;
+    compute(wa[0], wb[0], blk);
+    if (blk + 2 * kGemvWarps < nblk) load_w(0, blk + 2 * kGemvWarps);
+    if (has1) {
+      compute(wa[1], wb[1], blk + kGemvWarps);
+      if (blk + 3 * kGemvWarps < nblk) load_w(1, blk + 3 * kGemvWarps);
+    }
+  }
+  // per-token sums of squares: lanes of the same token (lane / 8) reduce, then warps via shared memory
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+#pragma unroll
+    for (int off = 4; off > 0; off >>= 1) ss[e] += __shfl_xor_sync(0xffffffffu, ss[e], off);
+    if ((lane & 7) == 0) ssq[warp][(lane >> 3) + 4 * e] = ss[e];
+  }
+#pragma unroll
+  for (int t = 0; t < kGemvTiles; ++t)
+    *reinterpret_cast<float4*>(red + ((warp * kGemvTiles + t) * 32 + lane) * 4) =
+        make_float4(acc[t][0], acc[t][1], acc[t][2], acc[t][3]);
+  __syncthreads();
+  if (warp >= kGemvTiles) return;
+  // epilogue: warp t finishes tile t — sum the warps' partials in order, 1/rms, RoPE, bf16 stores
+  const int t = warp;
+  if (rowA[t] < 0) return;
+  float c[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int w = 0; w < kGemvWarps; ++w) {
+    const float4 v = *reinterpret_cast<const float4*>(red + ((w * kGemvTiles + t) * 32 + lane) * 4);
+    c[0] += v.x;
+    c[1] += v.y;
+    c[2] += v.z;
+    c[3] += v.w;
+  }
+  const int head = rowA[t] >> 7, dA = rowA[t] & 127, dB = rowB[t] & 127;
+  const int kind_q = p.Hq, kind_k = p.Hq + p.Hkv;
+  const int kind = head < kind_q ? 0 : head < kind_k ? 1 : 2;
+  const int j = p.style == 0 ? dA : dA >> 1;  // RoPE pair of this row pair
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int tok = 2 * t4 + e;
+    if (tok >= T) break;
+    double s2 = 0.0;  // 1/rms of this token (warp-order sum: deterministic)
+    for (int w = 0; w < kGemvWarps; ++w) s2 += ssq[w][tok];
+    const float rs = static_cast<float>(1.0 / sqrt(s2 / D + static_cast<double>(p.eps)));
+    float yA = c[e] * rs, yB = c[2 + e] * rs;
+    const int b = tok / p.rows, r = tok - b * p.rows;
+    if (kind < 2) {
+      double turns = static_cast<double>(p.pos0[b] + r) * exp2(-p.log2_theta * (2.0 * j) / 128.0) * 0.15915494309189535;
+      turns -= floor(turns);
+      double sd, cd;
+      sincospi(2.0 * turns, &sd, &cd);
+      const float cs = static_cast<float>(cd), sn = static_cast<float>(sd);
+      const float nA = __fsub_rn(__fmul_rn(yA, cs), __fmul_rn(yB, sn));
+      const float nB = __fadd_rn(__fmul_rn(yB, cs), __fmul_rn(yA, sn));
+      yA = nA;
+      yB = nB;
+    }
+    __nv_bfloat16* dst;
+    if (kind == 0)
+      dst = p.q + ((static_cast<size_t>(b) * p.Hq + head) * p.rows + r) * 128;
+    else
+      dst = (kind == 1 ? p.k_new : p.v_new) +
+            ((static_cast<size_t>(b) * p.rows + r) * p.Hkv + head - kind_q - (kind == 2 ? p.Hkv : 0)) * 128;
+    dst[dA] = __float2bfloat16_rn(yA);
+    dst[dB] = __float2bfloat16_rn(yB);
+  }
+}
+
+size_t qkv_gemv_smem(int D, int T) {
+  return (static_cast<size_t>(T) * (D + 4) + kGemvWarps * kGemvTiles * 32 * 4) * sizeof(float);
+}
+
 }  // namespace sa
 
 extern "C" {
@@ -555,6 +777,32 @@ SA_API sa_status sa_qkv_project(sa_qkv* h, int32_t layer, const float* x, const 
   p.k_new = static_cast<__nv_bfloat16*>(k_new);
   p.v_new = static_cast<__nv_bfloat16*>(v_new);
   auto s = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute pdl1[1];
+  pdl1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl1[0].val.programmaticStreamSerializationAllowed = 1;
+  static const bool force_tc = [] {  // dev knob: the tcgen05 stream-K path for every token count
+    const char* e = std::getenv("SA_QKV_IMPL");
+    return e && std::string(e) == "tc";
+  }();
+  const size_t gsmem = sa::qkv_gemv_smem(h->D, p.n_tok);
+  if (p.n_tok <= 8 && gsmem <= 200 * 1024 && !force_tc) {  // decode sizes: one fused mma.sync launch
+    static std::atomic<uint64_t> gattr{0};
+    int gdev = 0;
+    if (sa::func_attrs_needed(gattr, &gdev)) {
+      SA_CUDA_CHECK(cudaFuncSetAttribute(sa::qkv_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      sa::func_attrs_done(gattr, gdev);
+    }
+    const int P = h->n_out / 2;
+    cudaLaunchConfig_t cg{};
+    cg.gridDim = dim3(std::max((P + sa::kGemvTiles * 8 - 1) / (sa::kGemvTiles * 8), std::min(h->num_sms, P)));
+    cg.blockDim = dim3(sa::kGemvThreads);
+    cg.dynamicSmemBytes = gsmem;
+    cg.stream = s;
+    cg.attrs = pdl1;
+    cg.numAttrs = 1;
+    SA_CUDA_CHECK(cudaLaunchKernelEx(&cg, sa::qkv_gemv, p));
+    return SA_OK;
+  }
   static std::atomic<uint64_t> attr_mask{0};
   int dev = 0;
   if (sa::func_attrs_needed(attr_mask, &dev)) {
