@@ -411,7 +411,7 @@ def next_rows(dev, B, gamma, hbm_peak):
         out[name] = {"tokens": B * rows, "us_per_layer": round(us, 2), "bytes_per_layer": nbytes,
                      "achieved_gbs": round(gbs, 1), "frac": round(gbs / hbm_peak, 4)}
     proj.close()
-    res = {"producer": dict(out, kernel="qkv_prepare + qkv_gemm (tcgen05, stream-K)", shape="Llama-3.1-8B layer",
+    res = {"producer": dict(out, kernel="qkv_gemv (one fused mma.sync launch: RMSNorm + QKV + RoPE, <= 8 tokens)", shape="Llama-3.1-8B layer",
                             chain="32 layers, one CUDA graph, PDL")}
     V = 128256
     p = torch.softmax(torch.randn((B, gamma + 1, V), generator=g, device=dev), -1)
