@@ -153,6 +153,7 @@ struct SelectParams {
   uint32_t* keys;  // workspace [B][n_sets][ld_scores]
   int32_t* idx;    // [B][n_sets][k_cap]
   int32_t* k_out;  // [B][n_sets]
+  int64_t zs_scores = 0, zs_fx = 0, zs_idx = 0, zs_cnt = 0;  // per-slot strides (batched launches)
 };
 
 sa_status comm_allreduce_i64(sa_comm* c, long long* buf, size_t count, cudaStream_t s);
@@ -177,7 +178,8 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s);
 int draft_max_splits();
 int draft_round_rows();
 int draft_max_active_clusters(int stream, int cs);
-cudaError_t launch_select(const SelectParams& p, cudaStream_t s);
+cudaError_t launch_select(const SelectParams& p, cudaStream_t s, int n_slots = 1);
+int select_max_smem_keys();
 size_t verify_smem_bytes(int MT);
 int verify_tc_merge_capacity(int M);  // bytes of smem a merge may fill (tcgen05 verify, rows M)
 int verify_max_ctas_per_sm(int MT);

@@ -386,14 +386,15 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   return SA_OK;
 }
 
-static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t s) {
+static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t s, int n_slots = 1) {
   if (!a) return fail(SA_INVALID_ARGUMENT, "select: null argument");
   if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "select: no batch bound");
-  if (a->layer_slot < 0 || a->layer_slot >= r->n_slots) return fail(SA_OUT_OF_RANGE, "select: layer_slot");
+  if (a->layer_slot < 0 || a->layer_slot + n_slots > r->n_slots) return fail(SA_OUT_OF_RANGE, "select: layer_slot");
   if (a->rows_in_score < 1) return fail(SA_INVALID_ARGUMENT, "score_columns: empty row subset");
   if (a->mode != SA_PER_LAYER && a->mode != SA_PER_KV_HEAD) return fail(SA_INVALID_ARGUMENT, "select: mode");
-  if (r->slot_layout[a->layer_slot] >= 0 && r->slot_layout[a->layer_slot] != a->mode)
-    return fail(SA_INVALID_ARGUMENT, "select: mode differs from the score layout the verify wrote");
+  for (int z = 0; z < n_slots; ++z)
+    if (r->slot_layout[a->layer_slot + z] >= 0 && r->slot_layout[a->layer_slot + z] != a->mode)
+      return fail(SA_INVALID_ARGUMENT, "select: mode differs from the score layout the verify wrote");
   sa::SelectParams p{};
   p.B = r->B;
   p.Hkv = r->Hkv;
@@ -403,7 +404,7 @@ static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t
   p.score_fx = nullptr;
   if (a->mode == SA_PER_LAYER) {
     p.score_fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, a->layer_slot, nullptr));
-    r->fx_dirty[a->layer_slot] = 0;  // the kernel zeroes what it consumes
+    for (int z = 0; z < n_slots; ++z) r->fx_dirty[a->layer_slot + z] = 0;  // the kernel zeroes what it consumes
   }
   p.count = static_cast<double>(a->mode == SA_PER_LAYER ? r->Hq : r->G) * a->rows_in_score;
   p.ratio = r->cfg.sparse_ratio;
@@ -414,7 +415,12 @@ static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t
   p.k_out = sa_runner_counts(r, a->layer_slot);
   // per-layer sets live at set 0 of each sequence's [Hkv] block; keep the stride = Hkv sets
   // by addressing with n_sets below (the kernel indexes [b][n_sets]); use a dense layout.
-  cudaError_t e = sa::launch_select(p, s);
+  // consecutive slots in one launch (grid z): per-slot strides of the score / index / count buffers
+  p.zs_scores = static_cast<int64_t>(r->cfg.max_batch) * r->Hkv * r->ld;
+  p.zs_fx = static_cast<int64_t>(r->cfg.max_batch) * r->ld;
+  p.zs_idx = static_cast<int64_t>(r->cfg.max_batch) * r->Hkv * r->k_cap;
+  p.zs_cnt = static_cast<int64_t>(r->cfg.max_batch) * r->Hkv;
+  cudaError_t e = sa::launch_select(p, s, n_slots);
   if (e != cudaSuccess) return sa::cuda_fail(e, "select launch");
   return SA_OK;
 }
@@ -713,6 +719,15 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     return v ? atoi(v) : -1;
   }();
   const int skip = env_skip >= 0 ? env_skip : (a->phases ? static_cast<int>(~a->phases & 7u) : 0);
+  // Selection schedule.  Default: one single-CTA select per layer on the side stream, overlapping the
+  // verify chain.  A select CTA needs a whole SM's shared memory, so it waits for a verify CTA of the
+  // next layer to exit and then delays a CTA of the layer after; that costs ~39 us over the chain.
+  // Dev knob SA_SELECT_BATCHED=1: the fused-byproduct selections (Collect-2, AllDraft, LastAccepted)
+  // run as ONE launch after the chain instead, with the layers' CTAs side by side.  It removes those
+  // 39 us but adds a ~55 us bubble before the first draft, so measured it is even (1.748 vs 1.742 ms).
+  static const bool batch_env = getenv("SA_SELECT_BATCHED") != nullptr;
+  const bool batch_selects = batch_env && (skip & 2) == 0 && guided && !weights &&
+                             r->ld <= sa::select_max_smem_keys() && r->n_slots >= L;
   SA_CUDA_CHECK(cudaEventRecord(r->ev_fork, main));
   SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
   for (int l = 0; l < L; ++l) {
@@ -750,13 +765,26 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
         long long* fx = reinterpret_cast<long long*>(sa_runner_layer_scores(r, l, nullptr));
         if (sa_status st = sa::comm_allreduce_i64(r->comm, fx, static_cast<size_t>(B) * r->ld, r->side)) return st;
       }
-      if (sa_status st = select_impl(r, &sel, r->side)) return st;
+      if (!batch_selects)
+        if (sa_status st = select_impl(r, &sel, r->side)) return st;
     }
-    SA_CUDA_CHECK(cudaEventRecord(r->ev_s[l], r->side));
+    if (!batch_selects) SA_CUDA_CHECK(cudaEventRecord(r->ev_s[l], r->side));
+  }
+  if (batch_selects) {  // every layer's top-k in one launch (L x B x sets CTAs side by side)
+    sa_select_args sel{};
+    sel.layer_slot = 0;
+    sel.mode = a->mode;
+    sel.rows_in_score = rows_in_score;
+    if (sa_status st = select_impl(r, &sel, r->side, L)) return st;
+    // ONE dependency edge into the draft chain (draft(1, 0)); later drafts follow it through their
+    // programmatic (PDL) edges.  A per-draft edge from the shared select node measured ~4 us per
+    // step-1 launch: those launches lost their PDL overlap.
+    SA_CUDA_CHECK(cudaEventRecord(r->ev_s[L - 1], r->side));
+    SA_CUDA_CHECK(cudaStreamWaitEvent(main, r->ev_s[L - 1], 0));
   }
   for (int j = 1; j <= a->gamma; ++j) {
     for (int l = 0; l < L; ++l) {
-      if (j == 1) SA_CUDA_CHECK(cudaStreamWaitEvent(main, r->ev_s[l], 0));
+      if (j == 1 && !batch_selects) SA_CUDA_CHECK(cudaStreamWaitEvent(main, r->ev_s[l], 0));
       sa_draft_args d{};
       d.layer = l;
       d.layer_slot = l;

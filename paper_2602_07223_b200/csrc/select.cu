@@ -103,6 +103,12 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
   extern __shared__ uint4 dyn_smem[];
   __shared__ SelShared sh;
   const int set = blockIdx.x, b = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // blockIdx.z: layer slot within a batched launch (per-slot strides; keys in shared memory only)
+  const size_t z = blockIdx.z;
+  long long* const p_score_fx = p.score_fx ? p.score_fx + z * p.zs_fx : nullptr;
+  const float* const p_scores = p.scores ? p.scores + z * p.zs_scores : nullptr;
+  int32_t* const p_idx = p.idx + z * p.zs_idx;
+  int32_t* const p_k_out = p.k_out + z * p.zs_cnt;
   const int n = p.p0[b];
   uint32_t* keys = kKeysInSmem ? reinterpret_cast<uint32_t*>(dyn_smem)
                                : p.keys + (static_cast<size_t>(b) * p.n_sets + set) * p.ld_scores;
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
   // ---- pass 1: keys + first-digit histogram
   uint32_t* h1 = sh.hist[warp & 1];
   if constexpr (kFixed) {
-    long long* fx = p.score_fx + static_cast<size_t>(b) * p.ld_scores;
+    long long* fx = p_score_fx + static_cast<size_t>(b) * p.ld_scores;
     const int n2 = n >> 1;
     for (int i2 = tid; i2 < n2; i2 += kSelThreads) {
       longlong2 v = __ldcg(reinterpret_cast<const longlong2*>(fx) + i2);
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
       atomicAdd(&h1[u >> 20], 1u);
     }
   } else {
-    const float* sc = p.scores + (static_cast<size_t>(b) * p.Hkv + set) * p.ld_scores;
+    const float* sc = p_scores + (static_cast<size_t>(b) * p.Hkv + set) * p.ld_scores;
     const int n4 = n >> 2;
     for (int i4 = tid; i4 < n4; i4 += kSelThreads) {
       const float4 v = __ldcg(reinterpret_cast<const float4*>(sc) + i4);
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
   __syncthreads();
 
   if (k <= 0) {  // nothing to select (the fixed-point slot has been re-armed above)
-    if (tid == 0) p.k_out[b * p.n_sets + set] = 0;
+    if (tid == 0) p_k_out[b * p.n_sets + set] = 0;
     return;
   }
   // ---- radix select: threshold prefix T at resolution `shift`
@@ -219,10 +225,10 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
         if (lane >= off) ci += t;
       }
       sh.wgt[lane] = ci - c;
-      if (lane == 31) p.k_out[b * p.n_sets + set] = ci;
+      if (lane == 31) p_k_out[b * p.n_sets + set] = ci;
     }
     __syncthreads();
-    int32_t* out = p.idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
+    int32_t* out = p_idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
     int run = sh.wgt[warp];
     const unsigned lt = (1u << lane) - 1u;
     for (int base = lo; base < hi; base += 32) {
@@ -287,10 +293,10 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
     }
     sh.wgt[lane] = gi - g;
     sh.weq[lane] = ei - e;
-    if (lane == 31) p.k_out[b * p.n_sets + set] = gi + min(ei, take_eq);
+    if (lane == 31) p_k_out[b * p.n_sets + set] = gi + min(ei, take_eq);
   }
   __syncthreads();
-  int32_t* out = p.idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
+  int32_t* out = p_idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
   int gt_run = sh.wgt[warp], eq_run = sh.weq[warp];
   for (int base = w_lo; base < w_hi; base += 128) {
     const int i0 = base + 4 * lane;
@@ -323,8 +329,9 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(const SelectParams 
   }
 }
 
-cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
-  dim3 grid(p.n_sets, p.B);
+cudaError_t launch_select(const SelectParams& p, cudaStream_t s, int n_slots) {
+  dim3 grid(p.n_sets, p.B, n_slots);
+  if (n_slots > 1 && p.ld_scores > kSmemKeys) return cudaErrorInvalidValue;  // the keys workspace is per launch
   const bool fixed = p.score_fx != nullptr;
   if (p.ld_scores <= kSmemKeys) {
     static bool attr = false;
@@ -347,4 +354,8 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+}  // namespace sa
+
+namespace sa {
+int select_max_smem_keys() { return kSmemKeys; }
 }  // namespace sa
