@@ -10,7 +10,7 @@ for what in "$@"; do
     prof_verify) timeout 300 ncu --set full --clock-control none --import-source on -k regex:verify -s 2 -c 1 -o gpurun_out/prof_verify -f python tools/profile_step.py --layers 4 --iters 1 > gpurun_out/prof_v.log 2>&1 ;;
     prof_draft) timeout 300 ncu --set full --clock-control none --import-source on -k regex:draft -s 8 -c 1 -o gpurun_out/prof_draft -f python tools/profile_step.py --layers 4 --iters 1 > gpurun_out/prof_d.log 2>&1 ;;
     prof_select) timeout 300 ncu --set full --clock-control none --import-source on -k regex:select -s 2 -c 1 -o gpurun_out/prof_select -f python tools/profile_step.py --layers 4 --iters 1 > gpurun_out/prof_s.log 2>&1 ;;
-    prof_qkv) PYTHONPATH=. timeout 300 ncu --set full --clock-control none --import-source on -k regex:qkv_gemm -s 4 -c 1 -o gpurun_out/prof_qkv -f python tools/qkv_bench.py > gpurun_out/prof_q.log 2>&1 ;;
+    prof_qkv) PYTHONPATH=. timeout 300 ncu --set full --clock-control none --import-source on -k regex:qkv_gem -s 40 -c 1 -o gpurun_out/prof_qkv -f python tools/qkv_bench.py > gpurun_out/prof_q.log 2>&1 ;;
     prof_accept) timeout 300 ncu --set full --clock-control none --import-source on -k regex:accept -s 2 -c 1 -o gpurun_out/prof_accept -f python tools/accept_bench.py > gpurun_out/prof_a.log 2>&1 ;;
     bench) timeout 400 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log ;;
     sweep) bash tools/sweep_k_gamma.sh > gpurun_out/sweep.jsonl 2> gpurun_out/sweep.err ;;
