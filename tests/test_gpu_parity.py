@@ -922,3 +922,18 @@ def test_full_size_verify_select_draft(cuda, ref, Hkv, G, R, p0, kfix):
         got = o.cpu().numpy()[0]
         assert rel_err_rows(got, o_ref) < 2e-4, (step, rel_err_rows(got, o_ref))
         assert rel_err_elem(got, o_ref) < 2e-3
+
+
+def test_iteration_parity_batched_selects(cuda):
+    """The batched selection schedule (SA_SELECT_BATCHED=1: every layer's top-k in one grid-z launch
+    after the verify chain, one dependency edge into the draft chain) passes the same iteration
+    parity cases.  The knob is read once per process, so the cases run in a child pytest."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SA_SELECT_BATCHED="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        "tests/test_gpu_parity.py::test_iteration_parity"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
