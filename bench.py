@@ -275,10 +275,10 @@ def run_ours(args, rank, world, local_rank):
     ev_done = [torch.cuda.Event() for _ in range(n_e2e)]
     ev_out = [torch.cuda.Event() for _ in range(n_e2e)]
 
-    def upload(i):  # inputs of step i into set i % 2 once step i-2 (same set) finished computing
+    def upload(i):  # inputs of step i into set i % 2 once step i-2 (same set) is computed AND read back
         st = i % 2
         if i >= 2:
-            up.wait_event(ev_done[i - 2])
+            up.wait_event(ev_out[i - 2])  # implies ev_done[i - 2]; the compute stream then waits on ev_in only
         with torch.cuda.stream(up):
             for h, d_ in zip(host_in[st], dev_sets[st][:6]):
                 d_.copy_(h, non_blocking=True)
@@ -290,9 +290,7 @@ def run_ours(args, rank, world, local_rank):
             st = i % 2
             if i + 1 < hi:
                 upload(i + 1)
-            stream.wait_event(ev_in[i])
-            if i >= 2:
-                stream.wait_event(ev_out[i - 2])  # step i-2's outputs (same set) read back
+            stream.wait_event(ev_in[i])  # (ev_in[i] follows ev_out[i - 2]: set st's outputs are free)
             runner.iteration(set_args[st], stream=stream)
             ev_done[i].record(stream)
             down.wait_event(ev_done[i])
