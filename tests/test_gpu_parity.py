@@ -497,20 +497,21 @@ def test_draft_streaming_mode(cuda, ref):
     for b in range(B):
         assert cnt[b, 0] == selection_k(0.5, p0s[b], 16)
         m.cache.set_size(p0s[b], seq=b)
-    qd = normal_bf16(63, 1, (B, Hq, D))
-    kd, vd = normal_bf16(63, 2, (B, Hkv, D)), normal_bf16(63, 3, (B, Hkv, D))
-    od = torch.zeros((B, Hq, D), dtype=torch.float32, device="cuda")
-    r.draft(1, 1, to_dev_bf16(qd), od, to_dev_bf16(kd), to_dev_bf16(vd), scale=SCALE)
-    got = od.cpu().numpy()
-    for b in range(B):
-        kv = m.refs[b]
-        kk, vv = np.zeros((2 * Hkv, D), np.float32), np.zeros((2 * Hkv, D), np.float32)
-        kk[Hkv:], vv[Hkv:] = kd[b], vd[b]
-        kv.append(kk, vv)
-        sets = [idx[b, 0, : cnt[b, 0]].astype(np.int64)]
-        o_ref = kv.draft_layer(1, Hq, qd[b], sets, p0s[b], 1, SCALE, threads=8)
-        assert rel_err_rows(got[b], o_ref) < 2e-4, (b, rel_err_rows(got[b], o_ref))
-        assert rel_err_elem(got[b], o_ref) < 2e-3
+    for step in range(1, R):  # step 2 also gathers the tail row step 1 appended (old-tail path)
+        qd = normal_bf16(63, 10 * step + 1, (B, Hq, D))
+        kd, vd = normal_bf16(63, 10 * step + 2, (B, Hkv, D)), normal_bf16(63, 10 * step + 3, (B, Hkv, D))
+        od = torch.zeros((B, Hq, D), dtype=torch.float32, device="cuda")
+        r.draft(1, step, to_dev_bf16(qd), od, to_dev_bf16(kd), to_dev_bf16(vd), scale=SCALE)
+        got = od.cpu().numpy()
+        for b in range(B):
+            kv = m.refs[b]
+            kk, vv = np.zeros((2 * Hkv, D), np.float32), np.zeros((2 * Hkv, D), np.float32)
+            kk[Hkv:], vv[Hkv:] = kd[b], vd[b]
+            kv.append(kk, vv)
+            sets = [idx[b, 0, : cnt[b, 0]].astype(np.int64)]
+            o_ref = kv.draft_layer(1, Hq, qd[b], sets, p0s[b], step, SCALE, threads=8)
+            assert rel_err_rows(got[b], o_ref) < 2e-4, (step, b, rel_err_rows(got[b], o_ref))
+            assert rel_err_elem(got[b], o_ref) < 2e-3
 
 
 def test_quest_and_window_selectors(cuda, ref):
