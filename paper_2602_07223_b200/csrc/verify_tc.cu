@@ -566,9 +566,10 @@ __global__ void __launch_bounds__(384, 1)
       const bool full = tstart + C::kTile <= p0;  // chunk tiles: every row sees every token
       const bool in_range = pos < p0 + R;         // window tiles: positions past the window masked
       if ((score_out || score_fx) && pos < p0) {  // fused Collect-k column sum (raw logits)
-        float sc = 0.f;
+        float sc4[4] = {0.f, 0.f, 0.f, 0.f};  // four independent FMA chains (latency, not throughput)
 #pragma unroll
-        for (int m = 0; m < MR; ++m) sc = fmaf(wsc[m], s[m], sc);
+        for (int m = 0; m < MR; ++m) sc4[m & 3] = fmaf(wsc[m], s[m], sc4[m & 3]);
+        const float sc = (sc4[0] + sc4[1]) + (sc4[2] + sc4[3]);
         if (score_fx)  // per-layer: integer atomics over the KV heads (order-independent, deterministic)
           atomicAdd(reinterpret_cast<unsigned long long*>(score_fx + pos),
                     static_cast<unsigned long long>(__float2ll_rn(sc * kScoreFxScale)));
@@ -588,15 +589,16 @@ __global__ void __launch_bounds__(384, 1)
       float mr[N];
 #pragma unroll
       for (int m = 0; m < MR; m += 4) *reinterpret_cast<float4*>(&mr[m]) = *reinterpret_cast<const float4*>(&mref[m]);
-      bool exceed = false;
+      bool ex4[4] = {false, false, false, false};  // four independent OR chains
       if (full) {
 #pragma unroll
-        for (int m = 0; m < MR; ++m) exceed |= fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
+        for (int m = 0; m < MR; ++m) ex4[m & 3] |= fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
       } else {
 #pragma unroll
         for (int m = 0; m < MR; ++m)
-          exceed |= (in_range && pos <= lim[m]) && fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
+          ex4[m & 3] |= (in_range && pos <= lim[m]) && fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
       }
+      const bool exceed = (ex4[0] || ex4[1]) || (ex4[2] || ex4[3]);
       if (ts == 0) SA_TRACE(13, t);
       const bool any_exceed = named_bar_or(bar_wg, 128, exceed);
       if (ts == 0) SA_TRACE(14, t);
