@@ -35,7 +35,7 @@
  *    fit config 3 in one B200's HBM).  fp32 inputs are rounded to nearest-even bf16.
  *  - Threading (kv_store.hpp:16-18): one writer stream per cache; read-only calls may
  *    run on other streams after an event.
- *  - head_dim must be 128 (all BASELINE configs); page_size a power of two >= 64.
+ *  - head_dim must be 128 (all BASELINE configs); page_size a power of two >= 128.
  */
 #ifndef SPECATTN_B200_H_
 #define SPECATTN_B200_H_
@@ -93,7 +93,7 @@ typedef struct sa_cache_config {
   int64_t head_dim;    /* ModelConfig::head_dim (must be 128) */
   int64_t max_context; /* ModelConfig::max_context, per sequence */
   int64_t max_seqs;    /* sequences addressable by seq id 0..max_seqs-1 (reference: 1) */
-  int64_t page_size;   /* tokens per page (power of two >= 64); 0 -> 256 */
+  int64_t page_size;   /* tokens per page (power of two >= 128, sa_cache_create checks); 0 -> 256 */
   int64_t num_pages;   /* page pool size; 0 -> max_seqs * ceil(max_context / page_size) */
 } sa_cache_config;
 
@@ -229,8 +229,10 @@ SA_API sa_status sa_draft_attention(sa_runner* r, const sa_draft_args* a, void* 
 typedef struct sa_iteration_args {
   int32_t gamma;
   sa_strategy strategy;     /* any sa_strategy: the logit-guided ones select from the verify byproduct;
-                               SA_WINDOW selects once per iteration (sink 4, window k - 4), SA_QUEST_LIKE
-                               before every draft launch from that step's query (the baselines) */
+                               SA_WINDOW selects once per iteration with the fixed baseline budget
+                               sink 4 + window (k_cap - 4), k_cap = selection_k(ratio, max_prefix,
+                               k_min); SA_QUEST_LIKE before every draft launch from that step's
+                               query (the baselines; not with a KV-head group communicator) */
   sa_select_mode mode;
   float scale;
   const void *qv, *kv_new, *vv_new, *qd, *kd_new, *vd_new;
@@ -238,8 +240,14 @@ typedef struct sa_iteration_args {
   int32_t use_graph;
   uint32_t phases;          /* 0 = all; else a mask of SA_PHASE_* (timing breakdowns: the phases left
                                out are skipped, their buffers are left as the last run wrote them) */
-  int32_t accepted;         /* SA_LAST_ACCEPTED: drafts accepted by the previous verify (row a+1,
-                               selection.cpp:198-207); 0 <= accepted <= gamma */
+  int32_t accepted;         /* a, 0 <= a <= gamma: the drafts the caller accepts from THIS iteration's
+                               verify (sa_accept's result).  SA_LAST_ACCEPTED selects from row a+1
+                               (selection.cpp:198-207).  The draft phase is the NEXT draft chain
+                               (SPEC.md:382-385): its new rows go to p0+a+1, p0+a+2, ... after the
+                               rows [y, x1..xa] the verify wrote, and every draft step's tail is
+                               [p0, p0+a+1+step).  Commit with sa_kv_commit_accepted(seq, p0, a):
+                               it keeps the verify's rows p0..p0+a (the draft rows beyond are
+                               provisional, and the next verify rewrites them). */
 } sa_iteration_args;
 #define SA_PHASE_VERIFY 1u
 #define SA_PHASE_SELECT 2u
@@ -248,10 +256,14 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
 /* Number of kernels one sa_iteration_run launches (for gpu_launches accounting). */
 SA_API int64_t sa_iteration_kernel_count(const sa_runner* r, const sa_iteration_args* a);
 
-/* Development hook (not part of the reference surface): with SA_TRACE=1 in the environment the
- * verify kernel records per-CTA start / main-loop-end / end timestamps per layer; this writes the
- * trace buffer to `path` after a device sync.  Returns 0 on success, < 0 otherwise. */
-SA_API int sa_dev_trace_dump(const char* path);
+/* Development hooks (not part of the reference surface; the product never reads the environment).
+ * sa_dev_set_knob sets one dev-only tuning / tracing knob of a runner (internal.h DevConfig: e.g.
+ * "verify_impl" 1 = the mma.sync baseline kernel, "iter_skip" phase bits, "trace" 1 = per-CTA
+ * globaltimer traces); the defaults are the product settings.  Unknown names: SA_INVALID_ARGUMENT.
+ * sa_dev_trace_dump writes the runner's verify + draft trace buffers to `path` after a device sync;
+ * returns 0 on success, < 0 otherwise (e.g. tracing not enabled). */
+SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value);
+SA_API int sa_dev_trace_dump(sa_runner* r, const char* path);
 
 /* ---------------------------------------------------------------- multi-GPU
  * The path's only collective: when a layer's KV heads are sharded over several GPUs (one process
@@ -263,6 +275,15 @@ typedef struct sa_comm sa_comm;
 SA_API sa_status sa_comm_unique_id(void* id_out_128);
 SA_API sa_status sa_comm_create(const void* id_128, int32_t nranks, int32_t rank, sa_comm** out);
 SA_API sa_status sa_comm_destroy(sa_comm* comm);
+/* The communicator's size and this rank as NCCL reports them (ncclCommCount / ncclCommUserRank). */
+SA_API sa_status sa_comm_info(const sa_comm* comm, int32_t* nranks, int32_t* rank);
+/* NCCL asynchronous-error check (ncclCommGetAsyncError): on an error the communicator is aborted
+ * (ncclCommAbort, so no kernel of this rank waits on a dead peer) and SA_NCCL_ERROR is returned;
+ * every later exchange on it fails.  sa_iteration_run checks it after each launch. */
+SA_API sa_status sa_comm_check(sa_comm* comm);
+/* Wait for `stream` while watching the communicator: returns when the stream is idle, or aborts the
+ * communicator and returns SA_NCCL_ERROR on an asynchronous error or after timeout_ms (< 0: none). */
+SA_API sa_status sa_comm_sync(sa_comm* comm, void* stream, int64_t timeout_ms);
 /* Attach the head-group communicator: sa_iteration_run then exchanges every layer's sums before
  * its select (per-layer mode).  NULL detaches. */
 SA_API sa_status sa_runner_set_comm(sa_runner* r, sa_comm* comm);
@@ -300,6 +321,9 @@ SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, i
                                int32_t n_q_heads, int32_t n_kv_heads, double norm_eps, double rope_theta,
                                int32_t rope_style, sa_qkv** out);
 SA_API sa_status sa_qkv_destroy(sa_qkv* h);
+/* Dev-only knobs of a projection ("trace" 1: per-CTA stamps, dumped to /tmp/sa_qkv_trace.bin by
+ * sa_qkv_destroy; "dev": variant bits; "impl_tc" 1: the tcgen05 path for every token count). */
+SA_API sa_status sa_qkv_dev_set_knob(sa_qkv* h, const char* name, int64_t value);
 /* x: f32 [B][rows][d_model] hidden states (device); positions: int32 [B] (device) absolute position of
  * each sequence's row 0 (row r is at positions[b] + r); 1 <= B * rows <= 128.  Out (device, bf16):
  * q [B][Hq][rows][128], k_new / v_new [B][rows][Hkv][128].  Stream-ordered, graph-capturable. */

@@ -89,7 +89,9 @@ SIGNATURES = {
     "sa_draft_attention": (C.c_int, [_vp, C.POINTER(DraftArgs), _vp]),
     "sa_iteration_run": (C.c_int, [_vp, C.POINTER(IterationArgs), _vp]),
     "sa_iteration_kernel_count": (_i64, [_vp, C.POINTER(IterationArgs)]),
-    "sa_dev_trace_dump": (C.c_int, [C.c_char_p]),
+    "sa_dev_trace_dump": (C.c_int, [_vp, C.c_char_p]),
+    "sa_dev_set_knob": (C.c_int, [_vp, C.c_char_p, _i64]),
+    "sa_qkv_dev_set_knob": (C.c_int, [_vp, C.c_char_p, _i64]),
     "sa_score_weights": (C.c_int, [_vp, _i32, _vp, _i64, _i32, C.c_int, _vp]),
     "sa_kv_enable_page_summaries": (C.c_int, [_vp, _i64]),
     "sa_qkv_create": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, C.c_double, C.c_double, _i32, C.POINTER(_vp)]),
@@ -102,6 +104,9 @@ SIGNATURES = {
     "sa_comm_unique_id": (C.c_int, [_vp]),
     "sa_comm_create": (C.c_int, [_vp, _i32, _i32, C.POINTER(_vp)]),
     "sa_comm_destroy": (C.c_int, [_vp]),
+    "sa_comm_info": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32)]),
+    "sa_comm_check": (C.c_int, [_vp]),
+    "sa_comm_sync": (C.c_int, [_vp, _vp, _i64]),
     "sa_runner_set_comm": (C.c_int, [_vp, _vp]),
     "sa_exchange_layer_scores": (C.c_int, [_vp, _i32, _vp]),
 }
@@ -369,6 +374,14 @@ class Runner:
     def iteration_kernel_count(self, args: IterationArgs) -> int:
         return int(lib().sa_iteration_kernel_count(self.h, C.byref(args)))
 
+    def set_dev_knob(self, name: str, value: int):
+        """Dev-only tuning / tracing knob (sa_dev_set_knob); the defaults are the product settings."""
+        _check(lib().sa_dev_set_knob(self.h, name.encode(), int(value)))
+
+    def trace_dump(self, path: str) -> int:
+        """Dev-only: write the verify + draft trace buffers (knob "trace") to `path`."""
+        return int(lib().sa_dev_trace_dump(self.h, path.encode()))
+
 
 class Comm:
     """KV-head group communicator (sa_comm): NCCL over NVLink for the per-layer score exchange.
@@ -386,6 +399,20 @@ class Comm:
         h = _vp()
         _check(lib().sa_comm_create(buf, nranks, rank, C.byref(h)))
         self.h, self.nranks, self.rank = h, nranks, rank
+
+    def info(self):
+        """(nranks, rank) as NCCL reports them for this communicator."""
+        n, r = _i32(), _i32()
+        _check(lib().sa_comm_info(self.h, C.byref(n), C.byref(r)))
+        return n.value, r.value
+
+    def check(self):
+        """Raise SpecAttnError (nccl_error) if NCCL reported an asynchronous error (comm aborted)."""
+        _check(lib().sa_comm_check(self.h))
+
+    def sync(self, stream=None, timeout_ms=-1):
+        """Wait for `stream` while watching for NCCL errors / a hung peer (aborts on timeout)."""
+        _check(lib().sa_comm_sync(self.h, _stream(stream), int(timeout_ms)))
 
     def close(self):
         if getattr(self, "h", None):
@@ -422,6 +449,10 @@ class QkvProjection:
             self.close()
         except Exception:
             pass
+
+    def set_dev_knob(self, name: str, value: int):
+        """Dev-only knob (sa_qkv_dev_set_knob): "trace", "dev" variant bits, "impl_tc"."""
+        _check(lib().sa_qkv_dev_set_knob(self.h, name.encode(), int(value)))
 
     def project(self, layer, x, positions, q=None, k_new=None, v_new=None, stream=None):
         """x: f32 [B][rows][d_model] device, positions int32 [B] device -> (q, k_new, v_new) bf16."""

@@ -188,6 +188,7 @@ SA_API sa_status sa_cache_create(const sa_cache_config* cfg, sa_cache** out) {
   c->len.assign(c->max_seqs, 0);
   c->committed.assign(c->max_seqs, 0);
   c->pages_of_seq.assign(c->max_seqs, 0);
+  c->verified_end.assign(c->max_seqs, 0);
   c->free_pages.resize(c->num_pages);
   for (int64_t i = 0; i < c->num_pages; ++i) c->free_pages[i] = static_cast<int32_t>(c->num_pages - 1 - i);
   std::string err;
@@ -218,8 +219,11 @@ SA_API sa_status sa_kv_commit_accepted(sa_cache* c, int32_t seq, int64_t p0, int
   if (seq < 0 || seq >= c->max_seqs) return fail(SA_OUT_OF_RANGE, "sequence id out of range");
   // The verify rows p0.. were written by the verify kernel's fused append into pages reserved for
   // them (sa_runner_set_batch), whether or not the host length was advanced: keep p0 .. p0+accepted.
+  // Rows that exist: the host length, or the last verify's fused append [p0, p0 + n_rows).
   const int64_t keep = p0 + accepted + 1;
-  if (accepted < 0 || p0 < 0 || p0 > c->len[seq] || keep > (c->pages_of_seq[seq] << c->page_shift))
+  const int64_t written = std::max(c->len[seq], c->verified_end[seq]);
+  if (accepted < 0 || p0 < 0 || p0 > c->len[seq] || keep > written || keep > c->max_context ||
+      keep > (c->pages_of_seq[seq] << c->page_shift))
     return fail(SA_OUT_OF_RANGE, "KvStore: commit beyond the appended verify rows");
   c->summaries_stale_from(seq, std::min(c->len[seq], p0));
   c->len[seq] = keep;

@@ -116,18 +116,21 @@ struct DraftWarp {
       const float p2 = fast_exp2(fmaf(s[bi][2], c, -b0)), p3 = fast_exp2(fmaf(s[bi][3], c, -b1));
       l[0] += p0 + p2;
       l[1] += p1 + p3;
-      uint32_t h01, l01, h23, l23;
-      split_bf16(p0, p1, h01, l01);  // token gid,   rows 2t4, 2t4+1
-      split_bf16(p2, p3, h23, l23);  // token gid+8
+      // P = hi + mid + lo bf16 planes (~2^-27 relative: the tau = 1e-3 elementwise bar of SURVEY §8c)
+      uint32_t h01, m01, l01, h23, m23, l23;
+      split3_bf16(p0, p1, h01, m01, l01);  // token gid,   rows 2t4, 2t4+1
+      split3_bf16(p2, p3, h23, m23, l23);  // token gid+8
       // B fragments of P^T (k = tokens, n = rows): 8x8 transposes of the two token halves
       const uint32_t bh0 = movmatrix_trans(h01), bh1 = movmatrix_trans(h23);
+      const uint32_t bm0 = movmatrix_trans(m01), bm1 = movmatrix_trans(m23);
       const uint32_t bl0 = movmatrix_trans(l01), bl1 = movmatrix_trans(l23);
       const int tok = r0[bi] + (mi >> 1) * 8 + (lane & 7);
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {  // one V fragment load serves the hi and lo P planes
+      for (int jj = 0; jj < 8; ++jj) {  // one V fragment load serves the three P planes
         uint32_t a[4];
         ldsm_x4_t(v_smem[bi] + swz(tok, 2 * jj + (mi & 1), half), a[0], a[1], a[2], a[3]);
         mma_bf16(o[jj], a, bh0, bh1);
+        mma_bf16(o[jj], a, bm0, bm1);
         mma_bf16(o[jj], a, bl0, bl1);
       }
     }
@@ -186,7 +189,7 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
 }
 
 // Grid (CS, Hkv, B) in clusters of CS CTAs: CTA `split` of a (sequence, KV head) owns rows
-// [split*chunk, (split+1)*chunk) of the virtual key list T[0..k) ++ [p0, p0+step).
+// [split*chunk, (split+1)*chunk) of the virtual key list T[0..k) ++ [p0, p0+draft_off+step).
 //
 // Before griddepcontrol.wait (overlapping the previous launch, two CTAs per SM): every row that
 // already exists — the selected prefix rows and the tail rows appended by earlier draft steps —
@@ -215,13 +218,14 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   const int set = p.n_sets == 1 ? 0 : g;
   const int k = p.k_act[b * p.n_sets + set];
   const int32_t* T = p.idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
-  const int m_total = k + j;
+  const int tail = p.draft_off + j;  // tail rows [p0, p0 + tail): committed verify rows, then this chain's
+  const int m_total = k + tail;
   const int v_begin = split * p.chunk;
   const int v_end = min(m_total, v_begin + p.chunk);
   const int n = max(0, v_end - v_begin);
   const int Hq = p.Hkv * p.G;
-  const int new_pos = p0 + j - 1;
-  const int new_v = k + j - 1;  // virtual index of this step's new row
+  const int new_pos = p0 + tail - 1;
+  const int new_v = k + tail - 1;  // virtual index of this step's new row
   // rows written by earlier draft steps of this layer come from launches >= 2 back in the PDL
   // chain, complete once this grid runs (every earlier CTA passed its own wait before triggering)
   const bool old_tail_ready = p.cache.n_layers >= 2;
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   // the next round loaded one round ahead, so resolving a round's source rows costs no dependent
   // global round trip between two rounds' compute
   int* bt_s = reinterpret_cast<int*>(smem + DCfg::kOffBt);
-  const int n_pages_seq = ((p0 + j) >> p.cache.page_shift) + 1;
+  const int n_pages_seq = ((p0 + tail) >> p.cache.page_shift) + 1;
   const bool bt_smem = kStream && n_pages_seq <= DCfg::kBtMax;
   int tq = 0;
   if (kStream) {

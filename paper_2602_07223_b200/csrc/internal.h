@@ -51,6 +51,7 @@ struct sa_cache {
   std::vector<int32_t> h_block_table;
   std::vector<int64_t> len, committed, pages_of_seq;
   std::vector<int32_t> free_pages;           // LIFO free list
+  std::vector<int64_t> verified_end;         // p0 + n_rows of the last verify with a fused append (commit bound)
   CUtensorMap tmap_k{}, tmap_v{};            // 2-D [rows][128] bf16, box {64, 64}, SWIZZLE_128B
   CUtensorMap tmap_k128{}, tmap_v128{};      // same tensors, box {64, 128} (tcgen05 verify tiles)
   // Quest page summaries (kv_store.cpp:90-139): per (layer, page, KV head, quest page) elementwise key
@@ -81,6 +82,27 @@ struct sa_cache {
 };
 
 namespace sa {
+
+// Dev-only tuning / tracing knobs of one runner (sa_dev_set_knob).  The defaults ARE the product
+// settings; nothing here is read from the environment.
+struct DevConfig {
+  int verify_impl = 0;          // 0: tcgen05 verify (product); 1: the mma.sync baseline kernel (verify.cu)
+  int verify_chunk_tiles = 2;   // 128-token tiles per dynamically claimed chunk
+  int verify_prefetch = 0;      // tiles prefetched into L2 ahead of the K ring
+  int verify_next_pf = 0;       // chunks of the next layer each CTA prefetches into L2 at its stream end
+  int verify_no_prefill = 0;    // do not fill the ring before griddepcontrol.wait
+  int verify_static_first = 1;  // first chunk = split index (else every chunk claimed from the counter)
+  int verify_mergers = 4;       // CTAs (last arrivals of a unit) that split the merge's rows
+  int verify_full_rows = 0;     // softmax over all N MMA columns instead of MR = roundup4(M)
+  int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
+  int draft_multi_rounds = 3;   // rounds allowed in the two-CTA-per-SM multi-round mode
+  int draft_debug = 0;          // print the draft launch geometry to stderr
+  int draft_no_pdl = 0;         // launch iteration drafts without programmatic dependent launch
+  int iter_skip = -1;           // phase bits to skip in sa_iteration_run (-1: sa_iteration_args.phases)
+  int select_batched = 0;       // one grid-z select launch for all layers after the verify chain
+  int stream_priority = 1;      // side stream lowest priority, capture stream highest
+  int trace = 0;                // per-CTA globaltimer traces (sa_dev_trace_dump)
+};
 
 // ---- kernel launch parameter blocks (also used by the launchers in verify.cu / draft.cu / select.cu)
 
@@ -116,6 +138,7 @@ struct VerifyParams {
   int chunk_tiles;  // 128-token tiles per dynamically claimed chunk
   int prefetch;     // tiles prefetched into L2 ahead of the K ring
   int next_pf;      // chunks of the next layer each CTA prefetches into L2 at the end of its stream
+  int full_rows;    // dev: softmax over all N columns
 };
 
 struct DraftParams {
@@ -138,6 +161,7 @@ struct DraftParams {
   unsigned long long* trace;  // dev-only per-CTA phase timestamps; null in production
   int use_pdl;  // launch with programmatic stream serialization (iteration graph only)
   int stream;   // double-buffered multi-round chunks (one CTA per SM)
+  int draft_off;  // this chain's new rows start at p0 + draft_off; the tail is [p0, p0 + draft_off + step)
 };
 
 struct SelectParams {

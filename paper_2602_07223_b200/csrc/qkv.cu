@@ -53,7 +53,9 @@ struct sa_qkv {
   float* part = nullptr;           // [max grid][2][256][128] split-K partials
   int* counters = nullptr;         // [heads]
   int max_grid = 0;
-  unsigned long long* trace = nullptr;  // dev-only
+  unsigned long long* trace = nullptr;  // dev-only (knob "trace")
+  int dev_bits = 0;                      // dev-only variant bits (knob "dev")
+  int force_tc = 0;                      // dev-only: the tcgen05 stream-K path for every token count
   int device = 0, num_sms = 148;
 };
 
@@ -462,18 +464,7 @@ __global__ void __launch_bounds__(kQkvThreads, 1) qkv_gemm(QkvParams p) {
 //     (deterministic), then the tile's warp applies 1/rms and RoPE (fp32, angle reduced in double as in
 //     qkv_prepare) and stores bf16.
 // Pre-dependency: the CTA's weight rows are prefetched into L2 (they depend on nothing).
-// (a, b) -> three bf16 planes with a ~= hi + mid + lo to ~2^-24 relative (each residual is exact in fp32)
-__device__ __forceinline__ void split3_bf16(float a, float b, uint32_t& hi, uint32_t& mid, uint32_t& lo) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  const float2 hf = __bfloat1622float2(h);
-  const float ra = a - hf.x, rb = b - hf.y;
-  const __nv_bfloat162 m = __floats2bfloat162_rn(ra, rb);
-  const float2 mf = __bfloat1622float2(m);
-  const __nv_bfloat162 l = __floats2bfloat162_rn(ra - mf.x, rb - mf.y);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  mid = *reinterpret_cast<const uint32_t*>(&m);
-  lo = *reinterpret_cast<const uint32_t*>(&l);
-}
+// split3_bf16 (common.cuh): (a, b) -> three bf16 planes, a ~= hi + mid + lo
 
 constexpr int kGemvThreads = 512;
 constexpr int kGemvWarps = kGemvThreads / 32;
@@ -697,10 +688,6 @@ SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, i
     e = cudaMalloc(&h->part, static_cast<size_t>(h->max_grid) * 2 * 2 * sa::kQkvMaxTokens * 128 * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&h->counters, heads * sizeof(int));
   if (e == cudaSuccess) e = cudaMemset(h->counters, 0, heads * sizeof(int));
-  if (e == cudaSuccess && std::getenv("SA_QKV_TRACE")) {
-    e = cudaMalloc(&h->trace, static_cast<size_t>(n_layers) * h->max_grid * 32 * 8);
-    if (e == cudaSuccess) e = cudaMemset(h->trace, 0, static_cast<size_t>(n_layers) * h->max_grid * 32 * 8);
-  }
   if (e == cudaSuccess)
     e = cudaMemcpy(h->gain, attn_norm_gain, static_cast<size_t>(n_layers) * d_model * sizeof(float),
                    cudaMemcpyDefault);
@@ -715,6 +702,25 @@ SA_API sa_status sa_qkv_create(const void* w_qkv, const float* attn_norm_gain, i
     return sa::cuda_fail(e, "qkv create");
   }
   *out = h;
+  return SA_OK;
+}
+
+SA_API sa_status sa_qkv_dev_set_knob(sa_qkv* h, const char* name, int64_t value) {
+  if (!h || !name) return sa::fail(SA_INVALID_ARGUMENT, "null argument");
+  const std::string n(name);
+  if (n == "dev") {
+    h->dev_bits = static_cast<int>(value);
+  } else if (n == "impl_tc") {
+    h->force_tc = value ? 1 : 0;
+  } else if (n == "trace") {
+    if (value && !h->trace) {
+      const size_t bytes = static_cast<size_t>(h->L) * h->max_grid * 32 * 8;
+      SA_CUDA_CHECK(cudaMalloc(&h->trace, bytes));
+      SA_CUDA_CHECK(cudaMemset(h->trace, 0, bytes));
+    }
+  } else {
+    return sa::fail(SA_INVALID_ARGUMENT, "unknown dev knob '" + n + "'");
+  }
   return SA_OK;
 }
 
@@ -772,7 +778,7 @@ SA_API sa_status sa_qkv_project(sa_qkv* h, int32_t layer, const float* x, const 
   p.part = h->part;
   p.counters = h->counters;
   p.trace = h->trace;
-  if (const char* e = std::getenv("SA_QKV_DEV")) p.dev = std::atoi(e);
+  p.dev = h->dev_bits;
   p.q = static_cast<__nv_bfloat16*>(q);
   p.k_new = static_cast<__nv_bfloat16*>(k_new);
   p.v_new = static_cast<__nv_bfloat16*>(v_new);
@@ -780,10 +786,7 @@ SA_API sa_status sa_qkv_project(sa_qkv* h, int32_t layer, const float* x, const 
   cudaLaunchAttribute pdl1[1];
   pdl1[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl1[0].val.programmaticStreamSerializationAllowed = 1;
-  static const bool force_tc = [] {  // dev knob: the tcgen05 stream-K path for every token count
-    const char* e = std::getenv("SA_QKV_IMPL");
-    return e && std::string(e) == "tc";
-  }();
+  const bool force_tc = h->force_tc != 0;
   const size_t gsmem = sa::qkv_gemv_smem(h->D, p.n_tok);
   if (p.n_tok <= 8 && gsmem <= 200 * 1024 && !force_tc) {  // decode sizes: one fused mma.sync launch
     static std::atomic<uint64_t> gattr{0};

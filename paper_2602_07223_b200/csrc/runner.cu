@@ -53,6 +53,9 @@ struct sa_runner {
   std::vector<float*> wlogits;
   float2* wstats = nullptr;
   double* qbounds = nullptr;  // QuestLike page bounds [max_batch][max quest pages]
+  sa::DevConfig dev;  // dev-only knobs (sa_dev_set_knob); defaults = product settings
+  unsigned long long* vtrace = nullptr;  // dev traces (knob "trace"), null in production
+  unsigned long long* dtrace = nullptr;
 };
 
 namespace {
@@ -88,34 +91,26 @@ int mtiles_for(int G, int R) { return (G * R + 2 + 15) / 16; }
 
 }  // namespace
 
-// dev-only verify pipeline trace (SA_TRACE=1): [1024] per-tile events of CTA 0, then per layer
+// dev-only verify pipeline trace (knob "trace"): [1024] per-tile events of CTA 0, then per layer
 // (mod 64) [1024 CTAs][8] = start, end, main-loop end, tiles | split << 32, last PV done,
 // partial stored, arrival counted, merge inputs landed (globaltimer ns).
 constexpr size_t kVTraceWords = 1024 + 64 * 16384;
-static unsigned long long* dev_verify_trace() {
-  static unsigned long long* t = [] {
-    unsigned long long* b = nullptr;
-    if (getenv("SA_TRACE")) {
-      cudaMalloc(&b, kVTraceWords * 8);
-      cudaMemset(b, 0, kVTraceWords * 8);
-    }
-    return b;
-  }();
-  return t;
-}
-
-// dev-only draft trace (SA_TRACE=1): [(step-1) mod 8][layer mod 64][512 CTAs][16 phases] globaltimer ns.
+// dev-only draft trace: [(step-1) mod 8][layer mod 64][512 CTAs][16 phases] globaltimer ns.
 constexpr size_t kDTraceWords = static_cast<size_t>(8) * 64 * 512 * 16;
-static unsigned long long* dev_draft_trace() {
-  static unsigned long long* t = [] {
-    unsigned long long* b = nullptr;
-    if (getenv("SA_TRACE")) {
-      cudaMalloc(&b, kDTraceWords * 8);
-      cudaMemset(b, 0, kDTraceWords * 8);
-    }
-    return b;
-  }();
-  return t;
+
+// (Re)create the runner's side / capture streams with the priorities of its dev config: the selection
+// side stream at the lowest priority, the capture stream at the highest, so that when SMs free up the
+// next layer's verify CTAs are scheduled ahead of the (off-critical-path) selects.
+static cudaError_t make_streams(sa_runner* r) {
+  if (r->side) cudaStreamDestroy(r->side);
+  if (r->capture) cudaStreamDestroy(r->capture);
+  r->side = r->capture = nullptr;
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  const bool prio = r->dev.stream_priority != 0;
+  cudaError_t e = cudaStreamCreateWithPriority(&r->side, cudaStreamNonBlocking, prio ? least : 0);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&r->capture, cudaStreamNonBlocking, prio ? greatest : 0);
+  return e;
 }
 
 extern "C" {
@@ -135,8 +130,6 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   if (!(cfg->sparse_ratio > 0.0) || cfg->sparse_ratio > 1.0)
     return fail(SA_INVALID_ARGUMENT, "SelectorConfig: sparse_ratio must be in (0, 1]");  // selection.cpp:50-53
   if (cfg->k_min < 0) return fail(SA_INVALID_ARGUMENT, "SelectorConfig: k_min must be >= 0");
-  dev_verify_trace();  // dev trace buffers (SA_TRACE) allocated outside any graph capture
-  dev_draft_trace();
   auto* r = new sa_runner();
   r->cache = cache;
   r->cfg = *cfg;
@@ -172,15 +165,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
   alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
-  // the selection side stream at the lowest priority, the capture stream at the highest: when SMs
-  // free up, the next layer's verify CTAs are scheduled ahead of the (off-critical-path) selects
-  static const bool prio = !getenv("SA_NO_STREAM_PRIORITY");  // dev knob
-  int least = 0, greatest = 0;
-  cudaDeviceGetStreamPriorityRange(&least, &greatest);
-  if (e == cudaSuccess)
-    e = cudaStreamCreateWithPriority(&r->side, cudaStreamNonBlocking, prio ? least : 0);
-  if (e == cudaSuccess)
-    e = cudaStreamCreateWithPriority(&r->capture, cudaStreamNonBlocking, prio ? greatest : 0);
+  if (e == cudaSuccess) e = make_streams(r);
   r->ev_v.resize(S);
   r->ev_s.resize(S);
   for (int64_t i = 0; i < S && e == cudaSuccess; ++i) {
@@ -203,6 +188,8 @@ SA_API sa_status sa_runner_destroy(sa_runner* r) {
   for (float* w : r->wlogits) cudaFree(w);
   cudaFree(r->wstats);
   cudaFree(r->qbounds);
+  cudaFree(r->vtrace);
+  cudaFree(r->dtrace);
   for (auto ev : r->ev_v) if (ev) cudaEventDestroy(ev);
   for (auto ev : r->ev_s) if (ev) cudaEventDestroy(ev);
   if (r->ev_fork) cudaEventDestroy(r->ev_fork);
@@ -324,12 +311,8 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   const size_t po_stride = static_cast<size_t>(r->v_units_cap) * 64 * 128;
   const size_t pml_stride = static_cast<size_t>(r->v_units_cap) * 64 * 2;
   const size_t cnt_stride = static_cast<size_t>(r->cfg.max_batch) * r->Hkv;
-  static const bool use_mma_sync = [] {
-    const char* v = getenv("SA_VERIFY_IMPL");
-    return v && std::string(v) == "mma";
-  }();
   cudaError_t e;
-  if (use_mma_sync) {
+  if (r->dev.verify_impl == 1) {  // dev: the mma.sync baseline kernel (verify.cu)
     p.n_splits = choose_splits(units, r->p_max, 64, 0, r->num_sms, r->v_units_cap, 128, &p.chunk);
     p.part_o = r->v_po;
     p.part_ml = r->v_pml;
@@ -338,35 +321,18 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
   } else {
     // at most one CTA per SM over all units, a single wave (floor: a 149th CTA would run as a
     // second wave); dynamic chunk claiming balances inside a unit
-    static const int chunk_tiles = [] {
-      const char* v = getenv("SA_VERIFY_CHUNK");  // dev tuning knob
-      return v ? std::max(1, atoi(v)) : 2;
-    }();
-    static const int prefetch = [] {
-      const char* v = getenv("SA_VERIFY_PF");  // dev tuning knob
-      return v ? std::min(12, std::max(0, atoi(v))) : 0;
-    }();
-    static const int next_pf = [] {
-      const char* v = getenv("SA_VERIFY_NEXTPF");  // dev tuning knob
-      return v ? std::max(0, atoi(v)) : 0;
-    }();
-    p.next_pf = next_pf;
-    static const int no_prefill = getenv("SA_VERIFY_NOPREFILL") ? 1 : 0;
-    p.no_prefill = no_prefill;
-    static const int static_first = [] {
-      const char* v = getenv("SA_VERIFY_STATIC_FIRST");  // dev tuning knob
-      return v ? atoi(v) : 1;
-    }();
-    p.static_first = static_first;
+    const sa::DevConfig& dv = r->dev;
+    const int chunk_tiles = std::max(1, dv.verify_chunk_tiles);
+    p.next_pf = std::max(0, dv.verify_next_pf);
+    p.no_prefill = dv.verify_no_prefill ? 1 : 0;
+    p.static_first = dv.verify_static_first;
+    p.full_rows = dv.verify_full_rows ? 1 : 0;
     p.chunk_tiles = chunk_tiles;
-    p.prefetch = prefetch;
+    p.prefetch = std::min(12, std::max(0, dv.verify_prefetch));
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
     // split merge: the last n_mergers arrivals of a unit normalise a slice of rows each; their
     // partial rows and the (m, l) table must fit the ring buffers
-    static const int n_mergers = [] {
-      const char* v = getenv("SA_VERIFY_MERGERS");  // dev tuning knob
-      return v ? std::max(1, std::min(8, atoi(v))) : 4;
-    }();
+    const int n_mergers = std::max(1, std::min(8, dv.verify_mergers));
     const int rows_per = (p.M + n_mergers - 1) / n_mergers;
     const int fit = std::max(1, (sa::verify_tc_merge_capacity(p.M) - 128) / (rows_per * 512 + 64 * 8));
     p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, r->num_sms / units),
@@ -379,10 +345,12 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.counters = r->v_cnt + par * cnt_stride * 4;
     p.use_pdl = pdl ? 1 : 0;
     p.next_layer = next_layer;
-    p.trace = dev_verify_trace();
+    p.trace = r->vtrace;
     e = sa::launch_verify_tc(p, r->cache->tmap_k128, r->cache->tmap_v128, s);
   }
   if (e != cudaSuccess) return sa::cuda_fail(e, "verify launch");
+  if (a->k_new)  // the fused append wrote rows [p0, p0 + n_rows): sa_kv_commit_accepted may keep them
+    for (int i = 0; i < r->B; ++i) r->cache->verified_end[r->h_seq[i]] = r->h_p0[i] + a->n_rows;
   return SA_OK;
 }
 
@@ -425,7 +393,9 @@ static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t
   return SA_OK;
 }
 
-static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s, bool pdl = false) {
+// draft_off: this chain's new rows start at p0 + draft_off (0 for the direct API; the iteration's next
+// draft chain starts after the accepted verify rows, sa_iteration_args.accepted)
+static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s, bool pdl = false, int draft_off = 0) {
   if (!a || !a->q || !a->out) return fail(SA_INVALID_ARGUMENT, "draft: null argument");
   if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "draft: no batch bound");
   if (a->layer < 0 || a->layer >= r->cache->n_layers) return fail(SA_OUT_OF_RANGE, "draft: layer out of range");
@@ -434,7 +404,7 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   if (!(a->scale > 0.f)) return fail(SA_INVALID_ARGUMENT, "softmax_stable: scale must be positive");
   if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(SA_INVALID_ARGUMENT, "draft: k_new/v_new");
   for (int i = 0; i < r->B; ++i) {
-    const int64_t need = r->h_p0[i] + a->step - (a->k_new ? 1 : 0);
+    const int64_t need = r->h_p0[i] + draft_off + a->step - (a->k_new ? 1 : 0);
     if (need > r->cache->len[r->h_seq[i]] && !a->k_new)
       return fail(SA_OUT_OF_RANGE, "KvStore: gather indices must be strictly increasing and in range");
   }
@@ -445,6 +415,7 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.Hkv = r->Hkv;
   p.G = r->G;
   p.step = a->step;
+  p.draft_off = draft_off;
   p.seq_ids = r->d_seq;
   p.p0 = r->d_p0;
   p.q = static_cast<const __nv_bfloat16*>(a->q);
@@ -461,30 +432,23 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
      // (the PDL successor gathers while this one computes) and two of 16-CTA clusters do not.
      // Chunks of several rounds (large k) or grids far beyond two waves (many sequences x heads)
      // switch to the streaming mode: one CTA per SM, CS sized to one wave, rounds double-buffered.
-    const int64_t m = r->k_cap + a->step;
+    const int64_t m = r->k_cap + draft_off + a->step;
     const int round_rows = sa::draft_round_rows();
     int cs = -1;
     // at least 4 CTAs per unit while two launches still co-reside at two CTAs per SM: shorter
     // per-CTA chains beat the larger merge (k = 64: 4.27 -> 3.25 us, k = 256: 3.68 -> 3.32 us per
     // launch with CS 1/2 -> 4; CS 8-12 is slower again)
-    static const int min_cs_env = [] {  // dev knob
-      const char* e = std::getenv("SA_DRAFT_MIN_CS");
-      return e ? std::atoi(e) : 0;
-    }();
     int min_cs = 1;
     for (int c : {2, 4})
       if (units * c <= r->num_sms) min_cs = c;
-    if (min_cs_env) min_cs = min_cs_env;
+    if (r->dev.draft_min_cs) min_cs = r->dev.draft_min_cs;
     for (int c : {1, 2, 4, 8, 12, 16})
       if (c >= min_cs && (m + c - 1) / c <= round_rows) {
         cs = c;
         break;
       }
     p.stream = 0;
-    static const int multi_round_max = [] {  // dev knob: rounds allowed in the two-CTA-per-SM mode
-      const char* e = std::getenv("SA_DRAFT_MULTI_ROUNDS");
-      return e ? std::atoi(e) : 3;
-    }();
+    const int multi_round_max = r->dev.draft_multi_rounds;  // rounds allowed in the two-CTA-per-SM mode
     // a few units with a large budget (config 5 k = 4096, config 4's per-GPU shard): several rounds in
     // the two-CTA-per-SM mode, round 0 gathered before the dependency wait and later rounds reusing its
     // buffer.  Fewest rounds first, with a penalty when two successive launches' clusters cannot
@@ -525,8 +489,7 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
     }
     p.n_splits = cs;
     p.chunk = static_cast<int>(((m + cs - 1) / cs + 15) / 16 * 16);
-    static const bool dbg = std::getenv("SA_DRAFT_DEBUG") != nullptr;
-    if (dbg) {
+    if (r->dev.draft_debug) {
       std::fprintf(stderr, "draft: units %lld m %lld -> stream %d cs %d chunk %d | active clusters (stream/non):",
                    static_cast<long long>(units), static_cast<long long>(m), p.stream, cs, p.chunk);
       for (int c : {1, 2, 4, 8, 12, 16})
@@ -537,27 +500,70 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.part_o = r->d_po;
   p.part_ml = r->d_pml;
   p.counters = r->d_cnt;
-  p.trace = dev_draft_trace();
+  p.trace = r->dtrace;
   p.use_pdl = pdl ? 1 : 0;
   cudaError_t e = sa::launch_draft(p, s);
   if (e != cudaSuccess) return sa::cuda_fail(e, "draft launch");
   return SA_OK;
 }
 
-// dev-only: write the verify trace buffer to `path` (after a device sync); 0 on success.
-SA_API int sa_dev_trace_dump(const char* path) {
-  unsigned long long* t = dev_verify_trace();
-  if (!t || !path) return -1;
+// dev-only: write the runner's verify + draft trace buffers to `path` (after a device sync); 0 on success.
+SA_API int sa_dev_trace_dump(sa_runner* r, const char* path) {
+  if (!r || !r->vtrace || !r->dtrace || !path) return -1;
   if (cudaDeviceSynchronize() != cudaSuccess) return -2;
   std::vector<unsigned long long> h(kVTraceWords + kDTraceWords);
-  if (cudaMemcpy(h.data(), t, kVTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -3;
-  if (cudaMemcpy(h.data() + kVTraceWords, dev_draft_trace(), kDTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (cudaMemcpy(h.data(), r->vtrace, kVTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -3;
+  if (cudaMemcpy(h.data() + kVTraceWords, r->dtrace, kDTraceWords * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
     return -3;
   FILE* f = fopen(path, "wb");
   if (!f) return -4;
   fwrite(h.data(), 8, h.size(), f);
   fclose(f);
   return 0;
+}
+
+SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) {
+  if (!r || !name) return fail(SA_INVALID_ARGUMENT, "null argument");
+  sa::DevConfig& d = r->dev;
+  const std::string n(name);
+  const int v = static_cast<int>(value);
+  if (n == "verify_impl") d.verify_impl = v;
+  else if (n == "verify_chunk_tiles") d.verify_chunk_tiles = v;
+  else if (n == "verify_prefetch") d.verify_prefetch = v;
+  else if (n == "verify_next_pf") d.verify_next_pf = v;
+  else if (n == "verify_no_prefill") d.verify_no_prefill = v;
+  else if (n == "verify_static_first") d.verify_static_first = v;
+  else if (n == "verify_mergers") d.verify_mergers = v;
+  else if (n == "verify_full_rows") d.verify_full_rows = v;
+  else if (n == "draft_min_cs") d.draft_min_cs = v;
+  else if (n == "draft_multi_rounds") d.draft_multi_rounds = v;
+  else if (n == "draft_debug") d.draft_debug = v;
+  else if (n == "draft_no_pdl") d.draft_no_pdl = v;
+  else if (n == "iter_skip") d.iter_skip = v;
+  else if (n == "select_batched") d.select_batched = v;
+  else if (n == "stream_priority") {
+    d.stream_priority = v;
+    SA_CUDA_CHECK(cudaDeviceSynchronize());
+    SA_CUDA_CHECK(make_streams(r));
+  } else if (n == "trace") {
+    d.trace = v;
+    if (v && !r->vtrace) {
+      SA_CUDA_CHECK(cudaMalloc(&r->vtrace, kVTraceWords * 8));
+      SA_CUDA_CHECK(cudaMemset(r->vtrace, 0, kVTraceWords * 8));
+      SA_CUDA_CHECK(cudaMalloc(&r->dtrace, kDTraceWords * 8));
+      SA_CUDA_CHECK(cudaMemset(r->dtrace, 0, kDTraceWords * 8));
+    }
+    if (!v) {
+      cudaFree(r->vtrace);
+      cudaFree(r->dtrace);
+      r->vtrace = r->dtrace = nullptr;
+    }
+  } else {
+    return fail(SA_INVALID_ARGUMENT, "unknown dev knob '" + n + "'");
+  }
+  for (auto& kv : r->graphs) cudaGraphExecDestroy(kv.second);  // captured with the old settings
+  r->graphs.clear();
+  return SA_OK;
 }
 
 static sa_status ensure_weight_buffers(sa_runner* r) {  // lazily: only the weights metric needs them
@@ -714,19 +720,14 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
   const auto* kdn = static_cast<const __nv_bfloat16*>(a->kd_new);
   const auto* vdn = static_cast<const __nv_bfloat16*>(a->vd_new);
   // phase selection for timing breakdowns (sa_iteration_args::phases; SA_ITER_SKIP overrides in dev runs)
-  static const int env_skip = [] {
-    const char* v = getenv("SA_ITER_SKIP");
-    return v ? atoi(v) : -1;
-  }();
-  const int skip = env_skip >= 0 ? env_skip : (a->phases ? static_cast<int>(~a->phases & 7u) : 0);
+  const int skip = r->dev.iter_skip >= 0 ? r->dev.iter_skip : (a->phases ? static_cast<int>(~a->phases & 7u) : 0);
   // Selection schedule.  Default: one single-CTA select per layer on the side stream, overlapping the
   // verify chain.  A select CTA needs a whole SM's shared memory, so it waits for a verify CTA of the
   // next layer to exit and then delays a CTA of the layer after; that costs ~39 us over the chain.
-  // Dev knob SA_SELECT_BATCHED=1: the fused-byproduct selections (Collect-2, AllDraft, LastAccepted)
+  // Dev knob select_batched: the fused-byproduct selections (Collect-2, AllDraft, LastAccepted)
   // run as ONE launch after the chain instead, with the layers' CTAs side by side.  It removes those
   // 39 us but adds a ~55 us bubble before the first draft, so measured it is even (1.748 vs 1.742 ms).
-  static const bool batch_env = getenv("SA_SELECT_BATCHED") != nullptr;
-  const bool batch_selects = batch_env && (skip & 2) == 0 && guided && !weights &&
+  const bool batch_selects = r->dev.select_batched && (skip & 2) == 0 && guided && !weights &&
                              r->ld <= sa::select_max_smem_keys() && r->n_slots >= L;
   SA_CUDA_CHECK(cudaEventRecord(r->ev_fork, main));
   SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_fork, 0));
@@ -799,7 +800,8 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
       if (quest && (skip & 2) == 0)  // QuestLike re-selects before every draft forward
         if (sa_status st = quest_select_impl(r, l, l, d.q, main)) return st;
       if ((skip & 4) == 0)
-        if (sa_status st = draft_impl(r, &d, main, /*pdl=*/(j > 1 || l > 0) && !quest && !getenv("SA_DRAFT_NOPDL")))
+        if (sa_status st = draft_impl(r, &d, main, /*pdl=*/(j > 1 || l > 0) && !quest && !r->dev.draft_no_pdl,
+                                      /*draft_off=*/a->accepted + 1))
           return st;
     }
   }
@@ -819,8 +821,17 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
   }
   if (a->strategy == SA_COLLECT2_WEIGHTS)
     if (sa_status st = ensure_weight_buffers(r)) return st;  // (outside any graph capture)
-  if (a->strategy == SA_LAST_ACCEPTED && (a->accepted < 0 || a->accepted > a->gamma))
-    return fail(SA_INVALID_ARGUMENT, "select_last_accepted: row accepted+1 not collected");
+  if (a->accepted < 0 || a->accepted > a->gamma)
+    return fail(SA_INVALID_ARGUMENT, a->strategy == SA_LAST_ACCEPTED ? "select_last_accepted: row accepted+1 not collected"
+                                                                     : "iteration: accepted must be in [0, gamma]");
+  if (a->strategy == SA_QUEST_LIKE && r->comm)
+    return fail(SA_NOT_SUPPORTED, "select_quest: page bounds are not exchanged over a KV-head group (per-GPU heads only)");
+  // the next draft chain writes rows p0+a+1 .. p0+a+gamma: their pages exist before capture / launch
+  for (int i = 0; i < r->B; ++i) {
+    const int64_t end = r->h_p0[i] + a->accepted + 1 + a->gamma;
+    if (end > r->cache->max_context) return fail(SA_LENGTH_ERROR, "KvStore: draft rows past max_context");
+    if (sa_status st = r->cache->reserve(r->h_seq[i], end)) return st;
+  }
   if (r->n_slots < r->cache->n_layers) return fail(SA_INVALID_ARGUMENT, "iteration needs n_layers_buf >= n_layers");
   if (!a->qv || !a->qd || !a->out_v || !a->out_d) return fail(SA_INVALID_ARGUMENT, "iteration: null buffer");
   cudaStream_t main = static_cast<cudaStream_t>(stream);
@@ -836,6 +847,7 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
       }
   if (!a->use_graph) {
     sa_status st = enqueue_iteration(r, a, main);
+    if (st == SA_OK && r->comm) st = sa_comm_check(r->comm);
     if (st == SA_OK && a->mode == SA_PER_LAYER && a->phases && (a->phases & SA_PHASE_VERIFY) &&
         !(a->phases & SA_PHASE_SELECT))
       for (int l = 0; l < r->cache->n_layers; ++l) r->fx_dirty[l] = 1;
@@ -871,6 +883,8 @@ SA_API sa_status sa_iteration_run(sa_runner* r, const sa_iteration_args* a, void
     r->graphs.emplace_back(std::move(key), gexec);
   }
   SA_CUDA_CHECK(cudaGraphLaunch(gexec, main));
+  if (r->comm)  // a dead peer surfaces here (the communicator is aborted, the caller sees SA_NCCL_ERROR)
+    if (sa_status st = sa_comm_check(r->comm)) return st;
   // a verify without its select leaves per-layer sums unconsumed: zero them before the next use
   if (a->mode == SA_PER_LAYER && a->phases && (a->phases & SA_PHASE_VERIFY) && !(a->phases & SA_PHASE_SELECT))
     for (int l = 0; l < r->cache->n_layers; ++l) r->fx_dirty[l] = 1;

@@ -334,16 +334,17 @@ cudaError_t launch_select(const SelectParams& p, cudaStream_t s, int n_slots) {
   if (n_slots > 1 && p.ld_scores > kSmemKeys) return cudaErrorInvalidValue;  // the keys workspace is per launch
   const bool fixed = p.score_fx != nullptr;
   if (p.ld_scores <= kSmemKeys) {
-    static bool attr = false;
+    static std::atomic<uint64_t> attr_mask{0};  // per device (internal.h)
+    int dev = 0;
     const int bytes = static_cast<int>(p.ld_scores * 4);
-    if (!attr) {
+    if (func_attrs_needed(attr_mask, &dev)) {
       cudaError_t e = cudaFuncSetAttribute(select_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            kSmemKeys * 4);
       if (e == cudaSuccess)
         e = cudaFuncSetAttribute(select_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemKeys * 4);
       if (e != cudaSuccess) return e;
-      attr = true;
+      func_attrs_done(attr_mask, dev);
     }
     if (fixed) select_kernel<true, true><<<grid, kSelThreads, bytes, s>>>(p);
     else select_kernel<false, true><<<grid, kSelThreads, bytes, s>>>(p);

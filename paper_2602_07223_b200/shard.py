@@ -52,6 +52,18 @@ def plan(batch: int, n_kv_heads: int, world: int, rank: int) -> Shard:
                  range(hgrp * per_h, (hgrp + 1) * per_h), wh)
 
 
+def plan_heads(batch: int, n_kv_heads: int, world: int, rank: int) -> Shard:
+    """Shard the KV heads over ALL `world` ranks, every rank holding every sequence (the config-4
+    style split: each GPU owns n_kv_heads / world heads of every sequence and their G q-heads).
+    Per-layer selection then needs the exchange over the whole group."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank/world out of range")
+    if n_kv_heads % world:
+        raise ValueError(f"cannot split {n_kv_heads} KV heads over {world} ranks")
+    per_h = n_kv_heads // world
+    return Shard(rank, world, tuple(range(batch)), range(rank * per_h, (rank + 1) * per_h), world)
+
+
 def head_group_ranks(shard: Shard) -> list:
     """Ranks that hold the other KV heads of this rank's sequences."""
     base = (shard.rank // shard.head_group) * shard.head_group

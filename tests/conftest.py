@@ -20,11 +20,21 @@ def oracle():
 
 
 @pytest.fixture(scope="session")
-def ref():
+def _ref_session():
     from oracle.pyoracle import REF_SO, Ref
-    if not os.path.exists(REF_SO):
-        pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
-    return Ref()
+    return Ref() if os.path.exists(REF_SO) else None
+
+
+@pytest.fixture
+def ref(request, _ref_session):
+    """The reference's own TUs (oracle/_ref).  Under the gpu marker a missing oracle is a FAILURE: a
+    parity suite must never pass with its checker silently absent."""
+    if _ref_session is None:
+        msg = "oracle/_ref/libspecattn_ref.so not built (build() compiles it where /root/reference exists)"
+        if request.node.get_closest_marker("gpu") is not None:
+            pytest.fail(msg)
+        pytest.skip(msg)
+    return _ref_session
 
 
 @pytest.fixture(scope="session")

@@ -16,7 +16,7 @@ def rel_err_rows(gpu: np.ndarray, ref: np.ndarray) -> float:
     return float((np.abs(gpu - ref).max(-1) / den).max())
 
 
-def rel_err_elem(gpu: np.ndarray, ref: np.ndarray, tau: float = 1e-2) -> float:
+def rel_err_elem(gpu: np.ndarray, ref: np.ndarray, tau: float = 1e-3) -> float:
     """|gpu-ref| / max(|ref|, tau * max_row|ref|), max over elements."""
     gpu = gpu.reshape(-1, gpu.shape[-1]).astype(np.float64)
     ref = ref.reshape(-1, ref.shape[-1]).astype(np.float64)

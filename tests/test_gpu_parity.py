@@ -277,17 +277,27 @@ def test_draft_parity(cuda, ref, mode):
 
 # ----------------------------------------------------------------------------------- iteration
 
-@pytest.mark.parametrize("strategy,mode,use_graph,accepted", [(COLLECT2, 0, True, 0), (ALL_DRAFT, 1, False, 0),
-                                                                (LAST_ACCEPTED, 0, True, 2)])
-def test_iteration_parity(cuda, ref, strategy, mode, use_graph, accepted):
+ITERATION_CASES = [(COLLECT2, 0, True, 0, 0), (ALL_DRAFT, 1, False, 0, 0), (LAST_ACCEPTED, 0, True, 2, 0),
+                   (COLLECT2, 0, True, 4, 0),
+                   # the batched selection schedule (dev knob select_batched: every layer's top-k in one
+                   # grid-z launch after the verify chain, one dependency edge into the draft chain)
+                   (COLLECT2, 0, True, 1, 1), (ALL_DRAFT, 1, False, 3, 1), (LAST_ACCEPTED, 0, True, 2, 1)]
+
+
+@pytest.mark.parametrize("strategy,mode,use_graph,accepted,batched", ITERATION_CASES)
+def test_iteration_parity(cuda, ref, strategy, mode, use_graph, accepted, batched):
     """One full speculation iteration (verify -> select -> gamma drafts, all layers) through
-    sa_iteration_run vs the reference composition (SURVEY.md §8d unit of work)."""
+    sa_iteration_run vs the reference composition (SURVEY.md §8d unit of work).  The draft phase is the
+    next draft chain after accepting a = `accepted` drafts: its rows go to p0+a+1.. and its tail is
+    [p0, p0+a+1+j); the commit afterwards keeps the verify's rows p0..p0+a."""
     torch = cuda
     Runner, _, selection_k = _lib()
     L, Hkv, G, gamma, p0 = 3, 2, 4, 4, 1200
     R, Hq = gamma + 1, Hkv * G
     m = Matched(ref, L=L, Hkv=Hkv, n_tokens=p0, seed=81, max_context=p0 + 64, page_size=128)
     r = Runner(m.cache, Hq, max_rows=R, max_prefix=p0, sparse_ratio=0.07, k_min=16)
+    if batched:
+        r.set_dev_knob("select_batched", 1)
     r.set_batch([0], [p0])
     qv = normal_bf16(82, 1, (L, 1, Hq, R, D))
     kvn, vvn = normal_bf16(82, 2, (L, 1, R, Hkv, D)), normal_bf16(82, 3, (L, 1, R, Hkv, D))
@@ -325,12 +335,25 @@ def test_iteration_parity(cuda, ref, strategy, mode, use_graph, accepted):
                 assert len(want) == len(got) and len(set(want.tolist()) ^ set(got.tolist())) <= 2
             sets.append(got.astype(np.int64))
         sets_by_layer.append(sets)
-    kv.truncate(p0)
+    # the next draft chain: the reference keeps [y, x1..xa] (p0..p0+a), then appends the draft rows; the
+    # draft query of step j attends to T and the tail [p0, p0+a+1+j)
+    a = accepted
+    kv.truncate(p0 + a + 1)
     for j in range(1, gamma + 1):
         kv.append(kdn[j - 1, :, 0].reshape(L * Hkv, D), vdn[j - 1, :, 0].reshape(L * Hkv, D))
         for layer in range(L):
-            o_ref = kv.draft_layer(layer, Hq, qd[j - 1, layer, 0], sets_by_layer[layer], p0, j, SCALE, threads=8)
+            o_ref = kv.draft_layer(layer, Hq, qd[j - 1, layer, 0], sets_by_layer[layer], p0, a + 1 + j, SCALE,
+                                   threads=8)
             assert rel_err_rows(od[j - 1, layer, 0], o_ref) < 2e-4, (j, layer)
+            assert rel_err_elem(od[j - 1, layer, 0], o_ref) < 2e-3, (j, layer)
+    # commit a: the store keeps the verify's rows p0..p0+a, not the draft chain's provisional rows
+    m.cache.commit_accepted(p0, a)
+    assert m.cache.size() == p0 + a + 1
+    for layer in range(L):
+        for h in range(Hkv):
+            K, V = m.cache.read(layer, h, p0, a + 1)
+            assert np.array_equal(K.cpu().numpy(), kvn[layer, 0, : a + 1, h]), (layer, h)
+            assert np.array_equal(V.cpu().numpy(), vvn[layer, 0, : a + 1, h]), (layer, h)
 
 
 # ----------------------------------------------------------------------------------- sharding
@@ -608,7 +631,8 @@ def test_iteration_baseline_strategies(cuda, ref, strategy):
     for layer in range(L):  # verify outputs are strategy-independent
         o_ref, _ = kv.verify_layer(layer, Hq, qv[layer, 0], p0, R, SCALE, want_logits=False, threads=8)
         assert rel_err_rows(out_v.cpu().numpy()[layer, 0], o_ref) < 2e-4
-    kv.truncate(p0)
+    a = 0  # sa_iteration_args.accepted: the next draft chain starts at p0 + a + 1 (after y)
+    kv.truncate(p0 + a + 1)
     od = out_d.cpu().numpy()
     for j in range(1, gamma + 1):
         kv.append(kdn[j - 1, :, 0].reshape(L * Hkv, D), vdn[j - 1, :, 0].reshape(L * Hkv, D))
@@ -617,8 +641,9 @@ def test_iteration_baseline_strategies(cuda, ref, strategy):
                 T = ref_select_window(ref, p0, 4, k - 4)
             else:  # the set the reference picks from this step's query (summaries over the store)
                 T = kv.select_quest(qd[j - 1, layer, 0], layer, p0, 0.07, 16)
-            o_ref = kv.draft_layer(layer, Hq, qd[j - 1, layer, 0], [T], p0, j, SCALE, threads=8)
-            assert rel_err_rows(od[j - 1, layer, 0], o_ref) < 2e-3, (j, layer)
+            o_ref = kv.draft_layer(layer, Hq, qd[j - 1, layer, 0], [T], p0, a + 1 + j, SCALE, threads=8)
+            assert rel_err_rows(od[j - 1, layer, 0], o_ref) < 2e-4, (j, layer)
+            assert rel_err_elem(od[j - 1, layer, 0], o_ref) < 2e-3, (j, layer)
     idx, cnt = r.selection(L - 1, 1)
     assert cnt[0, 0] == k
 
@@ -923,18 +948,3 @@ def test_full_size_verify_select_draft(cuda, ref, Hkv, G, R, p0, kfix):
         got = o.cpu().numpy()[0]
         assert rel_err_rows(got, o_ref) < 2e-4, (step, rel_err_rows(got, o_ref))
         assert rel_err_elem(got, o_ref) < 2e-3
-
-
-def test_iteration_parity_batched_selects(cuda):
-    """The batched selection schedule (SA_SELECT_BATCHED=1: every layer's top-k in one grid-z launch
-    after the verify chain, one dependency edge into the draft chain) passes the same iteration
-    parity cases.  The knob is read once per process, so the cases run in a child pytest."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SA_SELECT_BATCHED="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        "tests/test_gpu_parity.py::test_iteration_parity"], cwd=root, env=env,
-                       capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

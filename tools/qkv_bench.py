@@ -1,3 +1,4 @@
+import os
 """Producer timing: L chained projections (graph, PDL) at the Llama-3.1-8B shape; prints JSON."""
 import json
 import sys
@@ -13,6 +14,8 @@ def main():
     w = (torch.randn(L, n_out, D, device="cuda") / 64).to(torch.bfloat16)
     gain = torch.ones(L, D, device="cuda")
     proj = QkvProjection(w, gain, Hq, Hkv)
+    if os.environ.get("SA_QKV_DEV"):  # tool parameter -> dev knob
+        proj.set_dev_knob("dev", int(os.environ["SA_QKV_DEV"]))
     out = {}
     for B, rows in ((1, 5), (1, 1), (4, 5), (16, 5)):
         x = torch.randn(B, rows, D, device="cuda")

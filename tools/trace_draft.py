@@ -1,4 +1,4 @@
-"""Dev tool: draft-phase CTA timeline inside the config-2 iteration graph (SA_TRACE=1).
+"""Dev tool: draft-phase CTA timeline inside the config-2 iteration graph (knob "trace").
   SA_ITER_SKIP=3 python tools/trace_draft.py     # drafts only (selections from an earlier run)
 Per draft launch (step, layer): first CTA start, median start, median 'loaded' (after the PDL wait),
 median 'computed', max end (us relative to the first draft start)."""
@@ -11,7 +11,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SA_TRACE"] = "1"
 import torch  # noqa: E402
 
 from paper_2602_07223_b200 import COLLECT2, Cache, Runner  # noqa: E402
@@ -26,6 +25,9 @@ for s in range(0, p0, 2048):
     cache.append(kk, kk)
 KFIX = int(os.environ.get("K_FIX", 0))  # fixed budget k (config 5 sweep points)
 r = Runner(cache, Hq, max_rows=R, max_prefix=p0, **({"sparse_ratio": 1e-9, "k_min": KFIX} if KFIX else {}))
+r.set_dev_knob("trace", 1)  # dev-only knobs (the library never reads the environment)
+if os.environ.get("SA_ITER_SKIP"):
+    r.set_dev_knob("iter_skip", int(os.environ["SA_ITER_SKIP"]))
 r.set_batch([0], [p0])
 
 
@@ -48,9 +50,7 @@ with torch.cuda.stream(st):
         r.iteration(args, stream=st)
 torch.cuda.synchronize()
 path = "/tmp/sa_trace_draft.bin"
-f = lib().sa_dev_trace_dump
-f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
-assert f(path.encode()) == 0
+assert r.trace_dump(path) == 0
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 dr = raw[1024 + 64 * 16384:].reshape(8, 64, 512, 16)
 t0 = None

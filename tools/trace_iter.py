@@ -1,4 +1,4 @@
-"""Dev tool: per-layer verify CTA timeline inside the config-2 iteration graph (SA_TRACE=1).
+"""Dev tool: per-layer verify CTA timeline inside the config-2 iteration graph (knob "trace").
   SA_ITER_SKIP=6 python tools/trace_iter.py      # verify-only graph
 Prints, per layer: first CTA start, median / max main-loop end, median / max CTA end (us, relative
 to layer 0's first start)."""
@@ -11,7 +11,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SA_TRACE"] = "1"
 import torch  # noqa: E402
 
 from paper_2602_07223_b200 import COLLECT2, Cache, Runner  # noqa: E402
@@ -25,6 +24,9 @@ for s in range(0, p0, 2048):
     kk = torch.randn((2048, L * Hkv, D), device="cuda").to(torch.bfloat16)
     cache.append(kk, kk)
 r = Runner(cache, Hq, max_rows=R, max_prefix=p0)
+r.set_dev_knob("trace", 1)  # dev-only knobs (the library never reads the environment)
+if os.environ.get("SA_ITER_SKIP"):
+    r.set_dev_knob("iter_skip", int(os.environ["SA_ITER_SKIP"]))
 r.set_batch([0], [p0])
 
 
@@ -45,10 +47,7 @@ with torch.cuda.stream(st):
 torch.cuda.synchronize()
 path = "/tmp/sa_trace_iter.bin"
 
-f = lib().sa_dev_trace_dump
-f.restype = ctypes.c_int
-f.argtypes = [ctypes.c_char_p]
-assert f(path.encode()) == 0
+assert r.trace_dump(path) == 0
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 t0 = None
 print(f"{'layer':>5s} {'start':>8s} {'st_med':>8s} {'loop_med':>8s} {'loop_max':>8s} {'end_med':>8s} {'end_max':>8s} {'dt':>7s}"

@@ -1,4 +1,4 @@
-"""Dev tool: producer CTA timeline (SA_QKV_TRACE=1) for L chained projections (graph, PDL).
+"""Dev tool: producer CTA timeline (knob "trace") for L chained projections (graph, PDL).
 Prints per-layer medians (us) relative to the layer's first CTA start: pdl-wait return, first
 stage landed, MMA loop end, first accumulator ready, partials counted, reducer done, exit."""
 import os
@@ -8,7 +8,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SA_QKV_TRACE"] = "1"
 import torch  # noqa: E402
 
 from paper_2602_07223_b200 import QkvProjection  # noqa: E402
@@ -18,6 +17,7 @@ B, rows = int(os.environ.get("B", 1)), int(os.environ.get("ROWS", 5))
 n_out = (Hq + 2 * Hkv) * 128
 w = (torch.randn(L, n_out, D, device="cuda") / 64).to(torch.bfloat16)
 proj = QkvProjection(w, torch.ones(L, D, device="cuda"), Hq, Hkv)
+proj.set_dev_knob("trace", 1)
 x = torch.randn(B, rows, D, device="cuda")
 pos = torch.full((B,), 32768, dtype=torch.int32, device="cuda")
 q = torch.empty(B, Hq, rows, 128, dtype=torch.bfloat16, device="cuda")

@@ -1,4 +1,4 @@
-"""Dev tool: verify tail anatomy inside the config-2 iteration graph (SA_TRACE=1, verify-only).
+"""Dev tool: verify tail anatomy inside the config-2 iteration graph (knob "trace", verify-only).
 For each layer and unit, times (us) relative to the unit's median main-loop end of: the last main-loop
 end, the last arrival's PV done / partial stored / arrival counted, the mergers' merge done, and the
 CTA ends; printed as medians over units and layers (layers 2.. of the chain)."""
@@ -11,8 +11,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SA_TRACE"] = "1"
-os.environ.setdefault("SA_ITER_SKIP", "6")
+os.environ.setdefault("SA_ITER_SKIP", "6")  # tool parameter -> knob iter_skip
 import torch  # noqa: E402
 
 from paper_2602_07223_b200 import COLLECT2, Cache, Runner  # noqa: E402
@@ -26,6 +25,9 @@ for s in range(0, p0, 2048):
     kk = torch.randn((2048, L * Hkv, D), device="cuda").to(torch.bfloat16)
     cache.append(kk, kk)
 r = Runner(cache, Hq, max_rows=R, max_prefix=p0)
+r.set_dev_knob("trace", 1)  # dev-only knobs (the library never reads the environment)
+if os.environ.get("SA_ITER_SKIP"):
+    r.set_dev_knob("iter_skip", int(os.environ["SA_ITER_SKIP"]))
 r.set_batch([0], [p0])
 
 
@@ -45,9 +47,7 @@ with torch.cuda.stream(st):
         r.iteration(args, stream=st)
 torch.cuda.synchronize()
 path = "/tmp/sa_trace_tail.bin"
-f = lib().sa_dev_trace_dump
-f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
-assert f(path.encode()) == 0
+assert r.trace_dump(path) == 0
 raw = np.fromfile(path, dtype=np.uint64).astype(np.int64)
 rows = []
 for l in range(2, min(L, 64)):

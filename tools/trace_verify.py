@@ -1,4 +1,4 @@
-"""Dev tool: config-2 verify of one layer with SA_TRACE set, after 3 other layers have streamed
+"""Dev tool: config-2 verify of one layer with the "trace" knob set, after 3 other layers have streamed
 through L2 (so the traced layer is read from DRAM): CTA start / main-loop end / end and the per-tile
 pipeline timeline of CTA 0."""
 import ctypes
@@ -9,7 +9,6 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["SA_TRACE"] = "1"
 import torch  # noqa: E402
 
 from paper_2602_07223_b200 import Cache, Runner  # noqa: E402
@@ -21,6 +20,9 @@ for s in range(0, p0, 4096):
     kk = torch.randn((4096, L * Hkv, 128), device="cuda").to(torch.bfloat16)
     cache.append(kk, kk)
 r = Runner(cache, Hq, max_rows=R, max_prefix=p0)
+r.set_dev_knob("trace", 1)  # dev-only knobs (the library never reads the environment)
+if os.environ.get("SA_ITER_SKIP"):
+    r.set_dev_knob("iter_skip", int(os.environ["SA_ITER_SKIP"]))
 r.set_batch([0], [p0])
 q = torch.randn((1, Hq, R, 128), device="cuda").to(torch.bfloat16)
 kn = torch.randn((1, R, Hkv, 128), device="cuda").to(torch.bfloat16)
@@ -31,9 +33,7 @@ for it in range(2):
 torch.cuda.synchronize()
 dump = "/tmp/sa_trace_verify.bin"
 
-f = lib().sa_dev_trace_dump
-f.restype, f.argtypes = ctypes.c_int, [ctypes.c_char_p]
-assert f(dump.encode()) == 0
+assert r.trace_dump(dump) == 0
 raw = np.fromfile(dump, dtype=np.uint64).astype(np.int64)
 ev = raw[:1024].reshape(16, 64)
 se = raw[1024:1024 + 16384].reshape(1024, 16)
