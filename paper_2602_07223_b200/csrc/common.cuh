@@ -442,6 +442,11 @@ __device__ __forceinline__ void st_async_v4(uint32_t remote_addr, float4 v, uint
                "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(remote_bar)
                : "memory");
 }
+__device__ __forceinline__ void st_async_v2(uint32_t remote_addr, float x, float y, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(remote_addr),
+               "f"(x), "f"(y), "r"(remote_bar)
+               : "memory");
+}
 __device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr),
                "r"(__float_as_uint(v)), "r"(remote_bar)

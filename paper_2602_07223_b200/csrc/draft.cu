@@ -25,9 +25,16 @@ namespace sa {
 
 // Swap-AB mma.sync flash step for <= 8 query rows (the G q-heads of one KV head):
 //   S^T(16 tok x 8 rows) = K(16x128) Q^T            8 x mma.m16n8k16 per 16 tokens
-//   O^T(128 d x 8 rows) += V^T(128 x 16 tok) P^T      8 d-blocks x (hi, lo) = 16 mma per 16 tokens
+//   O^T(128 d x 8 rows) += V^T(128 x 16 tok) P^T      8 d-blocks x (hi, mid, lo) = 24 mma per 16 tokens
 // Thread (gid = lane/4, t4 = lane%4) holds S^T for tokens gid / gid+8 and query rows 2*t4, 2*t4+1;
 // P^T is re-laid out as the B operand with movmatrix (8x8 transpose), so no shared-memory trip.
+//
+// kPack (G <= 4): the four real query rows use only half of the n8 tile, so the P planes share it:
+// B columns 0-3 carry P_hi of rows 0-3 and columns 4-7 P_mid of the same rows (one mma), and a second
+// mma adds P_lo into columns 0-3 — 16 instead of 24 PV mma per 16 tokens.  Lanes with t4 >= 2 then
+// track the running max of rows 2*t4-4+e (their accumulator columns hold those rows' P_mid terms), and
+// finalize() folds columns 4-7 into 0-3.
+template <bool kPack>
 struct DraftWarp {
   float o[8][4];     // O^T accumulators: d-block jj rows gid / gid+8, query rows 2t4 / 2t4+1
   float m[2], l[2];  // running max (scaled log2) and per-thread partial sums of rows 2t4, 2t4+1
@@ -89,6 +96,13 @@ struct DraftWarp {
       tmax[0] = fmaxf(tmax[0], __shfl_xor_sync(0xffffffffu, tmax[0], off));
       tmax[1] = fmaxf(tmax[1], __shfl_xor_sync(0xffffffffu, tmax[1], off));
     }
+    if (kPack) {  // lanes t4 >= 2 follow rows 2*t4-4+e (the P_mid columns they accumulate)
+      const float x0 = __shfl_xor_sync(0xffffffffu, tmax[0], 2), x1 = __shfl_xor_sync(0xffffffffu, tmax[1], 2);
+      if ((lane & 3) >= 2) {
+        tmax[0] = x0;
+        tmax[1] = x1;
+      }
+    }
     float mnew[2];
     bool grow = false;
 #pragma unroll
@@ -121,26 +135,39 @@ struct DraftWarp {
       split3_bf16(p0, p1, h01, m01, l01);  // token gid,   rows 2t4, 2t4+1
       split3_bf16(p2, p3, h23, m23, l23);  // token gid+8
       // B fragments of P^T (k = tokens, n = rows): 8x8 transposes of the two token halves
-      const uint32_t bh0 = movmatrix_trans(h01), bh1 = movmatrix_trans(h23);
+      uint32_t bh0 = movmatrix_trans(h01), bh1 = movmatrix_trans(h23);
       const uint32_t bm0 = movmatrix_trans(m01), bm1 = movmatrix_trans(m23);
-      const uint32_t bl0 = movmatrix_trans(l01), bl1 = movmatrix_trans(l23);
+      uint32_t bl0 = movmatrix_trans(l01), bl1 = movmatrix_trans(l23);
+      if (kPack) {  // columns 4-7 <- P_mid of rows 0-3 (held by lane ^ 16 after the transpose); P_lo: 0-3
+        const uint32_t x0 = __shfl_xor_sync(0xffffffffu, bm0, 16), x1 = __shfl_xor_sync(0xffffffffu, bm1, 16);
+        if (gid >= 4) {
+          bh0 = x0;
+          bh1 = x1;
+          bl0 = bl1 = 0u;
+        }
+      }
       const int tok = r0[bi] + (mi >> 1) * 8 + (lane & 7);
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {  // one V fragment load serves the three P planes
         uint32_t a[4];
         ldsm_x4_t(v_smem[bi] + swz(tok, 2 * jj + (mi & 1), half), a[0], a[1], a[2], a[3]);
         mma_bf16(o[jj], a, bh0, bh1);
-        mma_bf16(o[jj], a, bm0, bm1);
+        if (!kPack) mma_bf16(o[jj], a, bm0, bm1);
         mma_bf16(o[jj], a, bl0, bl1);
       }
     }
   }
 
-  __device__ __forceinline__ void finalize_l() {
+  __device__ __forceinline__ void finalize() {
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) l[e] += __shfl_xor_sync(0xffffffffu, l[e], off);
+    if (kPack)  // fold the P_mid columns 4-7 into rows 0-3 (lanes t4 < 2)
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[jj][i] += __shfl_xor_sync(0xffffffffu, o[jj][i], 2);
   }
 };
 
@@ -184,6 +211,11 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
       const size_t launch = static_cast<size_t>((p.step - 1) & 7) * 64 + (p.layer & 63);
       p.trace[(launch * 512 + cta) * 16 + phase] = gt;
+      if (phase == 0) {  // slot 15: the SM this CTA runs on
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[(launch * 512 + cta) * 16 + 15] = smid;
+      }
     }
   }
 }
@@ -201,7 +233,7 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
 // of the G x 128 outputs; every CTA pushes its partial slices and (m, l) into the owners' inboxes
 // with st.async (remote shared-memory stores completing as transaction bytes on the owner's
 // mbarrier), and each owner combines its slice once its inbox is full.
-template <bool kStream>
+template <bool kStream, bool kPack>
 __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kernel(const DraftParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -311,6 +343,16 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
         }
       }
   }
+  // the query and this step's new row are produced by the previous layer: pull their lines into L2
+  // now (L2 is the point of coherence, so a line the producer is still writing cannot go stale) and
+  // read them only after the wait
+  if (split == 0 && tid < 32) {
+    const __nv_bfloat16* src = nullptr;
+    if (tid < 2 * p.G) src = p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128 + tid * 64;
+    else if (p.k_new && tid < 2 * p.G + 4)
+      src = ((tid - 2 * p.G) < 2 ? p.k_new : p.v_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128 + (tid & 1) * 64;
+    if (src) prefetch_l2_bulk(src, 128);
+  }
   pdl_wait();  // previous layer complete: q and this step's new row are valid
   pdl_launch_dependents();
   dtrace(p, 1);
@@ -344,7 +386,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
     const int v2 = v_begin + kRoundRows + tid;
     if (tid < kRoundRows && v2 < min(v_end, k)) tq = __ldg(T + v2);
   }
-  DraftWarp w;
+  DraftWarp<kPack> w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
   const bool dbuf = kStream && n_rounds > 1;  // double-buffered rounds (streaming mode)
   auto issue_round = [&](int round, int buf) {  // every row of a later round (after the wait)
@@ -414,7 +456,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
     }
     if (dbuf && round + 2 < n_rounds) issue_round(round + 2, buf);
   }
-  w.finalize_l();
+  w.finalize();
   dtrace(p, 3);
 
   // in-CTA merge of the warps' partials (only the G real query rows), fused with the push: every
@@ -454,6 +496,26 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
     mbar_arrive_expect_tx(inbox_bar, static_cast<uint32_t>(CS) * (my_vals + 2 * p.G) * 4u);
   }
   const uint32_t inbox_addr = smem_u32(inbox), bar_addr = smem_u32(inbox_bar);
+  // the CTA's per-row (m*, l*) to every owner, by the last warp: lane 8*r + q holds warp q's (m, l) of
+  // row base + r; three xor levels give the row max and the rescaled sum (fixed tree order:
+  // deterministic), then lane 8*r + j pushes the (m*, l*) pair of its row to owners j and j + 8
+  if (warp == nwarps - 1) {
+    for (int base = 0; base < p.G; base += 4) {
+      const int row = base + (lane >> 3), q = lane & 7;
+      const bool ok = row < p.G && q < nwarps;
+      const float mq = ok ? wml[q * 16 + row] : -INFINITY;
+      float ms = mq;
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) ms = fmaxf(ms, __shfl_xor_sync(0xffffffffu, ms, off));
+      float ls = (ok && mq != -INFINITY) ? wml[q * 16 + 8 + row] * fast_exp2(mq - ms) : 0.f;
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
+      if (row < p.G)
+        for (int o = q; o < CS; o += 8)
+          st_async_v2(mapa_shared(inbox_addr + (split * rstride + per + 2 * row) * 4, o), ms, ls,
+                      mapa_shared(bar_addr, o));
+    }
+  }
   for (int q4 = tid; q4 < n_out / 4; q4 += nthr) {
     const int e = q4 * 4, row = e >> 7, col = e & 127;
     float mq[DCfg::kMaxWarps];
@@ -463,7 +525,6 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
 #pragma unroll
     for (int q = 0; q < DCfg::kMaxWarps; ++q) mstar = fmaxf(mstar, mq[q]);
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    float lsum = 0.f;
 #pragma unroll
     for (int q = 0; q < DCfg::kMaxWarps; ++q) {  // fixed warp order: deterministic
       if (q < nwarps) {
@@ -473,18 +534,11 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
         v.y += x.y * f;
         v.z += x.z * f;
         v.w += x.w * f;
-        if (col == 0) lsum += wml[q * 16 + 8 + row] * f;
       }
     }
     const int owner = e / per;
     st_async_v4(mapa_shared(inbox_addr + (split * rstride + (e - owner * per)) * 4, owner), v,
                 mapa_shared(bar_addr, owner));
-    if (col == 0)  // this row's (m*, l*) to every owner
-      for (int o = 0; o < CS; ++o) {
-        const uint32_t ob = mapa_shared(bar_addr, o);
-        st_async_f32(mapa_shared(inbox_addr + (split * rstride + per + row) * 4, o), mstar, ob);
-        st_async_f32(mapa_shared(inbox_addr + (split * rstride + per + 8 + row) * 4, o), lsum, ob);
-      }
   }
   // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45), off the
   // critical path: this launch reads the row from k_new / v_new; later steps of this layer gather it
@@ -507,8 +561,8 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
 #pragma unroll
     for (int s2 = 0; s2 < DCfg::kMaxCS; ++s2) {
       const bool ok = s2 < CS;
-      ms[s2] = ok ? inbox[s2 * rstride + per + row] : -INFINITY;
-      ls[s2] = ok ? inbox[s2 * rstride + per + 8 + row] : 0.f;
+      ms[s2] = ok ? inbox[s2 * rstride + per + 2 * row] : -INFINITY;
+      ls[s2] = ok ? inbox[s2 * rstride + per + 2 * row + 1] : 0.f;
       os[s2] = ok ? inbox[s2 * rstride + off] : 0.f;
     }
     float mstar = -INFINITY;
@@ -526,17 +580,22 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   dtrace(p, 4);
 }
 
+template <bool kStream, bool kPack>
+static cudaError_t draft_set_attrs_one() {
+  cudaError_t e = cudaFuncSetAttribute(draft_kernel<kStream, kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kStream ? DCfg::kSmemStream : DCfg::kSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(draft_kernel<kStream, kPack>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
+
 static cudaError_t draft_set_attrs() {
   static std::atomic<uint64_t> attr_mask{0};
   int dev = 0;
   if (func_attrs_needed(attr_mask, &dev)) {
-    cudaError_t e = cudaFuncSetAttribute(draft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg::kSmem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(draft_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(draft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DCfg::kSmemStream);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(draft_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaError_t e = draft_set_attrs_one<false, false>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<false, true>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<true, false>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<true, true>();
     if (e != cudaSuccess) return e;
     func_attrs_done(attr_mask, dev);
   }
@@ -568,8 +627,8 @@ int draft_max_active_clusters(int stream, int cs) {
     attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    if ((stream ? cudaOccupancyMaxActiveClusters(&n, draft_kernel<true>, &cfg)
-                : cudaOccupancyMaxActiveClusters(&n, draft_kernel<false>, &cfg)) != cudaSuccess) {
+    if ((stream ? cudaOccupancyMaxActiveClusters(&n, draft_kernel<true, false>, &cfg)
+                : cudaOccupancyMaxActiveClusters(&n, draft_kernel<false, false>, &cfg)) != cudaSuccess) {
       cudaGetLastError();
       n = 0;
     }
@@ -595,7 +654,10 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   attrs[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = p.use_pdl ? 2 : 1;
-  return p.stream ? cudaLaunchKernelEx(&cfg, draft_kernel<true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<false>, p);
+  const bool pack = p.G <= 4;  // P_hi | P_mid share one n8 tile (DraftWarp<true>)
+  if (p.stream)
+    return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<true, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<true, false>, p);
+  return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<false, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<false, false>, p);
 }
 
 int draft_max_splits() { return DCfg::kMaxCS; }

@@ -94,6 +94,8 @@ struct DevConfig {
   int verify_static_first = 1;  // first chunk = split index (else every chunk claimed from the counter)
   int verify_mergers = 4;       // CTAs (last arrivals of a unit) that split the merge's rows
   int verify_full_rows = 0;     // softmax over all N MMA columns instead of MR = roundup4(M)
+  int verify_max_splits = 0;    // cap on CTAs per (sequence, KV head) unit (0: automatic)
+  int verify_wait_pf = 0;       // tiles prefetched into L2 ahead of the ring before the dependency wait ends
   int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
   int draft_multi_rounds = 3;   // rounds allowed in the two-CTA-per-SM multi-round mode
   int draft_debug = 0;          // print the draft launch geometry to stderr
@@ -138,6 +140,7 @@ struct VerifyParams {
   int chunk_tiles;  // 128-token tiles per dynamically claimed chunk
   int prefetch;     // tiles prefetched into L2 ahead of the K ring
   int next_pf;      // chunks of the next layer each CTA prefetches into L2 at the end of its stream
+  int wait_pf;      // tiles of its own stream a CTA prefetches into L2 while waiting for the dependency
   int full_rows;    // dev: softmax over all N columns
 };
 

@@ -329,6 +329,7 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.full_rows = dv.verify_full_rows ? 1 : 0;
     p.chunk_tiles = chunk_tiles;
     p.prefetch = std::min(12, std::max(0, dv.verify_prefetch));
+    p.wait_pf = std::min(16, std::max(0, dv.verify_wait_pf));  // the producer's 32-entry position ring
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
     // split merge: the last n_mergers arrivals of a unit normalise a slice of rows each; their
     // partial rows and the (m, l) table must fit the ring buffers
@@ -337,6 +338,7 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     const int fit = std::max(1, (sa::verify_tc_merge_capacity(p.M) - 128) / (rows_per * 512 + 64 * 8));
     p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, r->num_sms / units),
                                                      n_chunks, 128, r->v_units_cap / units, fit}));
+    if (dv.verify_max_splits > 0) p.n_splits = std::min(p.n_splits, dv.verify_max_splits);
     p.n_mergers = n_mergers;
     p.chunk = 0;
     p.chunk_ctr = r->v_chunk + par * cnt_stride;
@@ -535,6 +537,8 @@ SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) 
   else if (n == "verify_static_first") d.verify_static_first = v;
   else if (n == "verify_mergers") d.verify_mergers = v;
   else if (n == "verify_full_rows") d.verify_full_rows = v;
+  else if (n == "verify_max_splits") d.verify_max_splits = v;
+  else if (n == "verify_wait_pf") d.verify_wait_pf = v;
   else if (n == "draft_min_cs") d.draft_min_cs = v;
   else if (n == "draft_multi_rounds") d.draft_multi_rounds = v;
   else if (n == "draft_debug") d.draft_debug = v;

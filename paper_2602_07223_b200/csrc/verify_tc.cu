@@ -52,7 +52,7 @@ struct TCfg {
   static constexpr int kOffP = kOffQ + 2 * kQHalf;     // [wg][planes]
   static constexpr int kOffBar = kOffP + 2 * kPlanes * kPBytes;
   static constexpr int kPosRing = 8;                  // published tile positions (consumer-visible)
-  static constexpr int kNumBars = 2 * kSK + 2 * kSV + 10 + kPosRing + 2;
+  static constexpr int kNumBars = 2 * kSK + 2 * kSV + 8 + kPosRing + 2;
   static constexpr int kOffMisc = kOffBar + kNumBars * 8;
   // misc: tmem slot, flag, ntiles[2] | mref[2][64] fac[2][64] ltot[2][64] wsc[64] lim[64] | red[2][4][64]
   //       | tile_pos[kPosRing] | producer ring pring[32]
@@ -61,9 +61,18 @@ struct TCfg {
                                     kBtMax * 4 + 64 * 4;
   static constexpr int kSmem = kOffMisc + kMiscBytes + 1024;
   static constexpr int kThreads = 384;
-  // TMEM columns: S[2] (N each) then O[2] (kNP each: one N-column block per P plane)
+  // TMEM columns: S[2] (N each), O[2] (kNP each: one N-column block per P plane), then Oacc[2] (N each)
   static constexpr int kOCol = 2 * N;
-  static constexpr uint32_t kTmemCols = (2 * N + 2 * kNP <= 128) ? 128 : (2 * N + 2 * kNP <= 256) ? 256 : 512;
+  static constexpr int kACol = 2 * N + 2 * kNP;
+  static constexpr int kCols = 4 * N + 2 * kNP;
+  static constexpr uint32_t kTmemCols = kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
+  static_assert(kCols <= 512, "TMEM columns");
+  // Accumulation blocks: the tensor core's fp32 accumulate is not IEEE round-to-nearest, so its error
+  // grows with the number of MMAs chained into one accumulator (one CTA streaming a whole 64K prefix,
+  // config 3: 2.6e-2 elementwise against the reference).  Every kFlush tiles of a warpgroup, the
+  // softmax threads fold the O^T planes into Oacc with IEEE fp32 adds and the next PV restarts
+  // the accumulator, so no chain is longer than kFlush * 8 MMAs.
+  static constexpr int kFlush = 16;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
@@ -225,8 +234,9 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* s_empty = s_full + 2;
   uint64_t* p_full = s_empty + 2;
   uint64_t* p_empty = p_full + 2;
-  uint64_t* pv_done = p_empty + 2;
-  uint64_t* pos_bar = pv_done + 2;  // [kPosRing]
+  // p_empty[wg] completes when the PV MMAs of the warpgroup's tile retire (tcgen05.commit after them),
+  // so it also marks "O^T final through that tile"; every phase of it is waited (no stray phases)
+  uint64_t* pos_bar = p_empty + 2;  // [kPosRing]
   uint64_t* dep_bar = pos_bar + C::kPosRing;  // Q staged + window appended (after griddepcontrol.wait)
   uint64_t* merge_bar = dep_bar + 1;          // split merge: partials bulk-loaded into smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::kOffMisc);
@@ -283,7 +293,6 @@ __global__ void __launch_bounds__(384, 1)
       mbar_init(&s_empty[i], 128);
       mbar_init(&p_full[i], 128);
       mbar_init(&p_empty[i], 1);
-      mbar_init(&pv_done[i], 1);
     }
     fence_mbar_init();
   }
@@ -367,9 +376,14 @@ __global__ void __launch_bounds__(384, 1)
                  << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1)));
       };
       int nk = 0, nv = 0, npf = 0;
+      bool released = false;  // griddepcontrol.wait passed (dep_bar): the consumers are running
       while (true) {
-        fill(nk + 1 + prefetch);
-        for (; npf < min(q_end, nv + C::kSV + prefetch) && nk >= 1; ++npf) {  // L2 prefetch
+        // before the dependency is released the ring is full and idle: pull `wait_pf` more tiles of
+        // this CTA's stream into L2 (HBM would otherwise idle through the previous layer's tail)
+        if (!released) released = mbar_test(dep_bar, 0);
+        const int depth = released ? prefetch : max(prefetch, p.wait_pf);
+        fill(nk + 1 + depth);
+        for (; npf < min(q_end, nv + C::kSV + depth) && nk >= 1; ++npf) {  // L2 prefetch
           const int row = row_of(pring[npf & 31]);
           tma_prefetch_l2_2d(&tmk, 0, row);
           tma_prefetch_l2_2d(&tmk, 64, row);
@@ -498,10 +512,9 @@ __global__ void __launch_bounds__(384, 1)
           a[kt] = umma_desc(v_base + kt * 2048, C::kHalf, 1024, kLayoutSW128);
           bp[kt] = umma_desc(p_pl + kt * 512, C::kTile * 32, 256, kLayoutSW32);
         }
-        umma_bf16_x8(o_tm, a, bp, idesc_pv, (u >> 1) > 0 ? 1u : 0u);
+        umma_bf16_x8(o_tm, a, bp, idesc_pv, ((u >> 1) % C::kFlush) != 0 ? 1u : 0u);  // block start: overwrite
         umma_commit_elect(&v_empty[sv]);
         umma_commit_elect(&p_empty[wg]);
-        umma_commit_elect(&pv_done[wg]);
         SA_TRACE(3, u);
       };
       int t = 0;
@@ -551,6 +564,7 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* p_hi = smem + C::kOffP + wg * C::kPlanes * C::kPBytes;
     const uint32_t s_tm = tmem + lane_off + wg * N;
     const uint32_t o_tm = tmem + lane_off + C::kOCol + wg * C::kNP;  // plane q's O^T at +q*N
+    const uint32_t a_tm = tmem + lane_off + C::kACol + wg * N;       // Oacc^T (closed accumulation blocks)
     float l[N];
 #pragma unroll
     for (int m = 0; m < N; ++m) l[m] = 0.f;
@@ -639,7 +653,7 @@ __global__ void __launch_bounds__(384, 1)
           mr[m] = mref[m];
         }
         if (i > 0) {  // O^T of this warpgroup is final through its previous tile once that PV is done
-          mbar_wait(&pv_done[wg], (i - 1) & 1);
+          mbar_wait(&p_empty[wg], (i - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int pl = 0; pl < C::kPlanes; ++pl) {
@@ -649,6 +663,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
             for (int m = 0; m < N; ++m) v[m] *= fac[m];
             tmem_st_n<N>(o_tm + pl * N, v);
+          }
+          if (i > C::kFlush) {  // Oacc holds closed blocks (the first flush ran at i = kFlush)
+            float v[N];
+            tmem_ld_n<N>(a_tm, v);
+            tc_wait_ld();
+#pragma unroll
+            for (int m = 0; m < N; ++m) v[m] *= fac[m];
+            tmem_st_n<N>(a_tm, v);
           }
           tc_wait_st();
         }
@@ -665,6 +687,26 @@ __global__ void __launch_bounds__(384, 1)
       for (int m = 0; m < MR; ++m) l[m] += s[m];
       if (ts == 0) SA_TRACE(8, t);
       if (i > 0) mbar_wait(&p_empty[wg], (i - 1) & 1);  // previous PV finished reading this P plane
+      if (i > 0 && i % C::kFlush == 0) {  // PV(i-1) closed an accumulation block: Oacc (+)= its planes
+        tc_fence_after();
+#pragma unroll
+        for (int c16 = 0; c16 < N / 16; ++c16) {
+          float op[C::kPlanes][16], acc[16];
+#pragma unroll
+          for (int pl = 0; pl < C::kPlanes; ++pl) tmem_ld16(o_tm + pl * N + 16 * c16, op[pl]);
+          if (i > C::kFlush) tmem_ld16(a_tm + 16 * c16, acc);
+          tc_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float v = op[C::kPlanes - 1][j];  // smallest plane first (the epilogue's order)
+#pragma unroll
+            for (int pl = C::kPlanes - 2; pl >= 0; --pl) v += op[pl][j];
+            acc[j] = i > C::kFlush ? v + acc[j] : v;
+          }
+          tmem_st16(a_tm + 16 * c16, acc);
+        }
+        tc_wait_st();
+      }
       if (ts == 0) SA_TRACE(9, t);
       // pass 2b: P^T -> smem as bf16 planes (MN-major SWIZZLE_32B, 16-row atoms: token tk's 8-row
       // chunk ch of atom a at a*4096 + tk*32 + 16*(ch ^ bit 2 of tk))
@@ -710,7 +752,7 @@ __global__ void __launch_bounds__(384, 1)
     const int my_tiles = i;  // tiles this warpgroup processed
     if (ts == 0) ntiles_wg[wg] = my_tiles;
     if (my_tiles > 0) {
-      mbar_wait(&pv_done[wg], (my_tiles - 1) & 1);
+      mbar_wait(&p_empty[wg], (my_tiles - 1) & 1);
       tc_fence_after();
     }
     if (wg == 0 && ts == 0) SA_TSTAMP(4);
@@ -763,6 +805,20 @@ __global__ void __launch_bounds__(384, 1)
         for (int j = 0; j < 16; ++j) {
           if (has0) s0[j] += o0[j];
           if (has1) s1[j] += o1[j];
+        }
+      }
+      // closed accumulation blocks (Oacc) of a warpgroup that ran more than kFlush tiles
+      const bool acc0 = ntiles_wg[0] > C::kFlush, acc1 = ntiles_wg[1] > C::kFlush;
+      if (acc0 || acc1) {
+        float a0[16], a1[16];
+        const uint32_t abase = tmem + lane_off + C::kACol + 16 * c16;
+        if (acc0) tmem_ld16(abase, a0);
+        if (acc1) tmem_ld16(abase + N, a1);
+        tc_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (acc0) s0[j] += a0[j];
+          if (acc1) s1[j] += a1[j];
         }
       }
 #pragma unroll

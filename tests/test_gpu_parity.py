@@ -249,10 +249,12 @@ def test_select_exact_ties_lower_index(cuda, ref):
 
 # ----------------------------------------------------------------------------------- draft
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_draft_parity(cuda, ref, mode):
+# (mode, Hkv, G): G <= 4 runs the packed-plane draft step (P_hi | P_mid share one n8 tile), G = 8 the
+# three-mma one; G = 1 and 3 leave padding columns inside the packed tile
+@pytest.mark.parametrize("mode,Hkv,G", [(0, 8, 4), (1, 8, 4), (0, 2, 1), (0, 4, 3), (1, 2, 8)])
+def test_draft_parity(cuda, ref, mode, Hkv, G):
     torch = cuda
-    Hkv, G, R, p0 = 8, 4, 5, 4096
+    R, p0 = 5, 4096
     m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=71, score_layout=mode)
     n_sets = 1 if mode == 0 else Hkv
     idx, cnt = _gpu_select(r, 1, mode, n_sets, 2)

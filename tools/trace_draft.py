@@ -103,3 +103,23 @@ for j in range(gamma):
             rel_g.setdefault(s_, []).append((blk[c, 2] - med_g) / 1e3)
 print("split: computed-vs-median (us) / gathered-vs-median (us)")
 print(" ".join(f"{s_}:{np.median(rel_c[s_]):+.2f}/{np.median(rel_g[s_]):+.2f}" for s_ in sorted(rel_c)))
+
+# stragglers vs SM sharing: for each launch, CTAs that share their SM with another CTA of the SAME
+# launch, and their 'computed' lag against the launch median
+shared_lag, alone_lag = [], []
+for j in range(gamma):
+    for l in range(2, L):
+        blk = dr[j, l]
+        live = np.nonzero(blk[:, 0] > 0)[0]
+        if not len(live):
+            continue
+        sm = blk[live, 15]
+        med_c = np.median(blk[live, 3])
+        cnt = {s_: int((sm == s_).sum()) for s_ in set(sm.tolist())}
+        for c, s_ in zip(live, sm):
+            (shared_lag if cnt[s_] > 1 else alone_lag).append((blk[c, 3] - med_c) / 1e3)
+if shared_lag or alone_lag:
+    print(f"CTAs sharing an SM with a CTA of the same launch: {len(shared_lag)} "
+          f"(computed lag median {np.median(shared_lag) if shared_lag else float('nan'):+.2f} us, "
+          f"p90 {np.percentile(shared_lag, 90) if shared_lag else float('nan'):+.2f}); alone: {len(alone_lag)} "
+          f"(median {np.median(alone_lag):+.2f}, p90 {np.percentile(alone_lag, 90):+.2f})")
