@@ -96,7 +96,10 @@ struct DevConfig {
   int verify_full_rows = 0;     // softmax over all N MMA columns instead of MR = roundup4(M)
   int verify_max_splits = 0;    // cap on CTAs per (sequence, KV head) unit (0: automatic)
   int verify_wait_pf = 0;       // tiles prefetched into L2 ahead of the ring before the dependency wait ends
+  int verify_tail_tiles = 18;   // single-tile chunks at the end of the prefix (guided claiming)
+  int verify_flush_tiles = 8;   // TMEM accumulation block (warpgroup tiles) folded into Oacc; 0: never
   int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
+  int draft_cs = 0;             // forced CTAs per unit (0: automatic)
   int draft_multi_rounds = 3;   // rounds allowed in the two-CTA-per-SM multi-round mode
   int draft_debug = 0;          // print the draft launch geometry to stderr
   int draft_no_pdl = 0;         // launch iteration drafts without programmatic dependent launch
@@ -141,6 +144,8 @@ struct VerifyParams {
   int prefetch;     // tiles prefetched into L2 ahead of the K ring
   int next_pf;      // chunks of the next layer each CTA prefetches into L2 at the end of its stream
   int wait_pf;      // tiles of its own stream a CTA prefetches into L2 while waiting for the dependency
+  int tail_tiles;   // the last tail_tiles tiles of the prefix are claimed as single-tile chunks
+  int flush_tiles;  // TMEM accumulation block length in a warpgroup's tiles (0: never flush)
   int full_rows;    // dev: softmax over all N columns
 };
 

@@ -329,7 +329,9 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.full_rows = dv.verify_full_rows ? 1 : 0;
     p.chunk_tiles = chunk_tiles;
     p.prefetch = std::min(12, std::max(0, dv.verify_prefetch));
-    p.wait_pf = std::min(16, std::max(0, dv.verify_wait_pf));  // the producer's 32-entry position ring
+    p.wait_pf = std::min(16, std::max(0, dv.verify_wait_pf));
+    p.tail_tiles = std::max(0, dv.verify_tail_tiles);
+    p.flush_tiles = std::max(0, dv.verify_flush_tiles);  // the producer's 32-entry position ring
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
     // split merge: the last n_mergers arrivals of a unit normalise a slice of rows each; their
     // partial rows and the (m, l) table must fit the ring buffers
@@ -489,6 +491,10 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
         }
       }
     }
+    if (r->dev.draft_cs > 0) {  // dev: forced CTAs per unit, two-CTA-per-SM mode (<= 3 rounds)
+      cs = std::min(r->dev.draft_cs, sa::draft_max_splits());
+      p.stream = 0;
+    }
     p.n_splits = cs;
     p.chunk = static_cast<int>(((m + cs - 1) / cs + 15) / 16 * 16);
     if (r->dev.draft_debug) {
@@ -539,7 +545,10 @@ SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) 
   else if (n == "verify_full_rows") d.verify_full_rows = v;
   else if (n == "verify_max_splits") d.verify_max_splits = v;
   else if (n == "verify_wait_pf") d.verify_wait_pf = v;
+  else if (n == "verify_tail_tiles") d.verify_tail_tiles = v;
+  else if (n == "verify_flush_tiles") d.verify_flush_tiles = v;
   else if (n == "draft_min_cs") d.draft_min_cs = v;
+  else if (n == "draft_cs") d.draft_cs = v;
   else if (n == "draft_multi_rounds") d.draft_multi_rounds = v;
   else if (n == "draft_debug") d.draft_debug = v;
   else if (n == "draft_no_pdl") d.draft_no_pdl = v;

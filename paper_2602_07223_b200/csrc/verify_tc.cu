@@ -34,15 +34,16 @@ namespace sa {
 template <int N>
 struct TCfg {
   static constexpr int kTile = 128;
-  static constexpr int kSK = 2;                       // K ring stages (K is recycled right after QK^T)
+  // K ring stages (K is recycled right after QK^T); N = 64 keeps one so the three P planes fit
+  static constexpr int kSK = N <= 48 ? 2 : 1;
   static constexpr int kSV = (N <= 32) ? 3 : 2;       // V ring stages (V is held until PV retires)
   static constexpr int kHalf = kTile * 128;           // one 64-column half of a K or V tile (16 KB)
   static constexpr int kTileBytes = 2 * kHalf;         // K or V tile (32 KB)
   static constexpr int kQHalf = N * 128;
   // P^T planes (bf16, MN-major SWIZZLE_32B, 16-row atoms): P = hi + mid + lo to ~2^-27 relative
-  // (the tau = 1e-3 elementwise bar of SURVEY §8c needs more than the ~2^-17 of hi + lo); N = 64 keeps
-  // two planes (three do not fit shared memory; G*(gamma+1) > 46 is outside the BASELINE configs)
-  static constexpr int kPlanes = N <= 48 ? 3 : 2;
+  // (the tau = 1e-3 elementwise bar of SURVEY §8c needs more than the ~2^-17 of hi + lo: two planes
+  // measured 2.3e-3 at G*(gamma+1) = 56)
+  static constexpr int kPlanes = 3;
   static constexpr int kPAtoms = N / 16;               // 16-row MN atoms of the SW32 P layout
   static constexpr int kPBytes = kPAtoms * kTile * 32; // one P plane (N rows x 128 tokens)
   static constexpr int kNP = kPlanes * N;              // merged PV width: [P_hi | P_mid | P_lo] columns
@@ -64,15 +65,17 @@ struct TCfg {
   // TMEM columns: S[2] (N each), O[2] (kNP each: one N-column block per P plane), then Oacc[2] (N each)
   static constexpr int kOCol = 2 * N;
   static constexpr int kACol = 2 * N + 2 * kNP;
-  static constexpr int kCols = 4 * N + 2 * kNP;
+  static constexpr int kColsBase = 2 * N + 2 * kNP;  // without Oacc (flushing off)
+  static constexpr bool kFlushable = 4 * N + 2 * kNP <= 512;  // Oacc fits TMEM (N <= 48)
+  static constexpr int kCols = kFlushable ? 4 * N + 2 * kNP : kColsBase;
   static constexpr uint32_t kTmemCols = kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
+  static constexpr uint32_t kTmemColsBase = kColsBase <= 128 ? 128 : kColsBase <= 256 ? 256 : 512;
   static_assert(kCols <= 512, "TMEM columns");
   // Accumulation blocks: the tensor core's fp32 accumulate is not IEEE round-to-nearest, so its error
   // grows with the number of MMAs chained into one accumulator (one CTA streaming a whole 64K prefix,
   // config 3: 2.6e-2 elementwise against the reference).  Every kFlush tiles of a warpgroup, the
   // softmax threads fold the O^T planes into Oacc with IEEE fp32 adds and the next PV restarts
-  // the accumulator, so no chain is longer than kFlush * 8 MMAs.
-  static constexpr int kFlush = 16;
+  // the accumulator, so no chain is longer than flush * 8 MMAs (p.flush_tiles; 0: one block per CTA).
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
 };
 
@@ -273,7 +276,14 @@ __global__ void __launch_bounds__(384, 1)
   const int win_lo = n_pref * C::kTile;
   const int n_win = (p0 + R - win_lo + C::kTile - 1) / C::kTile;
   const int chunk_tiles = p.chunk_tiles, prefetch = p.prefetch;
-  const int n_chunks = (n_pref + chunk_tiles - 1) / chunk_tiles;
+  // chunks: n_big chunks of chunk_tiles tiles, then single-tile chunks for the last n_tail tiles of the
+  // prefix (claims are monotonic, so the final claims of every CTA are small: less loop-end spread)
+  // (short prefixes keep whole chunks: every chunk is then a CTA's static first one, no claims)
+  const int n_tail_t = min(p.tail_tiles, max(0, n_pref - 2 * p.n_splits));
+  const int n_big = (n_pref - n_tail_t) / chunk_tiles;
+  const int n_chunks = n_big + (n_pref - n_big * chunk_tiles);
+  auto chunk_start = [&](int c) { return c < n_big ? c * chunk_tiles : n_big * chunk_tiles + (c - n_big); };
+  auto chunk_len = [&](int c) { return c < n_big ? chunk_tiles : 1; };
   const int unit = b * p.Hkv + g;
   // ------------------------------------------------------------------ prologue (all threads)
   if (tid == 0) {
@@ -313,7 +323,11 @@ __global__ void __launch_bounds__(384, 1)
                           static_cast<int>(p.ld_logits)
                     : -1;
   }
-  if (warp == 1) tmem_alloc(tmem_slot, C::kTmemCols);
+  // accumulation block length (tiles); N = 64 has no TMEM room for Oacc (one block per CTA)
+  const bool flushing = C::kFlushable && p.flush_tiles > 0;
+  const int flush = flushing ? p.flush_tiles : (1 << 30);
+  const uint32_t tmem_cols = flushing ? C::kTmemCols : C::kTmemColsBase;
+  if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(384, 1)
       bool exhausted = false, done = false, dep_seen = false, win_added = false;
       auto fill = [&](int upto) {
         while (q_end < upto && !exhausted) {
-          if (cur_chunk < 0 || cur_tile == min(chunk_tiles, n_pref - cur_chunk * chunk_tiles)) {
+          if (cur_chunk < 0 || cur_tile == chunk_len(cur_chunk)) {
             if (last && claims == 1 && !win_added) {  // window tiles go right after the first chunk
               for (int w2 = 0; w2 < n_win; ++w2) pring[q_end++ & 31] = win_lo + w2 * C::kTile;
               win_added = true;
@@ -362,7 +376,7 @@ __global__ void __launch_bounds__(384, 1)
             }
             cur_tile = 0;
           }
-          pring[q_end++ & 31] = (cur_chunk * chunk_tiles + cur_tile++) * C::kTile;
+          pring[q_end++ & 31] = (chunk_start(cur_chunk) + cur_tile++) * C::kTile;
         }
         if (exhausted && !done) {  // (short prefixes: the window tiles close the stream)
           if (last && !win_added)
@@ -428,8 +442,8 @@ __global__ void __launch_bounds__(384, 1)
       // layer's CTAs claim first)
       if (p.next_layer >= 0)
         for (int c = split, i = 0; i < p.next_pf && c < n_chunks; c += p.n_splits, ++i)
-          for (int t = 0; t < min(chunk_tiles, n_pref - c * chunk_tiles); ++t) {
-            const int pos = (c * chunk_tiles + t) * C::kTile;
+          for (int t = 0; t < chunk_len(c); ++t) {
+            const int pos = (chunk_start(c) + t) * C::kTile;
             const int row = (((p.next_layer * p.cache.num_pages + bt[pos >> p.cache.page_shift]) * p.cache.n_kv_heads + g)
                              << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1));
             tma_prefetch_l2_2d(&tmk, 0, row);
@@ -512,7 +526,7 @@ __global__ void __launch_bounds__(384, 1)
           a[kt] = umma_desc(v_base + kt * 2048, C::kHalf, 1024, kLayoutSW128);
           bp[kt] = umma_desc(p_pl + kt * 512, C::kTile * 32, 256, kLayoutSW32);
         }
-        umma_bf16_x8(o_tm, a, bp, idesc_pv, ((u >> 1) % C::kFlush) != 0 ? 1u : 0u);  // block start: overwrite
+        umma_bf16_x8(o_tm, a, bp, idesc_pv, ((u >> 1) % flush) != 0 ? 1u : 0u);  // block start: overwrite
         umma_commit_elect(&v_empty[sv]);
         umma_commit_elect(&p_empty[wg]);
         SA_TRACE(3, u);
@@ -664,7 +678,7 @@ __global__ void __launch_bounds__(384, 1)
             for (int m = 0; m < N; ++m) v[m] *= fac[m];
             tmem_st_n<N>(o_tm + pl * N, v);
           }
-          if (i > C::kFlush) {  // Oacc holds closed blocks (the first flush ran at i = kFlush)
+          if (i > flush) {  // Oacc holds closed blocks (the first flush ran at i = flush)
             float v[N];
             tmem_ld_n<N>(a_tm, v);
             tc_wait_ld();
@@ -687,21 +701,21 @@ __global__ void __launch_bounds__(384, 1)
       for (int m = 0; m < MR; ++m) l[m] += s[m];
       if (ts == 0) SA_TRACE(8, t);
       if (i > 0) mbar_wait(&p_empty[wg], (i - 1) & 1);  // previous PV finished reading this P plane
-      if (i > 0 && i % C::kFlush == 0) {  // PV(i-1) closed an accumulation block: Oacc (+)= its planes
+      if (i > 0 && i % flush == 0) {  // PV(i-1) closed an accumulation block: Oacc (+)= its planes
         tc_fence_after();
 #pragma unroll
         for (int c16 = 0; c16 < N / 16; ++c16) {
           float op[C::kPlanes][16], acc[16];
 #pragma unroll
           for (int pl = 0; pl < C::kPlanes; ++pl) tmem_ld16(o_tm + pl * N + 16 * c16, op[pl]);
-          if (i > C::kFlush) tmem_ld16(a_tm + 16 * c16, acc);
+          if (i > flush) tmem_ld16(a_tm + 16 * c16, acc);
           tc_wait_ld();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             float v = op[C::kPlanes - 1][j];  // smallest plane first (the epilogue's order)
 #pragma unroll
             for (int pl = C::kPlanes - 2; pl >= 0; --pl) v += op[pl][j];
-            acc[j] = i > C::kFlush ? v + acc[j] : v;
+            acc[j] = i > flush ? v + acc[j] : v;
           }
           tmem_st16(a_tm + 16 * c16, acc);
         }
@@ -808,7 +822,7 @@ __global__ void __launch_bounds__(384, 1)
         }
       }
       // closed accumulation blocks (Oacc) of a warpgroup that ran more than kFlush tiles
-      const bool acc0 = ntiles_wg[0] > C::kFlush, acc1 = ntiles_wg[1] > C::kFlush;
+      const bool acc0 = ntiles_wg[0] > flush, acc1 = ntiles_wg[1] > flush;
       if (acc0 || acc1) {
         float a0[16], a1[16];
         const uint32_t abase = tmem + lane_off + C::kACol + 16 * c16;
@@ -891,7 +905,7 @@ __global__ void __launch_bounds__(384, 1)
   }
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, C::kTmemCols);
+    tmem_dealloc(tmem, tmem_cols);
   }
 }
 

@@ -43,11 +43,13 @@ for p0 in [int(a) for a in sys.argv[1:]] or [16384, 65536]:
         r = Runner(c, Hq, max_rows=R, max_prefix=p0)
         if ms:
             r.set_dev_knob("verify_max_splits", ms)
+        if os.environ.get("FLUSH"):
+            r.set_dev_knob("verify_flush_tiles", int(os.environ["FLUSH"]))
         r.set_batch([0], [p0])
         out = torch.zeros((1, Hq, R, D), dtype=torch.float32, device="cuda")
         r.verify(0, to_dev_bf16(q), out, to_dev_bf16(kn), to_dev_bf16(vn), SCALE)
         got = out.cpu().numpy()[0]
-        print(f"p0={p0} max_splits={ms or 'auto'}: rel_err_rows {rel_err_rows(got, o_ref):.3e} "
+        print(f"p0={p0} flush={os.environ.get('FLUSH', 'default')} max_splits={ms or 'auto'}: rel_err_rows {rel_err_rows(got, o_ref):.3e} "
               f"rel_err_elem {rel_err_elem(got, o_ref):.3e}", flush=True)
         r.close()
         c.close()
