@@ -63,8 +63,10 @@ struct DraftWarp {
   // chains of the sub-blocks are independent (ILP), one row-max reduction and one rescale cover them.
   template <int NB>
   __device__ __forceinline__ void step(const uint32_t (&k_smem)[NB], const uint32_t (&v_smem)[NB], uint32_t half,
-                                       const int (&r0)[NB], int lane, float c, const int (&n_valid)[NB]) {
+                                       const int (&r0)[NB], int lane, float c, const int (&n_valid)[NB],
+                                       long long* cyc = nullptr) {
     const int gid = lane >> 2, mi = lane >> 3;
+    if (cyc) cyc[0] = clock64();
     float s[NB][4];
 #pragma unroll
     for (int bi = 0; bi < NB; ++bi) {
@@ -83,6 +85,10 @@ struct DraftWarp {
       for (int i = 0; i < 4; ++i) s[bi][i] += s2[i];
       if (gid >= n_valid[bi]) s[bi][0] = s[bi][1] = -INFINITY;
       if (gid + 8 >= n_valid[bi]) s[bi][2] = s[bi][3] = -INFINITY;
+    }
+    if (cyc) {  // dev timing: S landed
+      asm volatile("" ::"f"(s[NB - 1][0]), "f"(s[0][3]));
+      cyc[1] = clock64();
     }
     // per query row (2t4 + e): max over the NB x 16 tokens (in-thread, then 8 gid lanes)
     float tmax[2] = {fmaxf(s[0][0], s[0][2]), fmaxf(s[0][1], s[0][3])};
@@ -147,6 +153,10 @@ struct DraftWarp {
         }
       }
       const int tok = r0[bi] + (mi >> 1) * 8 + (lane & 7);
+      if (cyc && bi == 0) {  // dev timing: P fragments of the first sub-block ready
+        asm volatile("" ::"r"(bh0), "r"(bl1));
+        cyc[2] = clock64();
+      }
 #pragma unroll
       for (int jj = 0; jj < 8; ++jj) {  // one V fragment load serves the three P planes
         uint32_t a[4];
@@ -155,6 +165,10 @@ struct DraftWarp {
         if (!kPack) mma_bf16(o[jj], a, bm0, bm1);
         mma_bf16(o[jj], a, bl0, bl1);
       }
+    }
+    if (cyc) {  // dev timing: PV accumulators landed
+      asm volatile("" ::"f"(o[7][3]), "f"(o[0][0]));
+      cyc[3] = clock64();
     }
   }
 
@@ -386,8 +400,13 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
     const int v2 = v_begin + kRoundRows + tid;
     if (tid < kRoundRows && v2 < min(v_end, k)) tq = __ldg(T + v2);
   }
+  long long cyc[4] = {0, 0, 0, 0};  // dev timing of warp 0's first step (trace knob)
   DraftWarp<kPack> w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
+  if (p.trace) {  // dev: stamp 10 once this thread's query fragments have landed
+    asm volatile("" ::"r"(w.qb[7][1]), "r"(w.qb[0][0]));
+    dtrace(p, 10);
+  }
   const bool dbuf = kStream && n_rounds > 1;  // double-buffered rounds (streaming mode)
   auto issue_round = [&](int round, int buf) {  // every row of a later round (after the wait)
     const int rr0 = round * kRoundRows;
@@ -445,7 +464,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
         const uint32_t vs[2] = {vb + (sb >> 2) * DCfg::kTileBytes, vb + (sb2 >> 2) * DCfg::kTileBytes};
         const int rr[2] = {(sb & 3) * 16, (sb2 & 3) * 16};
         const int nv[2] = {nv0, min(16, n - (r0 + sb2 * 16))};
-        w.step<2>(ks, vs, DCfg::kHalf, rr, lane, p.scale_log2, nv);
+        w.step<2>(ks, vs, DCfg::kHalf, rr, lane, p.scale_log2, nv, (p.trace && tid == 0) ? cyc : nullptr);
       } else {
         const uint32_t ks[1] = {kb + (sb >> 2) * DCfg::kTileBytes};
         const uint32_t vs[1] = {vb + (sb >> 2) * DCfg::kTileBytes};
@@ -458,6 +477,12 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   }
   w.finalize();
   dtrace(p, 3);
+  if (p.trace && tid == 0 && warp == 0) {  // dev: step<2> phases of warp 0 in cycles -> slots 11-13
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const size_t launch = static_cast<size_t>((p.step - 1) & 7) * 64 + (p.layer & 63);
+    if (cta < 512)
+      for (int k2 = 0; k2 < 3; ++k2) p.trace[(launch * 512 + cta) * 16 + 11 + k2] = cyc[k2 + 1] - cyc[k2];
+  }
 
   // in-CTA merge of the warps' partials (only the G real query rows), fused with the push: every
   // warp stores its raw O fragments and (m, l); after one barrier each thread rescales the warps'
@@ -645,15 +670,19 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   cfg.blockDim = dim3(32 * std::min(DCfg::kMaxWarps, std::max(1, (std::min(p.chunk, DCfg::kMaxTiles * DCfg::kTile) + 15) / 16)));
   cfg.dynamicSmemBytes = p.stream ? DCfg::kSmemStream : DCfg::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute attrs[2];
+  cudaLaunchAttribute attrs[3];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
   attrs[0].val.clusterDim.x = p.n_splits;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
-  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  // spread: the CTAs of a cluster on distinct SMs (the default policy packs two CTAs of one launch on
+  // an SM when a GPC hosts two clusters, and those CTAs compute ~1 us slower: the launch's straggler)
+  attrs[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+  attrs[1].val.clusterSchedulingPolicyPreference = static_cast<cudaClusterSchedulingPolicy>(p.cluster_policy);
+  attrs[2].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[2].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
-  cfg.numAttrs = p.use_pdl ? 2 : 1;
+  cfg.numAttrs = p.use_pdl ? 3 : 2;
   const bool pack = p.G <= 4;  // P_hi | P_mid share one n8 tile (DraftWarp<true>)
   if (p.stream)
     return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<true, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<true, false>, p);

@@ -100,11 +100,13 @@ struct DevConfig {
   int verify_flush_tiles = 8;   // TMEM accumulation block (warpgroup tiles) folded into Oacc; 0: never
   int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
   int draft_cs = 0;             // forced CTAs per unit (0: automatic)
+  int draft_cluster_policy = 1; // cudaClusterSchedulingPolicy: 1 spread (no two CTAs of a cluster share an SM)
   int draft_multi_rounds = 3;   // rounds allowed in the two-CTA-per-SM multi-round mode
   int draft_debug = 0;          // print the draft launch geometry to stderr
   int draft_no_pdl = 0;         // launch iteration drafts without programmatic dependent launch
   int iter_skip = -1;           // phase bits to skip in sa_iteration_run (-1: sa_iteration_args.phases)
   int select_batched = 0;       // one grid-z select launch for all layers after the verify chain
+  int select_legacy = 0;        // select kernel: 0 automatic, 1 single-CTA, 2 cluster (dev)
   int stream_priority = 1;      // side stream lowest priority, capture stream highest
   int trace = 0;                // per-CTA globaltimer traces (sa_dev_trace_dump)
 };
@@ -169,6 +171,7 @@ struct DraftParams {
   unsigned long long* trace;  // dev-only per-CTA phase timestamps; null in production
   int use_pdl;  // launch with programmatic stream serialization (iteration graph only)
   int stream;   // double-buffered multi-round chunks (one CTA per SM)
+  int cluster_policy;  // cudaClusterSchedulingPolicy of the launch (1: spread a cluster's CTAs over SMs)
   int draft_off;  // this chain's new rows start at p0 + draft_off; the tail is [p0, p0 + draft_off + step)
 };
 
@@ -186,6 +189,8 @@ struct SelectParams {
   int32_t* idx;    // [B][n_sets][k_cap]
   int32_t* k_out;  // [B][n_sets]
   int64_t zs_scores = 0, zs_fx = 0, zs_idx = 0, zs_cnt = 0;  // per-slot strides (batched launches)
+  int64_t max_n = 0;  // largest p0 of the bound batch (kernel choice)
+  int legacy = 0;     // kernel choice: 0 automatic, 1 single-CTA radix select, 2 cluster select (dev)
 };
 
 sa_status comm_allreduce_i64(sa_comm* c, long long* buf, size_t count, cudaStream_t s);

@@ -392,6 +392,8 @@ static sa_status select_impl(sa_runner* r, const sa_select_args* a, cudaStream_t
   p.zs_fx = static_cast<int64_t>(r->cfg.max_batch) * r->ld;
   p.zs_idx = static_cast<int64_t>(r->cfg.max_batch) * r->Hkv * r->k_cap;
   p.zs_cnt = static_cast<int64_t>(r->cfg.max_batch) * r->Hkv;
+  p.max_n = r->p_max;
+  p.legacy = r->dev.select_legacy;
   cudaError_t e = sa::launch_select(p, s, n_slots);
   if (e != cudaSuccess) return sa::cuda_fail(e, "select launch");
   return SA_OK;
@@ -510,6 +512,7 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
   p.counters = r->d_cnt;
   p.trace = r->dtrace;
   p.use_pdl = pdl ? 1 : 0;
+  p.cluster_policy = r->dev.draft_cluster_policy;
   cudaError_t e = sa::launch_draft(p, s);
   if (e != cudaSuccess) return sa::cuda_fail(e, "draft launch");
   return SA_OK;
@@ -549,11 +552,13 @@ SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) 
   else if (n == "verify_flush_tiles") d.verify_flush_tiles = v;
   else if (n == "draft_min_cs") d.draft_min_cs = v;
   else if (n == "draft_cs") d.draft_cs = v;
+  else if (n == "draft_cluster_policy") d.draft_cluster_policy = v;
   else if (n == "draft_multi_rounds") d.draft_multi_rounds = v;
   else if (n == "draft_debug") d.draft_debug = v;
   else if (n == "draft_no_pdl") d.draft_no_pdl = v;
   else if (n == "iter_skip") d.iter_skip = v;
   else if (n == "select_batched") d.select_batched = v;
+  else if (n == "select_legacy") d.select_legacy = v;
   else if (n == "stream_priority") {
     d.stream_priority = v;
     SA_CUDA_CHECK(cudaDeviceSynchronize());

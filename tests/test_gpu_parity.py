@@ -247,6 +247,55 @@ def test_select_exact_ties_lower_index(cuda, ref):
     assert np.array_equal(idx[0, 0, : cnt[0, 0]], want)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_select_kernels_agree(cuda, ref, mode):
+    """The cluster select (8 CTAs, keys in registers, pushed adaptive radix histograms; select_legacy=2)
+    and the single-CTA shared-memory radix select (select_legacy=1) give identical index sets and counts
+    on the same scores: three sequences with ragged prefixes (one at 40960, past one CTA's register
+    span), keys repeating every 16 positions in one of them (exact ties straddling the threshold), both
+    score layouts; and the reference's own selection agrees on the tie-heavy sequence."""
+    torch = cuda
+    Runner, _, selection_k = _lib()
+    Hkv, G, R = 2, 4, 3
+    p0s = [40960, 9000, 777]
+    m = Matched(ref, L=1, Hkv=Hkv, n_tokens=0, seed=66, max_context=max(p0s) + 64, page_size=256,
+                n_seqs=3, lens=p0s)
+    rep = m.K[1][np.arange(p0s[1]) % 16]  # sequence 1: every key repeats every 16 positions
+    m.cache.truncate(0, seq=1)
+    m.cache.append(torch.from_numpy(rep).cuda(), torch.from_numpy(m.V[1]).cuda(), seq=1)
+    q = normal_bf16(67, 1, (3, Hkv * G, R, D))
+    kn, vn = normal_bf16(67, 2, (3, R, Hkv, D)), normal_bf16(67, 3, (3, R, Hkv, D))
+    n_sets = 1 if mode == 0 else Hkv
+    res = []
+    for legacy in (2, 1):  # cluster kernel, single-CTA kernel
+        r = Runner(m.cache, Hkv * G, max_rows=R, max_prefix=max(p0s), max_batch=3, sparse_ratio=0.07, k_min=16)
+        r.set_dev_knob("select_legacy", legacy)
+        r.set_batch([0, 1, 2], p0s)
+        out = torch.zeros((3, Hkv * G, R, D), dtype=torch.float32, device="cuda")
+        r.verify(0, to_dev_bf16(q), out, to_dev_bf16(kn), to_dev_bf16(vn), SCALE, score_row_mask=1 | (1 << (R - 1)),
+                 score_layout=mode)
+        for b in range(3):
+            m.cache.set_size(p0s[b], seq=b)
+        res.append(_gpu_select(r, 0, mode, n_sets, 2))
+        r.close()
+    (i_new, c_new), (i_old, c_old) = res
+    assert np.array_equal(c_new, c_old)
+    for b in range(3):
+        assert c_new[b, 0] == selection_k(0.07, p0s[b], 16)
+        for s_ in range(n_sets):
+            assert np.array_equal(i_new[b, s_, :c_new[b, s_]], i_old[b, s_, :c_old[b, s_]]), (b, s_)
+    kv = ref.kv(1, Hkv, D, p0s[1] + 64)
+    for t in range(p0s[1]):
+        kv.append(rep[t], m.V[1][t])
+    for t in range(R):
+        kv.append(kn[1, t], vn[1, t])
+    _, l_ref = kv.verify_layer(0, Hkv * G, q[1], p0s[1], R, SCALE, threads=8)
+    for s_ in range(n_sets):
+        heads = list(range(Hkv * G)) if mode == 0 else list(range(s_ * G, (s_ + 1) * G))
+        want = ref.select(COLLECT2, np.ascontiguousarray(l_ref[heads]), list(range(1, R + 1)), 0.07, 16)
+        assert np.array_equal(i_new[1, s_, :c_new[1, s_]], want)
+
+
 # ----------------------------------------------------------------------------------- draft
 
 # (mode, Hkv, G): G <= 4 runs the packed-plane draft step (P_hi | P_mid share one n8 tile), G = 8 the

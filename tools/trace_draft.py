@@ -26,6 +26,8 @@ for s in range(0, p0, 2048):
 KFIX = int(os.environ.get("K_FIX", 0))  # fixed budget k (config 5 sweep points)
 r = Runner(cache, Hq, max_rows=R, max_prefix=p0, **({"sparse_ratio": 1e-9, "k_min": KFIX} if KFIX else {}))
 r.set_dev_knob("trace", 1)  # dev-only knobs (the library never reads the environment)
+for kv in filter(None, os.environ.get("DEV_KNOBS", "").split(",")):  # e.g. DEV_KNOBS=draft_no_pdl=1
+    r.set_dev_knob(kv.split("=")[0], int(kv.split("=")[1]))
 if os.environ.get("SA_ITER_SKIP"):
     r.set_dev_knob("iter_skip", int(os.environ["SA_ITER_SKIP"]))
 r.set_batch([0], [p0])
@@ -72,7 +74,7 @@ for j in range(gamma):
             print(f"{j + 1:4d} {l:5d} {s0.min():7.2f} {s0.max():7.2f} | {np.median(v(1)):7.2f} {v(1).max():7.2f} | "
                   f"{np.median(v(2)):7.2f} {v(2).max():7.2f} | {np.median(v(3)):7.2f} {v(3).max():7.2f} | "
                   f"{np.median(en):7.2f} {en.max():7.2f} | {dt:5.2f}  merge: sync1 {np.median(v(8)):7.2f} "
-                  f"written {np.median(v(9)):7.2f} t10 {np.median(v(10)):7.2f} t11 {np.median(v(11)):7.2f} ctamerged {np.median(v(5)):7.2f} "
+                  f"q_ready {np.median(v(10)):7.2f}/{v(10).max():7.2f} ctamerged {np.median(v(5)):7.2f} "
                   f"pushed {np.median(v(6)):7.2f} inbox {np.median(v(7)):7.2f}/{v(7).max():7.2f}")
 
 # verify phase on the same clock (globaltimer): last layer's end vs the first draft's start
@@ -101,6 +103,12 @@ for j in range(gamma):
             s_ = int(c % CS)
             rel_c.setdefault(s_, []).append((blk[c, 3] - med_c) / 1e3)
             rel_g.setdefault(s_, []).append((blk[c, 2] - med_g) / 1e3)
+ph = dr[:gamma, 2:L, :, 11:14].reshape(-1, 3)
+ph = ph[(ph > 0).all(1) & (ph < 10**6).all(1)]
+if len(ph):
+    print("warp-0 step<2> cycles (median / p90): QK " + f"{np.median(ph[:, 0]):.0f}/{np.percentile(ph[:, 0], 90):.0f}"
+          f"  softmax+P {np.median(ph[:, 1]):.0f}/{np.percentile(ph[:, 1], 90):.0f}"
+          f"  PV {np.median(ph[:, 2]):.0f}/{np.percentile(ph[:, 2], 90):.0f}")
 print("split: computed-vs-median (us) / gathered-vs-median (us)")
 print(" ".join(f"{s_}:{np.median(rel_c[s_]):+.2f}/{np.median(rel_g[s_]):+.2f}" for s_ in sorted(rel_c)))
 
