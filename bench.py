@@ -29,6 +29,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+if os.environ.get("SA_AB_ROOT"):  # dev A/B runs (tools/ab_build.sh): the package from another build
+    sys.path.insert(0, os.path.abspath(os.environ["SA_AB_ROOT"]))
 
 METRIC = "draft+verify attention tokens/s at 32K ctx; achieved HBM GB/s vs ~8 TB/s"
 HBM_NOMINAL = 8000.0  # GB/s, BASELINE.json denominator

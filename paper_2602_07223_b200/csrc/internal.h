@@ -92,7 +92,7 @@ struct DevConfig {
   int verify_next_pf = 0;       // chunks of the next layer each CTA prefetches into L2 at its stream end
   int verify_no_prefill = 0;    // do not fill the ring before griddepcontrol.wait
   int verify_static_first = 1;  // first chunk = split index (else every chunk claimed from the counter)
-  int verify_mergers = 4;       // CTAs (last arrivals of a unit) that split the merge's rows
+  int verify_mergers = 8;       // designated merger CTAs (splits 0..n-1) that split the merge's rows
   int verify_full_rows = 0;     // softmax over all N MMA columns instead of MR = roundup4(M)
   int verify_max_splits = 0;    // cap on CTAs per (sequence, KV head) unit (0: automatic)
   int verify_wait_pf = 0;       // tiles prefetched into L2 ahead of the ring before the dependency wait ends
@@ -139,6 +139,7 @@ struct VerifyParams {
   int static_first;  // first chunk = split index (else every chunk claimed from the counter)
   int* counters;   // [B*Hkv][4]: [0] arrivals, [1] go (all partials stored), [2] mergers done
   int* chunk_ctr;  // [B*Hkv] dynamic chunk claims (tcgen05 verify), re-armed by the merging CTA
+  int* flags;      // [B*Hkv][8 mergers][128 splits]: partial published (tcgen05 verify), reset by the merger
   unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production
   int use_pdl;  // programmatic dependent launch after the previous layer's verify (iteration graph)
   int next_layer;  // layer verified next (its first tiles are prefetched into L2), -1: none

@@ -41,7 +41,7 @@ struct sa_runner {
   // split-KV workspaces
   int64_t v_units_cap = 0, d_units_cap = 0;
   float *v_po = nullptr, *v_pml = nullptr, *d_po = nullptr, *d_pml = nullptr;
-  int *v_cnt = nullptr, *d_cnt = nullptr, *v_chunk = nullptr;
+  int *v_cnt = nullptr, *d_cnt = nullptr, *v_chunk = nullptr, *v_flags = nullptr;
   // streams / graph
   cudaStream_t side = nullptr;
   cudaStream_t capture = nullptr;  // graphs are captured here (the caller's stream may be legacy)
@@ -162,6 +162,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   alloc(reinterpret_cast<void**>(&r->v_pml), 2 * sizeof(float) * r->v_units_cap * 64 * 2);
   alloc(reinterpret_cast<void**>(&r->v_cnt), 2 * 4 * sizeof(int) * mb * H);
   alloc(reinterpret_cast<void**>(&r->v_chunk), 2 * sizeof(int) * mb * H);
+  alloc(reinterpret_cast<void**>(&r->v_flags), 2 * sizeof(int) * mb * H * 8 * 128);  // [parity][unit][merger][split]
   alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
   alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
@@ -199,7 +200,7 @@ SA_API sa_status sa_runner_destroy(sa_runner* r) {
   for (void* p : {static_cast<void*>(r->d_seq), static_cast<void*>(r->d_p0), static_cast<void*>(r->scores),
                   static_cast<void*>(r->idx), static_cast<void*>(r->score_fx), static_cast<void*>(r->kcnt), static_cast<void*>(r->keys),
                   static_cast<void*>(r->v_po), static_cast<void*>(r->v_pml), static_cast<void*>(r->v_cnt), static_cast<void*>(r->v_chunk),
-                  static_cast<void*>(r->d_po), static_cast<void*>(r->d_pml), static_cast<void*>(r->d_cnt)})
+                  static_cast<void*>(r->v_flags), static_cast<void*>(r->d_po), static_cast<void*>(r->d_pml), static_cast<void*>(r->d_cnt)})
     cudaFree(p);
   delete r;
   return SA_OK;
@@ -347,6 +348,7 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.part_o = r->v_po + par * po_stride;
     p.part_ml = r->v_pml + par * pml_stride;
     p.counters = r->v_cnt + par * cnt_stride * 4;
+    p.flags = r->v_flags + par * cnt_stride * 8 * 128;
     p.use_pdl = pdl ? 1 : 0;
     p.next_layer = next_layer;
     p.trace = r->vtrace;

@@ -158,26 +158,59 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
       p.trace[(e) * 64 + (t)] = clock64();                                                      \
   } while (0)  // log2 units: p <= 2^8 before a forced max update
 
-// Rows [r_lo, r_hi) of one unit's output from its `cnt` split partials (O rows [N][128]
-// unnormalised and (m, l) per row at src_o / src_ml, per-partial strides N*128 / N*2 floats): the
-// partial rows and the (m, l) table are bulk-copied into the idle ring buffers, then every thread
-// forms its rows' merge weights on the fly and writes normalised rows to dst_o (row stride 128).
-__device__ __forceinline__ void merge_rows(uint8_t* smem, uint64_t* bar, const float* src_o, const float* src_ml,
-                                           int cnt, int N, int r_lo, int r_hi, float* dst_o, int t256) {
+// Designated merger `part` (= split index < n_mergers) of a unit: rows [r_lo, r_hi) of the output.
+// It polls the unit's per-split "partial published" flags (set with st.release by every CTA after
+// its partial stores) and bulk-loads each split's (m, l) table and row slice into shared memory as
+// soon as that split is published, so when the last split publishes only its own small slice is
+// still in flight; then combines in fixed split order (deterministic) and resets its flags.
+__device__ __forceinline__ void merge_rows_progressive(uint8_t* smem, uint64_t* bar, const float* src_o,
+                                                       const float* src_ml, int cnt, int N, int r_lo, int r_hi,
+                                                       float* dst_o, int* flags, int t256,
+                                                       unsigned long long* tstamp = nullptr) {
+  auto stamp = [&](int k) {  // dev trace: globaltimer into the CTA's trace row (slots 7, 8)
+    if (tstamp) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      tstamp[k] = gt;
+    }
+  };
   const int nr = r_hi - r_lo;
-  if (nr <= 0) return;
-  const uint32_t obytes = static_cast<uint32_t>(nr) * 512u;
-  const uint32_t mlbytes = static_cast<uint32_t>(cnt) * N * 8u;
-  float2* sml = reinterpret_cast<float2*>(smem);                       // [partial][N] (m, l)
-  uint8_t* sop = smem + ((mlbytes + 127u) & ~127u);                      // [partial][nr][128]
-  if (t256 == 0) {
-    fence_proxy_async();  // generic writes of the other CTAs (acquired by the caller) -> async-proxy reads
-    mbar_expect_tx(bar, cnt * obytes + mlbytes);
-    bulk_load(sml, src_ml, mlbytes, bar);
-    for (int s2 = 0; s2 < cnt; ++s2)
-      bulk_load(sop + s2 * obytes, src_o + static_cast<size_t>(s2) * N * 128 + r_lo * 128, obytes, bar);
+  const uint32_t obytes = static_cast<uint32_t>(max(nr, 0)) * 512u;
+  const uint32_t mlb = static_cast<uint32_t>(N) * 8u;  // one split's (m, l) table
+  float2* sml = reinterpret_cast<float2*>(smem);                              // [partial][N] (m, l)
+  uint8_t* sop = smem + ((static_cast<uint32_t>(cnt) * mlb + 127u) & ~127u);  // [partial][nr][128]
+  if (t256 < 32) {  // one warp: lane l watches splits l, l + 32, ... (all flag loads in flight together)
+    const int lane = t256;
+    uint32_t mine = 0;  // splits of this lane not yet loaded (bit j: split lane + 32 j; cnt <= 128)
+    for (int j = 0; 32 * j + lane < cnt; ++j) mine |= 1u << j;
+    while (__any_sync(0xffffffffu, mine != 0)) {
+      bool got = false;
+      for (int j = 0; j < 4; ++j) {
+        if (!((mine >> j) & 1u)) continue;
+        const int s2 = 32 * j + lane;
+        int f;  // relaxed poll (L2, no L1 invalidation per probe); the fence below acquires
+        asm volatile("ld.relaxed.gpu.s32 %0, [%1];" : "=r"(f) : "l"(flags + s2) : "memory");
+        if (!f) continue;
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        fence_proxy_async();  // the split's generic-proxy stores (acquired) -> async-proxy reads
+        mbar_expect_tx_only(bar, mlb + obytes);
+        bulk_load(reinterpret_cast<uint8_t*>(sml) + s2 * mlb, src_ml + static_cast<size_t>(s2) * N * 2, mlb, bar);
+        if (nr > 0) bulk_load(sop + s2 * obytes, src_o + static_cast<size_t>(s2) * N * 128 + r_lo * 128, obytes, bar);
+        flags[s2] = 0;  // re-armed for this workspace's next use (two layers on, PDL-ordered)
+        mine &= ~(1u << j);
+        got = true;
+      }
+      (void)got;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      stamp(7);
+      mbar_arrive(bar);  // every expected byte is now accounted for
+    }
   }
   mbar_wait(bar, 0);
+  if (t256 == 0) stamp(8);
+  if (nr <= 0) return;
   const float4* so = reinterpret_cast<const float4*>(sop);
   for (int it = t256; it < nr * 32; it += 256) {
     const int rr = it >> 5, c4 = it & 31, row = r_lo + rr;
@@ -191,7 +224,7 @@ __device__ __forceinline__ void merge_rows(uint8_t* smem, uint64_t* bar, const f
     }
     float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
     float lsum = 0.f;
-    for (int s0 = 0; s0 < cnt; s0 += 8) {  // 8 independent smem loads per batch
+    for (int s0 = 0; s0 < cnt; s0 += 8) {
       float4 v[8];
       float2 ml[8];
 #pragma unroll
@@ -309,9 +342,6 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* sq = smem + C::kOffQ;
   for (int i = tid; i < ((p0 + R + (1 << p.cache.page_shift) - 1) >> p.cache.page_shift); i += C::kThreads)
     bt[i] = __ldg(p.cache.block_table + static_cast<int64_t>(seq) * p.cache.max_pages_per_seq + i);
-  __shared__ int s_go;  // this unit's merge generation before any arrival of this launch
-  if (tid == 0 && p.n_splits > 1)  // final value of the previous use (complete by the PDL transitivity)
-    asm volatile("ld.relaxed.gpu.s32 %0, [%1];" : "=r"(s_go) : "l"(p.counters + unit * 4 + 1) : "memory");
   if (tid < 64) {
     mref_all[tid] = -INFINITY;
     mref_all[64 + tid] = -INFINITY;
@@ -851,48 +881,25 @@ __global__ void __launch_bounds__(384, 1)
     if (single) {
       if (wg == 0 && ts == 0) p.chunk_ctr[unit] = 0;  // re-arm chunk claims
     } else {
-      // Split merge by the last-arriving CTAs of the unit, each normalising a slice of the rows.
-      // Arrival: one acq_rel atomic per CTA after the CTA-wide barrier (release of this CTA's
-      // partial stores).  The last arrival has acquired every partial; it re-arms the arrival and
-      // chunk counters (every CTA of the unit has claimed its last chunk and arrived) and releases the
-      // next `go` generation, which the other mergers (the few arrivals before it, still resident)
-      // acquire before reading partials.  `go` only ever increases, so nobody waits for the
-      // mergers to finish before the unit's counters are ready for their next use.
+      // Split merge by designated mergers: splits 0 .. nm-1 each normalise a slice of the rows.  Every
+      // CTA publishes its partial with one st.release per merger (after the CTA-wide barrier that
+      // orders its partial stores); a merger bulk-loads each split's slice as soon as it is published
+      // (merge_rows_progressive), so only the last split's slice is on the critical path.
       const int t256 = wg * 128 + ts;
-      int* ctr = p.counters + unit * 4;  // [0] arrivals, [1] go generation
-      named_bar_sync(1, 256);
-      if (t256 == 0) {
-        SA_TSTAMP(5);
-        int old;
-        asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
-        *flag = old;
-        SA_TSTAMP(6);
-      }
-      named_bar_sync(1, 256);
-      const int arrival = *flag;
       const int nm = min(p.n_mergers, p.n_splits);
-      if (arrival >= p.n_splits - nm) {
-        const int part = arrival - (p.n_splits - nm);  // the last arrival takes the last slice
-        if (arrival == p.n_splits - 1) {
-          if (t256 == 0) {
-            ctr[0] = 0;
-            p.chunk_ctr[unit] = 0;
-            if (nm > 1) asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(ctr + 1), "r"(s_go + 1) : "memory");
-          }
-        } else {
-          if (t256 == 0) {
-            int go = 0;
-            while (true) {
-              asm volatile("ld.acquire.gpu.s32 %0, [%1];" : "=r"(go) : "l"(ctr + 1) : "memory");
-              if (go != s_go) break;
-              __nanosleep(64);
-            }
-          }
-          named_bar_sync(1, 256);
-        }
+      int* uflags = p.flags + static_cast<size_t>(unit) * 8 * 128;
+      named_bar_sync(1, 256);
+      if (t256 < nm) {
+        if (t256 == 0) SA_TSTAMP(5);
+        asm volatile("st.release.gpu.s32 [%0], %1;" ::"l"(uflags + t256 * 128 + split), "r"(1) : "memory");
+        if (t256 == 0) SA_TSTAMP(6);
+      }
+      if (split < nm) {
         const int per = (M + nm - 1) / nm;
-        merge_rows(smem, merge_bar, po, pml, p.n_splits, N, min(M, part * per), min(M, (part + 1) * per), out_unit,
-                   t256);
+        merge_rows_progressive(smem, merge_bar, po, pml, p.n_splits, N, min(M, split * per), min(M, (split + 1) * per),
+                               out_unit, uflags + split * 128, t256,
+                               (p.trace && cta_lin < 1024) ? p.trace + 1024 + (p.layer & 63) * 16384 + 16 * cta_lin : nullptr);
+        if (split == 0 && t256 == 0) p.chunk_ctr[unit] = 0;  // every split has claimed its last chunk
         if (t256 == 0) SA_TSTAMP(9);
       }
     }

@@ -1,0 +1,9 @@
+#!/bin/bash
+# Dev: build git revision $1 into .ab/$2 (package + its .so) for same-box A/B runs:
+#   tools/ab_build.sh HEAD old && gpurun -- 'AB=.ab/old bash tools/knob_sweep.sh ...'
+set -e
+rev=$1; name=$2
+rm -rf .ab/$name && mkdir -p .ab/$name
+git archive "$rev" paper_2602_07223_b200 include | tar -x -C .ab/$name
+make -s -j8 -C .ab/$name/paper_2602_07223_b200/csrc > /dev/null
+echo "built $rev into .ab/$name"

@@ -6,7 +6,8 @@ EXTRA=${EXTRA:-}
 for setting in "$@"; do
   devs=""
   for kv in $setting; do devs="$devs --dev $kv"; done
-  line=$(timeout 300 python bench.py --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline --no-extras $EXTRA $devs 2>/dev/null | tail -1)
+  # AB=.ab/<name>: run with that build of the package (tools/ab_build.sh) instead of the working tree's
+  line=$(SA_AB_ROOT=${AB:-} timeout 300 python bench.py --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline --no-extras $EXTRA $devs 2>/dev/null | tail -1)
   python - "$setting" "$line" <<'PY'
 import json, sys
 s, line = sys.argv[1], sys.argv[2]

@@ -65,11 +65,15 @@ for l in range(2, min(L, 64)):
         ref = np.median(b[:, 2])
         last = b[np.argmax(b[:, 6])] if (b[:, 6] > 0).any() else None
         md = b[:, 9][b[:, 9] > 0]
+        f7 = b[:, 7][b[:, 7] > 0]
+        f8 = b[:, 8][b[:, 8] > 0]
         rows.append([b[:, 2].max() - ref, last[4] - ref, last[10] - ref, last[11] - ref, last[12] - ref,
                      last[5] - ref, last[6] - ref,
+                     (f7.max() - ref) if len(f7) else np.nan, (f8.max() - ref) if len(f8) else np.nan,
                      (md.max() - ref) if len(md) else np.nan, b[:, 1].max() - ref, b[:, 0].max() - ref])
 a = np.array(rows) / 1e3
 names = ["loop_end_max", "last:pv_done", "last:l_reduced", "last:ml_stored", "last:o_stored",
-         "last:partial_stored", "last:counted", "merge_done_max", "cta_end_max", "cta_start_max"]
+         "last:partial_stored", "last:published", "merger:all_flags_seen", "merger:partials_landed",
+         "merge_done_max", "cta_end_max", "cta_start_max"]
 for i, n in enumerate(names):
     print(f"{n:22s} median {np.nanmedian(a[:, i]):7.2f}  p90 {np.nanpercentile(a[:, i], 90):7.2f} us")
