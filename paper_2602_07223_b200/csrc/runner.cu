@@ -141,7 +141,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   r->ld = std::max<int64_t>(64, round_up(cfg->max_prefix, 64));
   r->k_cap = static_cast<int>(std::max<int64_t>(1, sa_selection_k(cfg->sparse_ratio, cfg->max_prefix, cfg->k_min)));
   const int64_t mb = cfg->max_batch, H = r->Hkv, S = r->n_slots;
-  r->v_units_cap = std::max<int64_t>(4 * r->num_sms, mb * H);
+  r->v_units_cap = std::max<int64_t>(8 * r->num_sms, mb * H);  // verify partial slots (multi-wave splits)
   r->d_units_cap = std::max<int64_t>(8 * r->num_sms, mb * H);
   cudaError_t e = cudaSuccess;
   auto alloc = [&](void** p, size_t bytes) {
@@ -339,8 +339,19 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     const int n_mergers = std::max(1, std::min(8, dv.verify_mergers));
     const int rows_per = (p.M + n_mergers - 1) / n_mergers;
     const int fit = std::max(1, (sa::verify_tc_merge_capacity(p.M) - 128) / (rows_per * 512 + 64 * 8));
-    p.n_splits = static_cast<int>(std::min<int64_t>({std::max<int64_t>(1, r->num_sms / units),
-                                                     n_chunks, 128, r->v_units_cap / units, fit}));
+    // one wave of at most one CTA per SM when that keeps >= 90 % of the SMs busy; otherwise (e.g. 128
+    // units on 148 SMs: 20 idle) the smallest split count whose waves fill >= 90 % of the SM slots —
+    // the CTAs of a unit share its chunks, so a wave boundary inside a unit only shifts work
+    int64_t ns = std::max<int64_t>(1, r->num_sms / units);
+    if (units * ns * 10 < 9LL * r->num_sms)
+      for (int64_t s2 = ns + 1; s2 <= 16; ++s2) {
+        const int64_t ctas = units * s2, waves = (ctas + r->num_sms - 1) / r->num_sms;
+        if (ctas * 10 >= 9LL * waves * r->num_sms) {
+          ns = s2;
+          break;
+        }
+      }
+    p.n_splits = static_cast<int>(std::min<int64_t>({ns, n_chunks, 128, r->v_units_cap / units, fit}));
     if (dv.verify_max_splits > 0) p.n_splits = std::min(p.n_splits, dv.verify_max_splits);
     p.n_mergers = n_mergers;
     p.chunk = 0;
