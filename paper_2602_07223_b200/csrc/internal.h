@@ -98,6 +98,7 @@ struct DevConfig {
   int verify_wait_pf = 0;       // tiles prefetched into L2 ahead of the ring before the dependency wait ends
   int verify_tail_tiles = 18;   // single-tile chunks at the end of the prefix (guided claiming)
   int verify_flush_tiles = 8;   // TMEM accumulation block (warpgroup tiles) folded into Oacc; 0: never
+  int verify_flush_min_tiles = 24;  // fold only when a CTA streams more than this many prefix tiles
   int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
   int draft_cs = 0;             // forced CTAs per unit (0: automatic)
   int draft_cluster_policy = 1; // cudaClusterSchedulingPolicy: 1 spread (no two CTAs of a cluster share an SM)

@@ -330,12 +330,12 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.full_rows = dv.verify_full_rows ? 1 : 0;
     p.chunk_tiles = chunk_tiles;
     p.prefetch = std::min(12, std::max(0, dv.verify_prefetch));
-    p.wait_pf = std::min(16, std::max(0, dv.verify_wait_pf));
+    p.wait_pf = std::min(16, std::max(0, dv.verify_wait_pf));  // the producer's 32-entry position ring
     p.tail_tiles = std::max(0, dv.verify_tail_tiles);
-    p.flush_tiles = std::max(0, dv.verify_flush_tiles);  // the producer's 32-entry position ring
+    p.flush_tiles = std::max(0, dv.verify_flush_tiles);
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
-    // split merge: the last n_mergers arrivals of a unit normalise a slice of rows each; their
-    // partial rows and the (m, l) table must fit the ring buffers
+    // split merge: the designated mergers (splits 0..n_mergers-1) normalise a slice of rows each; their
+    // staged partial rows and the (m, l) table must fit the ring buffers
     const int n_mergers = std::max(1, std::min(8, dv.verify_mergers));
     const int rows_per = (p.M + n_mergers - 1) / n_mergers;
     const int fit = std::max(1, (sa::verify_tc_merge_capacity(p.M) - 128) / (rows_per * 512 + 64 * 8));
@@ -353,6 +353,10 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
       }
     p.n_splits = static_cast<int>(std::min<int64_t>({ns, n_chunks, 128, r->v_units_cap / units, fit}));
     if (dv.verify_max_splits > 0) p.n_splits = std::min(p.n_splits, dv.verify_max_splits);
+    // accumulation-block folding only where a CTA's chain is long: the kernels that carry the fold
+    // code run their softmax loop 0.6 us per layer slower (same-box A/B), and chains of <= 24 tiles
+    // per CTA stay at ~6e-4 elementwise without it (tools/verify_precision.py)
+    if ((r->p_max / 128 + p.n_splits - 1) / p.n_splits <= dv.verify_flush_min_tiles) p.flush_tiles = 0;
     p.n_mergers = n_mergers;
     p.chunk = 0;
     p.chunk_ctr = r->v_chunk + par * cnt_stride;
@@ -563,6 +567,7 @@ SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) 
   else if (n == "verify_wait_pf") d.verify_wait_pf = v;
   else if (n == "verify_tail_tiles") d.verify_tail_tiles = v;
   else if (n == "verify_flush_tiles") d.verify_flush_tiles = v;
+  else if (n == "verify_flush_min_tiles") d.verify_flush_min_tiles = v;
   else if (n == "draft_min_cs") d.draft_min_cs = v;
   else if (n == "draft_cs") d.draft_cs = v;
   else if (n == "draft_cluster_policy") d.draft_cluster_policy = v;
