@@ -153,11 +153,19 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
   } while (0)
 
 // dev-only pipeline trace: ev[e][t] = clock64 of event e at tile t for CTA (0,0,0)
+// Per-tile pipeline stamps of CTA 0 (tools/trace_verify.py): a dev build only
+// (make -C paper_2602_07223_b200/csrc EXTRA_NVFLAGS=-DSA_PIPE_TRACE); the checks cost 0.5 us per layer.
+#ifndef SA_PIPE_TRACE
+#define SA_TRACE(e, t) \
+  do {                 \
+  } while (0)
+#else
 #define SA_TRACE(e, t)                                                                          \
   do {                                                                                          \
     if (p.trace && p.layer == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (t) < 64) \
       p.trace[(e) * 64 + (t)] = clock64();                                                      \
-  } while (0)  // log2 units: p <= 2^8 before a forced max update
+  } while (0)
+#endif  // log2 units: p <= 2^8 before a forced max update
 
 // Designated merger `part` (= split index < n_mergers) of a unit: rows [r_lo, r_hi) of the output.
 // It polls the unit's per-split "partial published" flags (set with st.release by every CTA after
@@ -254,7 +262,7 @@ __device__ __forceinline__ void merge_rows_progressive(uint8_t* smem, uint64_t* 
 
 // MR: the softmax rows that can be real (M rounded up to 8, <= N); rows MR..N-1 of the MMA tile are
 // padding and get no softmax work (P = 0).
-template <int N, int MR, bool kFlush>
+template <int N, int MR, bool kFlush, bool kLogits>
 __global__ void __launch_bounds__(384, 1)
     verify_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                      const VerifyParams p) {
@@ -355,7 +363,8 @@ __global__ void __launch_bounds__(384, 1)
                     : -1;
   }
   // accumulation block length (tiles); N = 64 has no TMEM room for Oacc (one block per CTA)
-  // kFlush instantiations carry the fold code; without it the softmax loop is shorter (0.6 us per layer)
+  // kFlush / kLogits instantiations carry the accumulation-block fold / the LogitMatrix stores; without
+  // them the softmax loop is shorter (0.6 / 0.55 us per layer, same-box A/B)
   const bool flushing = C::kFlushable && kFlush && p.flush_tiles > 0;
   const int flush = flushing ? p.flush_tiles : (1 << 30);
   const uint32_t tmem_cols = flushing ? C::kTmemCols : C::kTmemColsBase;
@@ -643,7 +652,7 @@ __global__ void __launch_bounds__(384, 1)
         else
           score_out[pos] = sc;
       }
-      if (p.logits && pos < p0) {  // LogitMatrix path (Collect2Weights, debug): raw prefix logits
+      if (kLogits && pos < p0) {  // LogitMatrix path (Collect2Weights, debug): raw prefix logits
         float* lb = p.logits + static_cast<size_t>(b) * Hq * p.n_collect * p.ld_logits + pos;
 #pragma unroll
         for (int m = 0; m < N; ++m) {
@@ -918,9 +927,9 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-template <int N, int MR, bool kFlush>
+template <int N, int MR, bool kFlush, bool kLogits>
 static cudaError_t launch_n(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s) {
-  auto kern = verify_tc_kernel<N, MR, kFlush>;
+  auto kern = verify_tc_kernel<N, MR, kFlush, kLogits>;
   static std::atomic<uint64_t> attr_mask{0};
   int dev = 0;
   if (func_attrs_needed(attr_mask, &dev)) {
@@ -944,14 +953,14 @@ static cudaError_t launch_n(const VerifyParams& p, const CUtensorMap& tk, const 
 // MR = N - 12, N - 8, N - 4 or N: the softmax warpgroups work only on the rows that can be real
 // (measured at gamma 4, M = 20 in an N = 32 tile: MR 24 instead of 32 took the verify phase from
 // 1.013 to 0.984 ms; the softmax instruction count is on the main loop's critical path)
-template <int N, bool kFlush>
+template <int N, bool kFlush, bool kLogits>
 static cudaError_t launch_mr_f(int mr, const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv,
                              cudaStream_t s) {
   switch (N - mr) {
-    case 12: return launch_n<N, N - 12, kFlush>(p, tk, tv, s);
-    case 8: return launch_n<N, N - 8, kFlush>(p, tk, tv, s);
-    case 4: return launch_n<N, N - 4, kFlush>(p, tk, tv, s);
-    default: return launch_n<N, N, kFlush>(p, tk, tv, s);
+    case 12: return launch_n<N, N - 12, kFlush, kLogits>(p, tk, tv, s);
+    case 8: return launch_n<N, N - 8, kFlush, kLogits>(p, tk, tv, s);
+    case 4: return launch_n<N, N - 4, kFlush, kLogits>(p, tk, tv, s);
+    default: return launch_n<N, N, kFlush, kLogits>(p, tk, tv, s);
   }
 }
 
@@ -959,8 +968,9 @@ static cudaError_t launch_mr_f(int mr, const VerifyParams& p, const CUtensorMap&
 template <int N>
 static cudaError_t launch_mr(int mr, const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv,
                              cudaStream_t s) {
-  return p.flush_tiles > 0 && TCfg<N>::kFlushable ? launch_mr_f<N, true>(mr, p, tk, tv, s)
-                                                  : launch_mr_f<N, false>(mr, p, tk, tv, s);
+  const bool f = p.flush_tiles > 0 && TCfg<N>::kFlushable, lg = p.logits != nullptr;
+  return f ? (lg ? launch_mr_f<N, true, true>(mr, p, tk, tv, s) : launch_mr_f<N, true, false>(mr, p, tk, tv, s))
+           : (lg ? launch_mr_f<N, false, true>(mr, p, tk, tv, s) : launch_mr_f<N, false, false>(mr, p, tk, tv, s));
 }
 
 }  // namespace sa

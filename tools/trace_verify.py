@@ -1,6 +1,7 @@
 """Dev tool: config-2 verify of one layer with the "trace" knob set, after 3 other layers have streamed
 through L2 (so the traced layer is read from DRAM): CTA start / main-loop end / end and the per-tile
-pipeline timeline of CTA 0."""
+pipeline timeline of CTA 0.  The per-tile stamps need a dev build of the library:
+  make -C paper_2602_07223_b200/csrc EXTRA_NVFLAGS=-DSA_PIPE_TRACE   (the product build compiles them out)"""
 import ctypes
 import os
 import sys
