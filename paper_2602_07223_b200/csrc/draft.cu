@@ -217,7 +217,12 @@ struct DCfg {
   static_assert(kSmemStream <= 227 * 1024, "streaming mode fits one CTA per SM");
 };
 
+// Per-CTA phase stamps (tools/trace_draft.py): dev builds only (-DSA_PIPE_TRACE); the checks cost
+// ~0.1 us per launch in the product build.
 __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
+#ifndef SA_PIPE_TRACE
+  return;
+#endif
   if (p.trace && threadIdx.x == 0) {
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     if (cta < 512) {
@@ -464,7 +469,11 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
         const uint32_t vs[2] = {vb + (sb >> 2) * DCfg::kTileBytes, vb + (sb2 >> 2) * DCfg::kTileBytes};
         const int rr[2] = {(sb & 3) * 16, (sb2 & 3) * 16};
         const int nv[2] = {nv0, min(16, n - (r0 + sb2 * 16))};
+#ifdef SA_PIPE_TRACE  // dev build: warp 0's step phases in cycles (tools/trace_draft.py)
         w.step<2>(ks, vs, DCfg::kHalf, rr, lane, p.scale_log2, nv, (p.trace && tid == 0) ? cyc : nullptr);
+#else
+        w.step<2>(ks, vs, DCfg::kHalf, rr, lane, p.scale_log2, nv);
+#endif
       } else {
         const uint32_t ks[1] = {kb + (sb >> 2) * DCfg::kTileBytes};
         const uint32_t vs[1] = {vb + (sb >> 2) * DCfg::kTileBytes};
@@ -477,12 +486,14 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   }
   w.finalize();
   dtrace(p, 3);
+#ifdef SA_PIPE_TRACE
   if (p.trace && tid == 0 && warp == 0) {  // dev: step<2> phases of warp 0 in cycles -> slots 11-13
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     const size_t launch = static_cast<size_t>((p.step - 1) & 7) * 64 + (p.layer & 63);
     if (cta < 512)
       for (int k2 = 0; k2 < 3; ++k2) p.trace[(launch * 512 + cta) * 16 + 11 + k2] = cyc[k2 + 1] - cyc[k2];
   }
+#endif
 
   // in-CTA merge of the warps' partials (only the G real query rows), fused with the push: every
   // warp stores its raw O fragments and (m, l); after one barrier each thread rescales the warps'

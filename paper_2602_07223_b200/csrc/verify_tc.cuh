@@ -143,6 +143,16 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
 }
 
 // dev-only per-CTA phase timestamps (globaltimer ns): slot k of CTA `cta_lin` in layer p.layer
+#ifdef SA_PIPE_TRACE
+constexpr bool kPipeTrace = true;
+#else
+constexpr bool kPipeTrace = false;  // product build: every kernel-internal timing stamp compiled out
+#endif
+#ifndef SA_PIPE_TRACE
+#define SA_TSTAMP(k) \
+  do {               \
+  } while (0)
+#else
 #define SA_TSTAMP(k)                                                                            \
   do {                                                                                          \
     if (p.trace && cta_lin < 1024) {                                                            \
@@ -151,6 +161,7 @@ __device__ __forceinline__ void warp_allreduce_sum(float (&x)[N]) {
       p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + (k)] = gt_;                          \
     }                                                                                           \
   } while (0)
+#endif
 
 // dev-only pipeline trace: ev[e][t] = clock64 of event e at tile t for CTA (0,0,0)
 // Per-tile pipeline stamps of CTA 0 (tools/trace_verify.py): a dev build only
@@ -374,7 +385,7 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   if (tid == 0) SA_TRACE(11, 0);
   const int cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  if (p.trace && tid == 0 && cta_lin < 1024) {
+  if (kPipeTrace && p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
     p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin] = gt;
@@ -798,7 +809,7 @@ __global__ void __launch_bounds__(384, 1)
     // layer-parity workspaces (partials, counters, chunk claims) are free again by transitivity.
     mbar_wait(dep_bar, 0);
     pdl_launch_dependents();
-    if (p.trace && ts == 0 && wg == 0 && cta_lin < 1024) {
+    if (kPipeTrace && p.trace && ts == 0 && wg == 0 && cta_lin < 1024) {
       unsigned long long gt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
       p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + 2] = gt;  // main loop done
@@ -909,14 +920,14 @@ __global__ void __launch_bounds__(384, 1)
         const int per = (M + nm - 1) / nm;
         merge_rows_progressive(smem, merge_bar, po, pml, p.n_splits, N, min(M, split * per), min(M, (split + 1) * per),
                                out_unit, uflags + split * 128, t256,
-                               (p.trace && cta_lin < 1024) ? p.trace + 1024 + (p.layer & 63) * 16384 + 16 * cta_lin : nullptr);
+                               (kPipeTrace && p.trace && cta_lin < 1024) ? p.trace + 1024 + (p.layer & 63) * 16384 + 16 * cta_lin : nullptr);
         if (split == 0 && t256 == 0) p.chunk_ctr[unit] = 0;  // every split has claimed its last chunk
         if (t256 == 0) SA_TSTAMP(9);
       }
     }
   }
   __syncthreads();
-  if (p.trace && tid == 0 && cta_lin < 1024) {
+  if (kPipeTrace && p.trace && tid == 0 && cta_lin < 1024) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
     p.trace[1024 + (p.layer & 63) * 16384 + 16 * cta_lin + 1] = gt;

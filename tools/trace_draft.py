@@ -1,4 +1,4 @@
-"""Dev tool: draft-phase CTA timeline inside the config-2 iteration graph (knob "trace").
+"""(needs a dev build: make -C paper_2602_07223_b200/csrc EXTRA_NVFLAGS=-DSA_PIPE_TRACE) Dev tool: draft-phase CTA timeline inside the config-2 iteration graph (knob "trace").
   SA_ITER_SKIP=3 python tools/trace_draft.py     # drafts only (selections from an earlier run)
 Per draft launch (step, layer): first CTA start, median start, median 'loaded' (after the PDL wait),
 median 'computed', max end (us relative to the first draft start)."""

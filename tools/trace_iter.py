@@ -1,4 +1,4 @@
-"""Dev tool: per-layer verify CTA timeline inside the config-2 iteration graph (knob "trace").
+"""(needs a dev build: make -C paper_2602_07223_b200/csrc EXTRA_NVFLAGS=-DSA_PIPE_TRACE) Dev tool: per-layer verify CTA timeline inside the config-2 iteration graph (knob "trace").
   SA_ITER_SKIP=6 python tools/trace_iter.py      # verify-only graph
 Prints, per layer: first CTA start, median / max main-loop end, median / max CTA end (us, relative
 to layer 0's first start)."""

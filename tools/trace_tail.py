@@ -1,4 +1,4 @@
-"""Dev tool: verify tail anatomy inside the config-2 iteration graph (knob "trace", verify-only).
+"""(needs a dev build: make -C paper_2602_07223_b200/csrc EXTRA_NVFLAGS=-DSA_PIPE_TRACE) Dev tool: verify tail anatomy inside the config-2 iteration graph (knob "trace", verify-only).
 For each layer and unit, times (us) relative to the unit's median main-loop end of: the last main-loop
 end, the last arrival's PV done / partial stored / arrival counted, the mergers' merge done, and the
 CTA ends; printed as medians over units and layers (layers 2.. of the chain)."""
