@@ -88,14 +88,11 @@ namespace sa {
 struct DevConfig {
   int verify_impl = 0;          // 0: tcgen05 verify (product); 1: the mma.sync baseline kernel (verify.cu)
   int verify_chunk_tiles = 2;   // 128-token tiles per dynamically claimed chunk
-  int verify_prefetch = 0;      // tiles prefetched into L2 ahead of the K ring
-  int verify_next_pf = 0;       // chunks of the next layer each CTA prefetches into L2 at its stream end
   int verify_no_prefill = 0;    // do not fill the ring before griddepcontrol.wait
   int verify_static_first = 1;  // first chunk = split index (else every chunk claimed from the counter)
   int verify_mergers = 8;       // designated merger CTAs (splits 0..n-1) that split the merge's rows
   int verify_full_rows = 0;     // softmax over all N MMA columns instead of MR = roundup4(M)
   int verify_max_splits = 0;    // cap on CTAs per (sequence, KV head) unit (0: automatic)
-  int verify_wait_pf = 0;       // tiles prefetched into L2 ahead of the ring before the dependency wait ends
   int verify_tail_tiles = 18;   // single-tile chunks at the end of the prefix (guided claiming)
   int verify_flush_tiles = 8;   // TMEM accumulation block (warpgroup tiles) folded into Oacc; 0: never
   int verify_flush_min_tiles = 24;  // fold only when a CTA streams more than this many prefix tiles
@@ -143,11 +140,7 @@ struct VerifyParams {
   int* flags;      // [B*Hkv][8 mergers][128 splits]: partial published (tcgen05 verify), reset by the merger
   unsigned long long* trace;  // dev-only pipeline timestamps of CTA (0,0,0); null in production
   int use_pdl;  // programmatic dependent launch after the previous layer's verify (iteration graph)
-  int next_layer;  // layer verified next (its first tiles are prefetched into L2), -1: none
   int chunk_tiles;  // 128-token tiles per dynamically claimed chunk
-  int prefetch;     // tiles prefetched into L2 ahead of the K ring
-  int next_pf;      // chunks of the next layer each CTA prefetches into L2 at the end of its stream
-  int wait_pf;      // tiles of its own stream a CTA prefetches into L2 while waiting for the dependency
   int tail_tiles;   // the last tail_tiles tiles of the prefix are claimed as single-tile chunks
   int flush_tiles;  // TMEM accumulation block length in a warpgroup's tiles (0: never flush)
   int full_rows;    // dev: softmax over all N columns

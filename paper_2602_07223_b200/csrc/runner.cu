@@ -252,7 +252,7 @@ SA_API int32_t* sa_runner_counts(sa_runner* r, int32_t slot) {
 }
 
 static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t s, bool pdl = false,
-                             bool in_iteration = false, int next_layer = -1) {
+                             bool in_iteration = false) {
   if (!a || !a->q || !a->out) return fail(SA_INVALID_ARGUMENT, "verify: null argument");
   if (r->B < 1) return fail(SA_INVALID_ARGUMENT, "verify: no batch bound");
   if (a->layer < 0 || a->layer >= r->cache->n_layers) return fail(SA_OUT_OF_RANGE, "verify: layer out of range");
@@ -324,13 +324,10 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     // second wave); dynamic chunk claiming balances inside a unit
     const sa::DevConfig& dv = r->dev;
     const int chunk_tiles = std::max(1, dv.verify_chunk_tiles);
-    p.next_pf = std::max(0, dv.verify_next_pf);
     p.no_prefill = dv.verify_no_prefill ? 1 : 0;
     p.static_first = dv.verify_static_first;
     p.full_rows = dv.verify_full_rows ? 1 : 0;
     p.chunk_tiles = chunk_tiles;
-    p.prefetch = std::min(12, std::max(0, dv.verify_prefetch));
-    p.wait_pf = std::min(16, std::max(0, dv.verify_wait_pf));  // the producer's 32-entry position ring
     p.tail_tiles = std::max(0, dv.verify_tail_tiles);
     p.flush_tiles = std::max(0, dv.verify_flush_tiles);
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
@@ -365,7 +362,6 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.counters = r->v_cnt + par * cnt_stride * 4;
     p.flags = r->v_flags + par * cnt_stride * 8 * 128;
     p.use_pdl = pdl ? 1 : 0;
-    p.next_layer = next_layer;
     p.trace = r->vtrace;
     e = sa::launch_verify_tc(p, r->cache->tmap_k128, r->cache->tmap_v128, s);
   }
@@ -557,14 +553,11 @@ SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) 
   const int v = static_cast<int>(value);
   if (n == "verify_impl") d.verify_impl = v;
   else if (n == "verify_chunk_tiles") d.verify_chunk_tiles = v;
-  else if (n == "verify_prefetch") d.verify_prefetch = v;
-  else if (n == "verify_next_pf") d.verify_next_pf = v;
   else if (n == "verify_no_prefill") d.verify_no_prefill = v;
   else if (n == "verify_static_first") d.verify_static_first = v;
   else if (n == "verify_mergers") d.verify_mergers = v;
   else if (n == "verify_full_rows") d.verify_full_rows = v;
   else if (n == "verify_max_splits") d.verify_max_splits = v;
-  else if (n == "verify_wait_pf") d.verify_wait_pf = v;
   else if (n == "verify_tail_tiles") d.verify_tail_tiles = v;
   else if (n == "verify_flush_tiles") d.verify_flush_tiles = v;
   else if (n == "verify_flush_min_tiles") d.verify_flush_min_tiles = v;
@@ -785,7 +778,7 @@ static sa_status enqueue_iteration(sa_runner* r, const sa_iteration_args* a, cud
     }
     v.out = a->out_v + l * qv_l;
     if ((skip & 1) == 0)
-      if (sa_status st = verify_impl(r, &v, main, /*pdl=*/l > 0, /*in_iteration=*/true, l + 1 < L ? l + 1 : -1))
+      if (sa_status st = verify_impl(r, &v, main, /*pdl=*/l > 0, /*in_iteration=*/true))
         return st;
     SA_CUDA_CHECK(cudaEventRecord(r->ev_v[l], main));
     SA_CUDA_CHECK(cudaStreamWaitEvent(r->side, r->ev_v[l], 0));

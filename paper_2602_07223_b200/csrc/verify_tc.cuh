@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(384, 1)
   const int n_pref = p0 / C::kTile;
   const int win_lo = n_pref * C::kTile;
   const int n_win = (p0 + R - win_lo + C::kTile - 1) / C::kTile;
-  const int chunk_tiles = p.chunk_tiles, prefetch = p.prefetch;
+  const int chunk_tiles = p.chunk_tiles;
   // chunks: n_big chunks of chunk_tiles tiles, then single-tile chunks for the last n_tail tiles of the
   // prefix (claims are monotonic, so the final claims of every CTA are small: less loop-end spread)
   // (short prefixes keep whole chunks: every chunk is then a CTA's static first one, no claims)
@@ -441,21 +441,12 @@ __global__ void __launch_bounds__(384, 1)
         return ((((p.layer * p.cache.num_pages + bt[pos >> p.cache.page_shift]) * p.cache.n_kv_heads + g)
                  << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1)));
       };
-      int nk = 0, nv = 0, npf = 0;
-      bool released = false;  // griddepcontrol.wait passed (dep_bar): the consumers are running
+      int nk = 0, nv = 0;
       while (true) {
-        // before the dependency is released the ring is full and idle: pull `wait_pf` more tiles of
-        // this CTA's stream into L2 (HBM would otherwise idle through the previous layer's tail)
-        if (!released) released = mbar_test(dep_bar, 0);
-        const int depth = released ? prefetch : max(prefetch, p.wait_pf);
-        fill(nk + 1 + depth);
-        for (; npf < min(q_end, nv + C::kSV + depth) && nk >= 1; ++npf) {  // L2 prefetch
-          const int row = row_of(pring[npf & 31]);
-          tma_prefetch_l2_2d(&tmk, 0, row);
-          tma_prefetch_l2_2d(&tmk, 64, row);
-          tma_prefetch_l2_2d(&tmv, 0, row);
-          tma_prefetch_l2_2d(&tmv, 64, row);
-        }
+        fill(nk + 1);
+        // no L2 prefetch: every form measured slower — the next layer's first chunks, tiles ahead of the
+        // ring, the CTA's own tiles during the dependency wait, and even the tiles inside the V ring window
+        // (same-box A/B: 30.7 -> 28.4 us per layer without it)
         if (nk < q_end && (nk < C::kSK || mbar_test(&k_empty[nk % C::kSK], ((nk / C::kSK) & 1) ^ 1))) {
           const int st = nk % C::kSK, pos = pring[nk & 31];
           if (pos >= win_lo && !dep_seen) {  // window rows are appended after the dependency wait
@@ -489,20 +480,6 @@ __global__ void __launch_bounds__(384, 1)
         tile_pos[(nk + e) % C::kPosRing] = -1;
         mbar_arrive(&pos_bar[(nk + e) % C::kPosRing]);
       }
-      // keep HBM busy across the layer boundary: pull the next layer's first chunks of this unit
-      // into L2 while this layer drains (chunks split, split + n_splits, ...: the ones the next
-      // layer's CTAs claim first)
-      if (p.next_layer >= 0)
-        for (int c = split, i = 0; i < p.next_pf && c < n_chunks; c += p.n_splits, ++i)
-          for (int t = 0; t < chunk_len(c); ++t) {
-            const int pos = (chunk_start(c) + t) * C::kTile;
-            const int row = (((p.next_layer * p.cache.num_pages + bt[pos >> p.cache.page_shift]) * p.cache.n_kv_heads + g)
-                             << p.cache.page_shift) | (pos & ((1 << p.cache.page_shift) - 1));
-            tma_prefetch_l2_2d(&tmk, 0, row);
-            tma_prefetch_l2_2d(&tmk, 64, row);
-            tma_prefetch_l2_2d(&tmv, 0, row);
-            tma_prefetch_l2_2d(&tmv, 64, row);
-          }
     }
   } else {
     // ------------------------- warps 1-3: dependency wait, Q staging, fused window append (96 threads,

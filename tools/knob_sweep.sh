@@ -1,6 +1,6 @@
 #!/bin/bash
 # Dev: config-2 iteration under several dev-knob settings (one bench line each, knobs in the "sweep" key).
-#   tools/knob_sweep.sh "verify_next_pf=0" "verify_next_pf=2 verify_prefetch=2" ...
+#   tools/knob_sweep.sh "verify_mergers=4" "verify_mergers=8 verify_tail_tiles=0" ...
 # Each argument is one setting: space-separated KNOB=VALUE pairs (sa_dev_set_knob names).
 EXTRA=${EXTRA:-}
 for setting in "$@"; do
