@@ -252,8 +252,11 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
 // of the G x 128 outputs; every CTA pushes its partial slices and (m, l) into the owners' inboxes
 // with st.async (remote shared-memory stores completing as transaction bytes on the owner's
 // mbarrier), and each owner combines its slice once its inbox is full.
-template <bool kStream, bool kPack>
-__global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kernel(const DraftParams p) {
+// kMode 0: one round of <= 192 rows per CTA, two CTAs per SM (config 2: the round loop compiles away);
+// 1: several rounds, two CTAs per SM; 2: streaming (double-buffered rounds, one CTA per SM)
+template <int kMode, bool kPack>
+__global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_kernel(const DraftParams p) {
+  constexpr bool kStream = kMode == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* part = reinterpret_cast<float*>(smem + DCfg::kOffPart);
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   };
 
   constexpr int kRoundRows = DCfg::kMaxTiles * DCfg::kTile;
-  const int n_rounds = max(1, (n + kRoundRows - 1) / kRoundRows);
+  const int n_rounds = kMode == 0 ? 1 : max(1, (n + kRoundRows - 1) / kRoundRows);
   // two-CTA-per-SM mode with several rounds (a few units, large k): every round's pre-existing source
   // rows are resolved before the dependency wait (own src_row area per round) and the rows of rounds
   // >= 1 are prefetched into L2, so a later round costs one L2 gather instead of index + block-table
@@ -606,11 +609,12 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kStream ? 1 : 2) draft_kern
   dtrace(p, 4);
 }
 
-template <bool kStream, bool kPack>
+template <int kMode, bool kPack>
 static cudaError_t draft_set_attrs_one() {
-  cudaError_t e = cudaFuncSetAttribute(draft_kernel<kStream, kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  constexpr bool kStream = kMode == 2;
+  cudaError_t e = cudaFuncSetAttribute(draft_kernel<kMode, kPack>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kStream ? DCfg::kSmemStream : DCfg::kSmem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(draft_kernel<kStream, kPack>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(draft_kernel<kMode, kPack>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
@@ -618,10 +622,12 @@ static cudaError_t draft_set_attrs() {
   static std::atomic<uint64_t> attr_mask{0};
   int dev = 0;
   if (func_attrs_needed(attr_mask, &dev)) {
-    cudaError_t e = draft_set_attrs_one<false, false>();
-    if (e == cudaSuccess) e = draft_set_attrs_one<false, true>();
-    if (e == cudaSuccess) e = draft_set_attrs_one<true, false>();
-    if (e == cudaSuccess) e = draft_set_attrs_one<true, true>();
+    cudaError_t e = draft_set_attrs_one<0, false>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<0, true>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<1, false>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<1, true>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<2, false>();
+    if (e == cudaSuccess) e = draft_set_attrs_one<2, true>();
     if (e != cudaSuccess) return e;
     func_attrs_done(attr_mask, dev);
   }
@@ -653,8 +659,8 @@ int draft_max_active_clusters(int stream, int cs) {
     attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    if ((stream ? cudaOccupancyMaxActiveClusters(&n, draft_kernel<true, false>, &cfg)
-                : cudaOccupancyMaxActiveClusters(&n, draft_kernel<false, false>, &cfg)) != cudaSuccess) {
+    if ((stream ? cudaOccupancyMaxActiveClusters(&n, draft_kernel<2, false>, &cfg)
+                : cudaOccupancyMaxActiveClusters(&n, draft_kernel<1, false>, &cfg)) != cudaSuccess) {
       cudaGetLastError();
       n = 0;
     }
@@ -686,8 +692,10 @@ cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   cfg.numAttrs = p.use_pdl ? 3 : 2;
   const bool pack = p.G <= 4;  // P_hi | P_mid share one n8 tile (DraftWarp<true>)
   if (p.stream)
-    return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<true, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<true, false>, p);
-  return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<false, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<false, false>, p);
+    return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<2, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<2, false>, p);
+  if (p.chunk <= DCfg::kMaxTiles * DCfg::kTile)  // one round per CTA
+    return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<0, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<0, false>, p);
+  return pack ? cudaLaunchKernelEx(&cfg, draft_kernel<1, true>, p) : cudaLaunchKernelEx(&cfg, draft_kernel<1, false>, p);
 }
 
 int draft_max_splits() { return DCfg::kMaxCS; }
