@@ -520,7 +520,10 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   __syncthreads();
   dtrace(p, 5);
   cluster_wait_acquire();  // every owner's inbox barrier is initialised
-  if (tid == 0) {
+  // a one-CTA "cluster" (streaming mode, cs = 1) writes its inbox with plain shared stores: st.async
+  // needs a real cluster (compute-sanitizer memcheck)
+  const bool solo = CS == 1;
+  if (tid == 0 && !solo) {
     const int my_vals = my_hi - my_lo;
     mbar_arrive_expect_tx(inbox_bar, static_cast<uint32_t>(CS) * (my_vals + 2 * p.G) * 4u);
   }
@@ -539,10 +542,14 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
       float ls = (ok && mq != -INFINITY) ? wml[q * 16 + 8 + row] * fast_exp2(mq - ms) : 0.f;
 #pragma unroll
       for (int off = 1; off < 8; off <<= 1) ls += __shfl_xor_sync(0xffffffffu, ls, off);
-      if (row < p.G)
+      if (row < p.G && solo && q == 0) {
+        inbox[per + 2 * row] = ms;
+        inbox[per + 2 * row + 1] = ls;
+      } else if (row < p.G && !solo) {
         for (int o = q; o < CS; o += 8)
           st_async_v2(mapa_shared(inbox_addr + (split * rstride + per + 2 * row) * 4, o), ms, ls,
                       mapa_shared(bar_addr, o));
+      }
     }
   }
   for (int q4 = tid; q4 < n_out / 4; q4 += nthr) {
@@ -566,8 +573,11 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
       }
     }
     const int owner = e / per;
-    st_async_v4(mapa_shared(inbox_addr + (split * rstride + (e - owner * per)) * 4, owner), v,
-                mapa_shared(bar_addr, owner));
+    if (solo)
+      *reinterpret_cast<float4*>(inbox + e) = v;
+    else
+      st_async_v4(mapa_shared(inbox_addr + (split * rstride + (e - owner * per)) * 4, owner), v,
+                  mapa_shared(bar_addr, owner));
   }
   // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45), off the
   // critical path: this launch reads the row from k_new / v_new; later steps of this layer gather it
@@ -581,7 +591,10 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   }
   // combine my slice once every sender's contribution has landed
   dtrace(p, 6);
-  mbar_wait_cluster(inbox_bar, 0);
+  if (solo)
+    __syncthreads();
+  else
+    mbar_wait_cluster(inbox_bar, 0);
   dtrace(p, 7);
   float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128;
   for (int e = my_lo + tid; e < my_hi; e += nthr) {

@@ -461,7 +461,9 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
     for (int c : {2, 4})
       if (units * c <= r->num_sms) min_cs = c;
     if (r->dev.draft_min_cs) min_cs = r->dev.draft_min_cs;
-    for (int c : {1, 2, 4, 8, 12, 16})
+    // the smallest CS whose chunk fits one round (any size up to 16: e.g. 13 for the 2311 rows of
+    // gamma 8 at k = 2294, where 16 CTAs per unit cost 6.0 against ~5.1 us per launch)
+    for (int c : {1, 2, 4, 8, 9, 10, 11, 12, 13, 14, 15, 16})
       if (c >= min_cs && (m + c - 1) / c <= round_rows) {
         cs = c;
         break;
