@@ -401,10 +401,12 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   long long cyc[4] = {0, 0, 0, 0};  // dev timing of warp 0's first step (trace knob)
   DraftWarp<kPack> w;
   w.init(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128, p.G, lane);
+#ifdef SA_PIPE_TRACE
   if (p.trace) {  // dev: stamp 10 once this thread's query fragments have landed
     asm volatile("" ::"r"(w.qb[7][1]), "r"(w.qb[0][0]));
     dtrace(p, 10);
   }
+#endif
   const bool dbuf = kStream && n_rounds > 1;  // double-buffered rounds (streaming mode)
   auto issue_round = [&](int round, int buf) {  // every row of a later round (after the wait)
     const int rr0 = round * kRoundRows;
