@@ -484,6 +484,11 @@ __global__ void __launch_bounds__(384, 1)
   } else {
     // ------------------------- warps 1-3: dependency wait, Q staging, fused window append (96 threads,
     // every global load of a batch in flight together)
+    // the unit's query rows into L2 before the wait (they come from the previous layer; L2 is the point
+    // of coherence, so the lines cannot go stale; same-box A/B: -0.14 us per layer)
+    if (tid - 32 < (M * 256 + 1023) / 1024)
+      prefetch_l2_bulk(p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128 + (tid - 32) * 512,
+                       min(1024, M * 256 - (tid - 32) * 1024));
     pdl_wait();
     const int t96 = tid - 32;
     const __nv_bfloat16* qb = p.q + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
