@@ -154,7 +154,10 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
     if args.gamma:  # config 5: gamma sweep at the workload's context
         gamma = args.gamma
     G = Hq_full // Hkv_full
-    sh, B, Hkv, seqs_global, strong = shard_for(workload, mode, world, rank)
+    emu = getattr(args, "emulate_world", 0) if world == 1 else 0
+    # --emulate-world N (one GPU): run rank 0's shard of an N-GPU job; the score exchange runs on a
+    # one-rank communicator (its launch in the graph, not the NVLink transfer)
+    sh, B, Hkv, seqs_global, strong = shard_for(workload, mode, emu or world, rank)
     Hq = G * Hkv
     R = gamma + 1
     p0 = ctx
@@ -202,7 +205,12 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
         runner.set_dev_knob(name, int(val))
     runner.set_batch(list(range(B)), [p0] * B)
     comm, comm_info = None, None
-    if sh is not None and sh.needs_score_exchange:  # KV heads of a layer on several GPUs: NCCL exchange
+    if sh is not None and sh.needs_score_exchange and emu:
+        comm = Comm(Comm.unique_id(), 1, 0)
+        comm_info = {"nranks": 1, "rank": 0, "group": [0], "ok": True,
+                     "emulated": f"rank 0 of a {emu}-GPU head group; one-rank communicator"}
+        runner.set_comm(comm)
+    elif sh is not None and sh.needs_score_exchange:  # KV heads of a layer on several GPUs: NCCL exchange
         import torch.distributed as dist
         groups = {}
         for base in range(0, world, sh.head_group):  # every rank creates every group (collective call)
@@ -387,7 +395,8 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
             traffic = None
     it_gbs = it_bytes / (ms / 1e3) / 1e9
     par = ("dp%d (one batch-%d replica per GPU, no collective)" % (world, B) if sh is None else
-           f"{world} GPUs: batch x KV-head shards ({B} seq x {Hkv} KV heads per GPU"
+           (f"EMULATED rank 0 of {emu}: " if emu else "") +
+           f"{emu or world} GPUs: batch x KV-head shards ({B} seq x {Hkv} KV heads per GPU"
            + (f", NCCL per-layer score exchange over {sh.head_group} GPUs)" if comm else ", no collective)"))
     result = {
         "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": steps,
@@ -428,6 +437,10 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
         result["heavy_hitter_recall"] = round(recall, 6)
     if comm_info is not None:
         result["comm"] = comm_info
+    if emu:
+        result["emulated"] = {"world": emu, "note": "one GPU runs rank 0's shard; value = whole-job tokens / "
+                              "rank 0's iteration time (every rank's shard is identical); the per-layer score "
+                              "all-reduce runs on a one-rank communicator (no NVLink transfer)"}
     if comm is not None:
         runner.set_comm(None)
         comm.close()
@@ -698,6 +711,8 @@ def main():
     ap.add_argument("--no-headsplit", action="store_true",
                     help="N > 1: skip the config-4 KV-head split with the NCCL score exchange")
     ap.add_argument("--plan-only", action="store_true", help="print every rank's shard plan and exit (no GPU)")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="one GPU: run rank 0's shard of an N-GPU job (per-rank work; a one-rank communicator)")
     ap.add_argument("--strategy", default="collect2", choices=sorted(STRATEGIES),
                     help="selection strategy of the iteration (the headline is collect2; the others are the "
                          "paper's variants / baselines for the overhead comparison)")
