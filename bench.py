@@ -232,7 +232,8 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
     stream = torch.cuda.Stream(device=dev)
 
     def it_args(bufs=(qv, kvn, vvn, qd, kdn, vdn, out_v, out_d), phases=0):
-        return runner.iteration_args(gamma, *bufs, strategy=strategy, mode=PER_LAYER, scale=scale,
+        return runner.iteration_args(gamma, *bufs, strategy=strategy, mode=(1 if args.per_kv_head else PER_LAYER),
+                                     scale=scale,
                                      use_graph=not args.no_graph, phases=phases, accepted=accepted)
 
     itargs = it_args()
@@ -409,7 +410,7 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
         "config": {"workload": label or (f"config5 sweep point (gamma {gamma}, k {k}) on {workload}'s shape"
                                          if args.gamma or args.k else f"{workload}: {desc}"),
                    "global_batch": seqs_global, "seq_len": p0,
-                   "gamma": gamma, "k": k, "selection": f"{args.strategy}, per-layer", "layers": L,
+                   "gamma": gamma, "k": k, "selection": f"{args.strategy}, " + ("per-KV-head" if args.per_kv_head else "per-layer"), "layers": L,
                    "accepted": accepted, "parallelism": par,
                    "l2": f"inputs > L2: KV cache {L * B * p0 * Hkv * D * 4 / 1e9:.1f} GB/GPU >> 126 MB",
                    "cuda_graph": not args.no_graph},
@@ -711,6 +712,8 @@ def main():
     ap.add_argument("--no-headsplit", action="store_true",
                     help="N > 1: skip the config-4 KV-head split with the NCCL score exchange")
     ap.add_argument("--plan-only", action="store_true", help="print every rank's shard plan and exit (no GPU)")
+    ap.add_argument("--per-kv-head", action="store_true",
+                    help="per-KV-head selection (one top-k per KV head; the reference default is per layer)")
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="one GPU: run rank 0's shard of an N-GPU job (per-rank work; a one-rank communicator)")
     ap.add_argument("--strategy", default="collect2", choices=sorted(STRATEGIES),
