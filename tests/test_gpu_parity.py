@@ -942,6 +942,7 @@ FULL_CASES = [
     (1, 8, 5, 131072, None),  # config 4 per-GPU shard: one KV head (+ its 8 q-heads) at 128K, k = 9175
     (8, 4, 9, 32768, 4096),   # config 5 corner: gamma 8, k 4096
     (8, 4, 3, 32768, 64),     # config 5 corner: gamma 2, k 64
+    (8, 4, 9, 32768, 2300),   # k + tail crosses 12 x 192 rows mid-chain: single-round drafts with 13-CTA clusters
 ]
 
 
