@@ -148,6 +148,7 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
     from paper_2602_07223_b200.synthetic import default_shift, heavy_hitter_positions, plant_shift, plant_torch
     steps = steps or args.steps
     warmup = max(3, warmup or args.warmup)
+    local_rank = _local_device(local_rank)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     L, Hq_full, Hkv_full, ctx, gamma, B_total, desc = WORKLOADS[workload]
@@ -248,7 +249,7 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
         if world == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if _SHARED_GPU else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -684,6 +685,19 @@ def run_reference(args, rank, world, workload):
     return res
 
 
+# dev only (SA_BENCH_SHARED_GPU=1): run N ranks on one visible GPU with a gloo process group, to check
+# the multi-rank plumbing (shard plan, per-rank runs, max over ranks, rank-0 line) where only one GPU
+# exists; its timings mean nothing (the ranks share the GPU), and no NCCL score exchange can run
+_SHARED_GPU = os.environ.get("SA_BENCH_SHARED_GPU") == "1"
+
+
+def _local_device(local_rank):
+    if _SHARED_GPU:
+        import torch
+        return local_rank % max(1, torch.cuda.device_count())
+    return local_rank
+
+
 def _free_port():
     import socket
     with socket.socket() as sk:
@@ -757,8 +771,11 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if _SHARED_GPU:  # dev plumbing check: every rank on the one visible GPU, host-side gloo
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank, workload, mode, data=args.data)
     if world > 1 and not args.no_headsplit:
         # §8e: the config-4 shape with its KV heads split over all N GPUs, so every layer's per-layer
