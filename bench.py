@@ -653,8 +653,8 @@ def run_reference(args, rank, world, workload):
     L, Hq, Hkv, ctx, gamma, B, desc = WORKLOADS[workload]
     full = B == 1
     n_layers = L if full else min(L, 4)
-    for _ in range(args.warmup):
-        ref.step(n_layers)
+    for _ in range(args.warmup):  # warm-up steps of one layer (threads and caches warm; the run stays short)
+        ref.step(1)
     secs, ph = 0.0, [0.0, 0.0, 0.0]
     for _ in range(args.steps):
         s1, p1 = ref.step(n_layers)
