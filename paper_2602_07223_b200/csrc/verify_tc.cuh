@@ -379,6 +379,11 @@ __global__ void __launch_bounds__(384, 1)
   const bool flushing = C::kFlushable && kFlush && p.flush_tiles > 0;
   const int flush = flushing ? p.flush_tiles : (1 << 30);
   const uint32_t tmem_cols = flushing ? C::kTmemCols : C::kTmemColsBase;
+  if (MR < N) {  // P^T rows >= MR stay zero: the softmax never stores the all-padding 8-row chunks
+    uint4* pz = reinterpret_cast<uint4*>(smem + C::kOffP);
+    for (int i = tid; i < 2 * C::kPlanes * C::kPBytes / 16; i += C::kThreads) pz[i] = make_uint4(0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();  // generic zero stores -> the tensor core's (async-proxy) reads
+  }
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
@@ -616,6 +621,16 @@ __global__ void __launch_bounds__(384, 1)
     float l[N];
 #pragma unroll
     for (int m = 0; m < N; ++m) l[m] = 0.f;
+    // this warpgroup's lazy row references (mref): held in registers across tiles where the register
+    // budget allows (N <= 32: -0.1..-0.4 us per layer), reloaded from shared memory each tile above that
+    // (N = 48 spilled: +1.4 us)
+    constexpr bool kRegRef = N <= 32;
+    float mr[N];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) mr[m] = -INFINITY;
+    uint64_t wbits = 0;  // rows in the Collect-k score (wsc as a register bitmask: no per-tile smem reads)
+#pragma unroll
+    for (int m = 0; m < MR; ++m) wbits |= (wsc[m] != 0.f ? 1ull : 0ull) << m;
 
     int i = 0;
     for (int t = wg;; t += 2, ++i) {
@@ -637,7 +652,7 @@ __global__ void __launch_bounds__(384, 1)
       if ((score_out || score_fx) && pos < p0) {  // fused Collect-k column sum (raw logits)
         float sc4[4] = {0.f, 0.f, 0.f, 0.f};  // four independent FMA chains (latency, not throughput)
 #pragma unroll
-        for (int m = 0; m < MR; ++m) sc4[m & 3] = fmaf(wsc[m], s[m], sc4[m & 3]);
+        for (int m = 0; m < MR; ++m) sc4[m & 3] += ((wbits >> m) & 1ull) ? s[m] : 0.f;
         const float sc = (sc4[0] + sc4[1]) + (sc4[2] + sc4[3]);
         if (score_fx)  // per-layer: integer atomics over the KV heads (order-independent, deterministic)
           atomicAdd(reinterpret_cast<unsigned long long*>(score_fx + pos),
@@ -655,9 +670,10 @@ __global__ void __launch_bounds__(384, 1)
       }
       // pass 1: does any logit exceed the lazy reference by more than 2^8?  (mref held in registers:
       // no shared-memory reads between the P stores below)
-      float mr[N];
+      if (!kRegRef) {
 #pragma unroll
-      for (int m = 0; m < MR; m += 4) *reinterpret_cast<float4*>(&mr[m]) = *reinterpret_cast<const float4*>(&mref[m]);
+        for (int m = 0; m < MR; m += 4) *reinterpret_cast<float4*>(&mr[m]) = *reinterpret_cast<const float4*>(&mref[m]);
+      }
       bool ex4[4] = {false, false, false, false};  // four independent OR chains
       if (full) {
 #pragma unroll
@@ -762,6 +778,7 @@ __global__ void __launch_bounds__(384, 1)
       for (int a = 0; a < C::kPAtoms; ++a)
 #pragma unroll
         for (int ch = 0; ch < 2; ++ch) {
+          if (16 * a + 8 * ch >= MR) continue;  // padding rows only: zeroed once in the prologue
           uint32_t hw[4], mw[4], lw[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
