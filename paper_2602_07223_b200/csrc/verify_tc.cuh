@@ -271,7 +271,7 @@ __device__ __forceinline__ void merge_rows_progressive(uint8_t* smem, uint64_t* 
   }
 }
 
-// MR: the softmax rows that can be real (M rounded up to 8, <= N); rows MR..N-1 of the MMA tile are
+// MR: the softmax rows that can be real (M rounded up to 4, <= N); rows MR..N-1 of the MMA tile are
 // padding and get no softmax work (P = 0).
 template <int N, int MR, bool kFlush, bool kLogits>
 __global__ void __launch_bounds__(384, 1)
