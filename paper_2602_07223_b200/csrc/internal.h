@@ -90,10 +90,10 @@ struct DevConfig {
   int verify_chunk_tiles = 2;   // 128-token tiles per dynamically claimed chunk
   int verify_no_prefill = 0;    // do not fill the ring before griddepcontrol.wait
   int verify_static_first = 1;  // first chunk = split index (else every chunk claimed from the counter)
-  int verify_mergers = 8;       // designated merger CTAs (splits 0..n-1) that split the merge's rows
+  int verify_mergers = 6;       // designated merger CTAs (splits 0..n-1) that split the merge's rows
   int verify_full_rows = 0;     // softmax over all N MMA columns instead of MR = roundup4(M)
   int verify_max_splits = 0;    // cap on CTAs per (sequence, KV head) unit (0: automatic)
-  int verify_tail_tiles = 18;   // single-tile chunks at the end of the prefix (guided claiming)
+  int verify_tail_tiles = 72;   // single-tile chunks at the end of the prefix (guided claiming)
   int verify_flush_tiles = 8;   // TMEM accumulation block (warpgroup tiles) folded into Oacc; 0: never
   int verify_flush_min_tiles = 24;  // fold only when a CTA streams more than this many prefix tiles
   int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
