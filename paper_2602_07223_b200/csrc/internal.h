@@ -96,6 +96,7 @@ struct DevConfig {
   int verify_tail_tiles = 72;   // single-tile chunks at the end of the prefix (guided claiming)
   int verify_flush_tiles = 8;   // TMEM accumulation block (warpgroup tiles) folded into Oacc; 0: never
   int verify_flush_min_tiles = 24;  // fold only when a CTA streams more than this many prefix tiles
+  int verify_row_split = 1;     // N >= 48: softmax warpgroups split every tile's rows instead of alternating tiles
   int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
   int draft_cs = 0;             // forced CTAs per unit (0: automatic)
   int draft_cluster_policy = 1; // cudaClusterSchedulingPolicy: 1 spread (no two CTAs of a cluster share an SM)
@@ -143,6 +144,7 @@ struct VerifyParams {
   int chunk_tiles;  // 128-token tiles per dynamically claimed chunk
   int tail_tiles;   // the last tail_tiles tiles of the prefix are claimed as single-tile chunks
   int flush_tiles;  // TMEM accumulation block length in a warpgroup's tiles (0: never flush)
+  int row_split;    // both softmax warpgroups on every tile, each on half of the rows
   int full_rows;    // dev: softmax over all N columns
 };
 

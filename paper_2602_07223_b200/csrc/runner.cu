@@ -330,6 +330,7 @@ static sa_status verify_impl(sa_runner* r, const sa_verify_args* a, cudaStream_t
     p.chunk_tiles = chunk_tiles;
     p.tail_tiles = std::max(0, dv.verify_tail_tiles);
     p.flush_tiles = std::max(0, dv.verify_flush_tiles);
+    p.row_split = dv.verify_row_split ? 1 : 0;
     const int64_t n_chunks = std::max<int64_t>(1, (r->p_max / 128 + chunk_tiles - 1) / chunk_tiles);
     // split merge: the designated mergers (splits 0..n_mergers-1) normalise a slice of rows each; their
     // staged partial rows and the (m, l) table must fit the ring buffers
@@ -563,6 +564,7 @@ SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) 
   else if (n == "verify_tail_tiles") d.verify_tail_tiles = v;
   else if (n == "verify_flush_tiles") d.verify_flush_tiles = v;
   else if (n == "verify_flush_min_tiles") d.verify_flush_min_tiles = v;
+  else if (n == "verify_row_split") d.verify_row_split = v;
   else if (n == "draft_min_cs") d.draft_min_cs = v;
   else if (n == "draft_cs") d.draft_cs = v;
   else if (n == "draft_cluster_policy") d.draft_cluster_policy = v;

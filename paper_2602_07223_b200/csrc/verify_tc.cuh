@@ -273,7 +273,7 @@ __device__ __forceinline__ void merge_rows_progressive(uint8_t* smem, uint64_t* 
 
 // MR: the softmax rows that can be real (M rounded up to 4, <= N); rows MR..N-1 of the MMA tile are
 // padding and get no softmax work (P = 0).
-template <int N, int MR, bool kFlush, bool kLogits>
+template <int N, int MR, bool kFlush, bool kLogits, bool kRS>
 __global__ void __launch_bounds__(384, 1)
     verify_tc_kernel(const __grid_constant__ CUtensorMap tmk, const __grid_constant__ CUtensorMap tmv,
                      const VerifyParams p) {
@@ -353,8 +353,8 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(merge_bar, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 128);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&s_empty[i], kRS ? 256 : 128);  // kRS: both warpgroups read every S and write every P
+      mbar_init(&p_full[i], kRS ? 256 : 128);
       mbar_init(&p_empty[i], 1);
     }
     fence_mbar_init();
@@ -558,14 +558,14 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t v_base = smem_u32(smem + C::kOffV + sv * C::kTileBytes);
         const uint32_t p_pl = p_base + wg * C::kPlanes * C::kPBytes;
-        const uint32_t o_tm = tmem + C::kOCol + wg * C::kNP;
+        const uint32_t o_tm = tmem + C::kOCol + (kRS ? 0 : wg * C::kNP);  // kRS: one O^T accumulator
         uint64_t a[8], bp[8];
 #pragma unroll
         for (int kt = 0; kt < 8; ++kt) {  // 16 tokens per MMA; one MMA covers every P plane (N' = kNP)
           a[kt] = umma_desc(v_base + kt * 2048, C::kHalf, 1024, kLayoutSW128);
           bp[kt] = umma_desc(p_pl + kt * 512, C::kTile * 32, 256, kLayoutSW32);
         }
-        umma_bf16_x8(o_tm, a, bp, idesc_pv, ((u >> 1) % flush) != 0 ? 1u : 0u);  // block start: overwrite
+        umma_bf16_x8(o_tm, a, bp, idesc_pv, ((kRS ? u : (u >> 1)) % flush) != 0 ? 1u : 0u);  // block start: overwrite
         umma_commit_elect(&v_empty[sv]);
         umma_commit_elect(&p_empty[wg]);
         SA_TRACE(3, u);
@@ -618,6 +618,228 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t s_tm = tmem + lane_off + wg * N;
     const uint32_t o_tm = tmem + lane_off + C::kOCol + wg * C::kNP;  // plane q's O^T at +q*N
     const uint32_t a_tm = tmem + lane_off + C::kACol + wg * N;       // Oacc^T (closed accumulation blocks)
+    const bool single = p.n_splits == 1;  // this CTA owns the whole unit: normalise in place
+    float* po = p.part_o + static_cast<size_t>(unit) * p.n_splits * N * 128;
+    float* pml = p.part_ml + static_cast<size_t>(unit) * p.n_splits * N * 2;
+    float* my_o = po + static_cast<size_t>(split) * N * 128;
+    float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
+    // row split of the MR softmax rows at an 8-row chunk boundary (kRS)
+    constexpr int kR0 = (MR + 8) / 16 * 8 < 8 ? 8 : (MR + 8) / 16 * 8;
+    if constexpr (kRS) {
+      // ------------------------------------------------------------------------------------------------
+      // Row split (kRS): both warpgroups work on EVERY tile, warpgroup w on query rows [rlo, rlo + RW):
+      // half the softmax latency per tile, one O^T accumulator (no warpgroup merge in the epilogue).
+      // S / P are double-buffered by tile parity; s_empty and p_full count both warpgroups' 256 threads.
+      auto rs = [&](auto rw_c, int rlo) {
+        constexpr int RW = decltype(rw_c)::value;          // this warpgroup's real rows
+        constexpr int RWP = (RW + 7) / 8 * 8;               // its 8-row P chunks
+        float l[RWP];
+        float mr[RWP];
+#pragma unroll
+        for (int m = 0; m < RWP; ++m) {
+          l[m] = 0.f;
+          mr[m] = -INFINITY;
+        }
+        uint64_t wbits = 0;
+#pragma unroll
+        for (int m = 0; m < RW; ++m) wbits |= (wsc[rlo + m] != 0.f ? 1ull : 0ull) << m;
+        const uint32_t o_rs = tmem + lane_off + C::kOCol + rlo;  // plane q's columns of my rows at +q*N
+        const uint32_t a_rs = tmem + lane_off + 2 * N + C::kNP + rlo;  // Oacc (after the single O)
+        int t = 0;
+        for (;; ++t) {
+          mbar_wait(&pos_bar[t % C::kPosRing], (t / C::kPosRing) & 1);
+          const int tstart = tile_pos[t % C::kPosRing];
+          if (tstart < 0) break;
+          const int sb = t & 1;
+          mbar_wait(&s_full[sb], (t >> 1) & 1);
+          tc_fence_after();
+          float s[RWP];
+          tmem_ld_cols<RWP>(tmem + lane_off + sb * N + rlo, s);
+          tc_wait_ld();
+          tc_fence_before();
+          mbar_arrive(&s_empty[sb]);
+          const int pos = tstart + tk;
+          const bool full = tstart + C::kTile <= p0;
+          const bool in_range = pos < p0 + R;
+          if (score_fx && pos < p0) {  // this warpgroup's rows of the Collect-k column sum (int64: exact)
+            float sc4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int m = 0; m < RW; ++m) sc4[m & 3] += ((wbits >> m) & 1ull) ? s[m] : 0.f;
+            const float sc = (sc4[0] + sc4[1]) + (sc4[2] + sc4[3]);
+            if (wbits)
+              atomicAdd(reinterpret_cast<unsigned long long*>(score_fx + pos),
+                        static_cast<unsigned long long>(__float2ll_rn(sc * kScoreFxScale)));
+          }
+          if (kLogits && pos < p0) {
+            float* lb = p.logits + static_cast<size_t>(b) * Hq * p.n_collect * p.ld_logits + pos;
+#pragma unroll
+            for (int m = 0; m < RW; ++m) {
+              const int o = loff[rlo + m];
+              if (o >= 0) lb[o] = s[m];
+            }
+          }
+          bool ex4[4] = {false, false, false, false};
+          if (full) {
+#pragma unroll
+            for (int m = 0; m < RW; ++m) ex4[m & 3] |= fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
+          } else {
+#pragma unroll
+            for (int m = 0; m < RW; ++m)
+              ex4[m & 3] |= (in_range && pos <= lim[rlo + m]) && fmaf(s[m], c, -mr[m]) > kLazyMaxThresh;
+          }
+          const bool exceed = (ex4[0] || ex4[1]) || (ex4[2] || ex4[3]);
+          if (named_bar_or(bar_wg, 128, exceed)) {
+            float x[RW];
+#pragma unroll
+            for (int m = 0; m < RW; ++m) x[m] = s[m] * c;
+            if (!full) {
+#pragma unroll
+              for (int m = 0; m < RW; ++m) x[m] = (in_range && pos <= lim[rlo + m]) ? x[m] : -INFINITY;
+            }
+            warp_allreduce_max<RW>(x);
+            if (lane == 0)
+#pragma unroll
+              for (int m = 0; m < RW; ++m) red[q4 * 64 + m] = x[m];
+            named_bar_sync(bar_wg, 128);
+            if (ts < RW) {
+              const float mo = mref_all[rlo + ts];
+              const float mx = fmaxf(fmaxf(red[ts], red[64 + ts]), fmaxf(red[128 + ts], red[192 + ts]));
+              const float mn = fmaxf(mo, mx);
+              fac_all[rlo + ts] = (mo == -INFINITY) ? 0.f : (mn == mo ? 1.f : fast_exp2(mo - mn));
+              mref_all[rlo + ts] = mn;
+            }
+            named_bar_sync(bar_wg, 128);
+#pragma unroll
+            for (int m = 0; m < RW; ++m) {
+              l[m] *= fac_all[rlo + m];
+              mr[m] = mref_all[rlo + m];
+            }
+            if (t > 0) {  // O^T of my rows is final through tile t-1 once PV(t-1) retired
+              mbar_wait(&p_empty[(t - 1) & 1], ((t - 1) >> 1) & 1);
+              tc_fence_after();
+#pragma unroll
+              for (int pl = 0; pl < C::kPlanes; ++pl) {
+                float v[RWP];
+                tmem_ld_cols<RWP>(o_rs + pl * N, v);
+                tc_wait_ld();
+#pragma unroll
+                for (int m = 0; m < RW; ++m) v[m] *= fac_all[rlo + m];
+                tmem_st_cols<RWP>(o_rs + pl * N, v);
+              }
+              if (kFlush && t > flush) {
+                float v[RWP];
+                tmem_ld_cols<RWP>(a_rs, v);
+                tc_wait_ld();
+#pragma unroll
+                for (int m = 0; m < RW; ++m) v[m] *= fac_all[rlo + m];
+                tmem_st_cols<RWP>(a_rs, v);
+              }
+              tc_wait_st();
+            }
+          }
+          if (full) {
+#pragma unroll
+            for (int m = 0; m < RW; ++m) s[m] = fast_exp2(fmaf(s[m], c, -mr[m]));
+          } else {
+#pragma unroll
+            for (int m = 0; m < RW; ++m)
+              s[m] = (in_range && pos <= lim[rlo + m]) ? fast_exp2(fmaf(s[m], c, -mr[m])) : 0.f;
+          }
+#pragma unroll
+          for (int m = RW; m < RWP; ++m) s[m] = 0.f;  // padding rows of my last chunk
+#pragma unroll
+          for (int m = 0; m < RW; ++m) l[m] += s[m];
+          if (t >= 2) mbar_wait(&p_empty[sb], ((t >> 1) - 1) & 1);  // PV(t-2) finished reading this P buffer
+          if (kFlush && t > 0 && t % flush == 0) {  // PV(t-1) closed a block: Oacc (+)= my rows' planes
+            mbar_wait(&p_empty[(t - 1) & 1], ((t - 1) >> 1) & 1);
+            tc_fence_after();
+            float op[C::kPlanes][RWP], acc[RWP];
+#pragma unroll
+            for (int pl = 0; pl < C::kPlanes; ++pl) tmem_ld_cols<RWP>(o_rs + pl * N, op[pl]);
+            if (t > flush) tmem_ld_cols<RWP>(a_rs, acc);
+            tc_wait_ld();
+#pragma unroll
+            for (int j = 0; j < RWP; ++j) {
+              float v = op[C::kPlanes - 1][j];
+#pragma unroll
+              for (int pl = C::kPlanes - 2; pl >= 0; --pl) v += op[pl][j];
+              acc[j] = t > flush ? v + acc[j] : v;
+            }
+            tmem_st_cols<RWP>(a_rs, acc);
+            tc_wait_st();
+          }
+          uint8_t* pb = smem + C::kOffP + sb * C::kPlanes * C::kPBytes;
+#pragma unroll
+          for (int q8 = 0; q8 < RWP / 8; ++q8) {  // my 8-row chunks (rows rlo + 8 q8 ..)
+            const int row8 = rlo / 8 + q8, a = row8 >> 1, ch = row8 & 1;
+            uint32_t hw[4], mw[4], lw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) split3_bf16(s[8 * q8 + 2 * e], s[8 * q8 + 2 * e + 1], hw[e], mw[e], lw[e]);
+            const uint32_t off = a * (C::kTile * 32) + tk * 32 + ((ch ^ ((tk >> 2) & 1)) << 4);
+            *reinterpret_cast<uint4*>(pb + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(pb + C::kPBytes + off) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+            *reinterpret_cast<uint4*>(pb + 2 * C::kPBytes + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+          }
+          fence_proxy_async_smem();
+          tc_fence_before();
+          mbar_arrive(&p_full[sb]);
+        }
+        // ---- epilogue of my rows (kRS): every tile's PV retired, then l, (m, l) and O of my rows
+        mbar_wait(dep_bar, 0);
+        pdl_launch_dependents();
+        const int T = t;  // tiles processed (by both warpgroups)
+        if (ts == 0) ntiles_wg[wg] = T;
+        if (T > 0) {
+          mbar_wait(&p_empty[(T - 1) & 1], ((T - 1) >> 1) & 1);
+          if (T > 1) mbar_wait(&p_empty[T & 1], ((T - 2) >> 1) & 1);
+          tc_fence_after();
+        }
+        float lw[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) lw[m] = m < RW ? l[m] : 0.f;
+        warp_transpose_sum_store<32>(lw, lane, red + q4 * 64);  // per-warp row sums -> red[q4][row]
+        named_bar_sync(bar_wg, 128);
+        if (ts < RW) {
+          const int row = rlo + ts;
+          const float lsum = red[ts] + red[64 + ts] + red[128 + ts] + red[192 + ts];
+          const float ms = mref_all[row];
+          ltot[row] = lsum;
+          if (!single) {
+            pml[(split * N + row) * 2] = T > 0 ? ms : -INFINITY;
+            pml[(split * N + row) * 2 + 1] = lsum;
+          }
+        }
+        named_bar_sync(bar_wg, 128);
+        if (T > 0) {
+          float o[C::kPlanes][RWP], acc[RWP];
+#pragma unroll
+          for (int pl = 0; pl < C::kPlanes; ++pl) tmem_ld_cols<RWP>(o_rs + pl * N, o[pl]);
+          const bool acc_on = kFlush && T > flush;
+          if (acc_on) tmem_ld_cols<RWP>(a_rs, acc);
+          tc_wait_ld();
+#pragma unroll
+          for (int m = 0; m < RW; ++m) {
+            float v = o[C::kPlanes - 1][m];  // smallest plane first
+#pragma unroll
+            for (int pl = C::kPlanes - 2; pl >= 0; --pl) v += o[pl][m];
+            if (acc_on) v += acc[m];
+            const int row = rlo + m;
+            if (row < M) {
+              if (single) out_unit[row * 128 + tk] = v / ltot[row];
+              else my_o[row * 128 + tk] = v;
+            }
+          }
+        } else if (!single) {
+#pragma unroll
+          for (int m = 0; m < RW; ++m)
+            if (rlo + m < M) my_o[(rlo + m) * 128 + tk] = 0.f;
+        }
+      };
+      if constexpr (MR - kR0 >= 1) {
+        if (wg == 0) rs(std::integral_constant<int, kR0>{}, 0);
+        else rs(std::integral_constant<int, MR - kR0>{}, kR0);
+      }
+    } else {
     float l[N];
 #pragma unroll
     for (int m = 0; m < N; ++m) l[m] = 0.f;
@@ -826,11 +1048,6 @@ __global__ void __launch_bounds__(384, 1)
     if (ts < N) ltot[wg * 64 + ts] = red[ts] + red[64 + ts] + red[128 + ts] + red[192 + ts];
     named_bar_sync(1, 256);  // both warpgroups' (mref, ltot) final
     if (wg == 0 && ts == 0) SA_TSTAMP(10);
-    const bool single = p.n_splits == 1;  // this CTA owns the whole unit: normalise in place
-    float* po = p.part_o + static_cast<size_t>(unit) * p.n_splits * N * 128;
-    float* pml = p.part_ml + static_cast<size_t>(unit) * p.n_splits * N * 2;
-    float* my_o = po + static_cast<size_t>(split) * N * 128;
-    float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
     float* fin_l = red_all;  // [64] per-row sum of this CTA (both warpgroups, common max)
     float* wgfac = red_all + 64;  // [2][64] per-row rescale of each warpgroup's O to the common max
     const bool has0 = ntiles_wg[0] > 0, has1 = ntiles_wg[1] > 0;
@@ -897,6 +1114,7 @@ __global__ void __launch_bounds__(384, 1)
         else my_o[m * 128 + tk] = acc;
       }
     }
+    }  // kRS / ping-pong
     if (wg == 0 && ts == 0) SA_TSTAMP(12);
     tc_fence_before();
     if (single) {
@@ -939,11 +1157,21 @@ __global__ void __launch_bounds__(384, 1)
 
 template <int N, int MR, bool kFlush, bool kLogits>
 static cudaError_t launch_n(const VerifyParams& p, const CUtensorMap& tk, const CUtensorMap& tv, cudaStream_t s) {
-  auto kern = verify_tc_kernel<N, MR, kFlush, kLogits>;
+  // row split: both softmax warpgroups on every tile (not with per-KV-head scores: two partial stores)
+  // row split where it pays: MMA widths N >= 48 (same-box A/B: gamma 8 at 32K, 37.1 -> 32.3 us per layer;
+  // config 4's per-rank shard, 80.1 -> 67.3 us); at N = 32 the 8 / 12 or 16 / 12 row halves were slower
+  // than tile ping-pong (+0.5 us per layer at gamma 4 and 6)
+  constexpr bool kRSok = MR >= 12 && N >= 48;
+  const bool rs = kRSok && p.row_split && p.scores == nullptr;
+  auto kern = rs ? verify_tc_kernel<N, MR, kFlush, kLogits, kRSok> : verify_tc_kernel<N, MR, kFlush, kLogits, false>;
   static std::atomic<uint64_t> attr_mask{0};
   int dev = 0;
   if (func_attrs_needed(attr_mask, &dev)) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TCfg<N>::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(verify_tc_kernel<N, MR, kFlush, kLogits, kRSok>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, TCfg<N>::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(verify_tc_kernel<N, MR, kFlush, kLogits, false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, TCfg<N>::kSmem);
     if (e != cudaSuccess) return e;
     func_attrs_done(attr_mask, dev);
   }
