@@ -264,8 +264,10 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   uint64_t* inbox_bar = reinterpret_cast<uint64_t*>(smem + DCfg::kOffBar);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nthr = blockDim.x, nwarps = nthr >> 5;
-  const int split = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
-  const int CS = gridDim.x;
+  const int g = blockIdx.y, b = blockIdx.z;
+  const int CS = p.n_splits;          // CTAs per cluster
+  const int split = blockIdx.x % CS;  // rank in the cluster
+  const int sub = blockIdx.x / CS, n_sub = gridDim.x / CS;  // clusters per unit (two-level merge if > 1)
   const int seq = p.seq_ids[b];
   const int p0 = p.p0[b];
   const int j = p.step;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   const int32_t* T = p.idx + (static_cast<size_t>(b) * p.n_sets + set) * p.k_cap;
   const int tail = p.draft_off + j;  // tail rows [p0, p0 + tail): committed verify rows, then this chain's
   const int m_total = k + tail;
-  const int v_begin = split * p.chunk;
+  const int v_begin = blockIdx.x * p.chunk;
   const int v_end = min(m_total, v_begin + p.chunk);
   const int n = max(0, v_end - v_begin);
   const int Hq = p.Hkv * p.G;
@@ -584,7 +586,7 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   // fused append of this step's provisional row (KvStore::append, kv_store.cpp:39-45), off the
   // critical path: this launch reads the row from k_new / v_new; later steps of this layer gather it
   // from the cache either before their own dependency wait (launches >= L back, complete) or after it
-  if (split == CS - 1 && p.k_new && tid < 32) {
+  if (blockIdx.x == gridDim.x - 1 && p.k_new && tid < 32) {
     const int which = tid >> 4, ch = tid & 15;
     const __nv_bfloat16* src = (which ? p.v_new : p.k_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128;
     const int64_t row = cache_row(p.cache, seq, p.layer, g, new_pos);
@@ -599,6 +601,13 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
     mbar_wait_cluster(inbox_bar, 0);
   dtrace(p, 7);
   float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * 128;
+  // two-level merge (n_sub clusters per unit): each cluster's owner r stores its merged slice
+  // (unnormalised, relative to the slice rows' max) and the (m, l) of its rows; the last of the
+  // unit's n_sub owners of slice r to arrive combines them in cluster order (deterministic)
+  const size_t ubase = (static_cast<size_t>(b) * p.Hkv + g) * n_sub;
+  float* lvl_o = p.part_o + ubase * n_out;                       // [unit][sub][G*128]
+  float* lvl_ml = p.part_ml + (ubase * CS + split) * 16;         // [unit][sub][CS][8 rows][2]
+  const size_t lvl_ml_sub = static_cast<size_t>(CS) * 16;
   for (int e = my_lo + tid; e < my_hi; e += nthr) {
     const int row = e >> 7, off = e - my_lo;
     float ms[DCfg::kMaxCS], ls[DCfg::kMaxCS], os[DCfg::kMaxCS];  // all inbox loads in flight together
@@ -619,7 +628,40 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
       acc += os[s2] * f;
       lsum += ls[s2] * f;
     }
-    out_unit[e] = acc / lsum;
+    if (n_sub == 1) {
+      out_unit[e] = acc / lsum;
+    } else {
+      lvl_o[static_cast<size_t>(sub) * n_out + e] = acc;
+      if (e == my_lo || (e & 127) == 0) {
+        lvl_ml[sub * lvl_ml_sub + 2 * row] = mstar;
+        lvl_ml[sub * lvl_ml_sub + 2 * row + 1] = lsum;
+      }
+    }
+  }
+  if (n_sub > 1) {
+    int* cnt = p.counters + (static_cast<size_t>(b) * p.Hkv + g) * DCfg::kMaxCS + split;
+    __syncthreads();
+    int prev = 0;
+    if (tid == 0) {
+      __threadfence();
+      prev = atomicAdd(cnt, 1);
+    }
+    if (!__syncthreads_or(tid == 0 && prev == n_sub - 1)) return;
+    __threadfence();
+    for (int e = my_lo + tid; e < my_hi; e += nthr) {
+      const int row = e >> 7;
+      float mstar = -INFINITY;
+      for (int s2 = 0; s2 < n_sub; ++s2) mstar = fmaxf(mstar, __ldcg(lvl_ml + s2 * lvl_ml_sub + 2 * row));
+      float acc = 0.f, lsum = 0.f;
+      for (int s2 = 0; s2 < n_sub; ++s2) {  // cluster order: deterministic
+        const float m2 = __ldcg(lvl_ml + s2 * lvl_ml_sub + 2 * row);
+        const float f = m2 == -INFINITY ? 0.f : fast_exp2(m2 - mstar);
+        acc += __ldcg(lvl_o + static_cast<size_t>(s2) * n_out + e) * f;
+        lsum += __ldcg(lvl_ml + s2 * lvl_ml_sub + 2 * row + 1) * f;
+      }
+      out_unit[e] = acc / lsum;
+    }
+    if (tid == 0) *cnt = 0;  // re-armed for the next launch (which reads it after its dependency wait)
   }
   dtrace(p, 4);
 }
@@ -687,7 +729,7 @@ int draft_max_active_clusters(int stream, int cs) {
 cudaError_t launch_draft(const DraftParams& p, cudaStream_t s) {
   if (cudaError_t e = draft_set_attrs()) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.n_splits, p.Hkv, p.B);
+  cfg.gridDim = dim3(p.n_splits * p.n_sub, p.Hkv, p.B);
   // one warp per 16-row sub-block of the CTA's chunk (<= 9 warps, two CTAs per SM)
   cfg.blockDim = dim3(32 * std::min(DCfg::kMaxWarps, std::max(1, (std::min(p.chunk, DCfg::kMaxTiles * DCfg::kTile) + 15) / 16)));
   cfg.dynamicSmemBytes = p.stream ? DCfg::kSmemStream : DCfg::kSmem;

@@ -99,6 +99,8 @@ struct DevConfig {
   int verify_row_split = 1;     // N >= 48: softmax warpgroups split every tile's rows instead of alternating tiles
   int draft_min_cs = 0;         // minimum CTAs per (sequence, KV head) unit (0: automatic)
   int draft_cs = 0;             // forced CTAs per unit (0: automatic)
+  int draft_sub = 0;            // forced clusters per unit, two-level merge (0: automatic)
+  int draft_stream = -1;        // forced streaming (1) / two-CTA-per-SM (0) mode (-1: automatic)
   int draft_cluster_policy = 1; // cudaClusterSchedulingPolicy: 1 spread (no two CTAs of a cluster share an SM)
   int draft_multi_rounds = 3;   // rounds allowed in the two-CTA-per-SM multi-round mode
   int draft_debug = 0;          // print the draft launch geometry to stderr
@@ -161,10 +163,11 @@ struct DraftParams {
   int n_sets, k_cap;
   float scale_log2;
   float* out;
-  int n_splits, chunk;
-  float* part_o;   // [B*Hkv][n_splits][16][128]
-  float* part_ml;
-  int* counters;
+  int n_splits, chunk;  // n_splits: CTAs per cluster
+  int n_sub;            // clusters per (sequence, KV head); > 1: two-level merge through part_o / part_ml
+  float* part_o;        // [B*Hkv][n_sub][G*128]
+  float* part_ml;       // [B*Hkv][n_sub][n_splits][8][2]
+  int* counters;        // [B*Hkv][16] arrivals per output slice, re-armed by the combining CTA
   unsigned long long* trace;  // dev-only per-CTA phase timestamps; null in production
   int use_pdl;  // launch with programmatic stream serialization (iteration graph only)
   int stream;   // double-buffered multi-round chunks (one CTA per SM)

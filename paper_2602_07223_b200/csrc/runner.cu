@@ -165,7 +165,7 @@ SA_API sa_status sa_runner_create(sa_cache* cache, const sa_runner_config* cfg, 
   alloc(reinterpret_cast<void**>(&r->v_flags), 2 * sizeof(int) * mb * H * 8 * 128);  // [parity][unit][merger][split]
   alloc(reinterpret_cast<void**>(&r->d_po), sizeof(float) * r->d_units_cap * 16 * 128);
   alloc(reinterpret_cast<void**>(&r->d_pml), sizeof(float) * r->d_units_cap * 16 * 2);
-  alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H);
+  alloc(reinterpret_cast<void**>(&r->d_cnt), sizeof(int) * mb * H * sa::draft_max_splits());
   if (e == cudaSuccess) e = make_streams(r);
   r->ev_v.resize(S);
   r->ev_s.resize(S);
@@ -476,10 +476,27 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
     // buffer.  Fewest rounds first, with a penalty when two successive launches' clusters cannot
     // co-reside (the next launch's pre-wait gathers would then start late); the one-CTA-per-SM
     // streaming mode would need two waves of 16-CTA clusters here.
+    p.n_sub = 1;
+    // A few units whose rows do not fit one round of one cluster (config 4's per-GPU shard: 4 units
+    // of 9.2K rows): still ONE round per CTA, over n_sub clusters of 8 (or 6, 4) CTAs per unit merged
+    // in two levels (the second through global memory, ~2 us), while the grid stays within ~4/3 CTAs
+    // per SM.  Measured on config 4's shard: 13.3 us per launch for three rounds of one 16-CTA
+    // cluster, 11.8 for two rounds of 4 x 8 CTAs, 10.0 for one round of 6 x 8 (grids past ~200 CTAs
+    // or 12-CTA clusters are slower again); at config 2 the second level would cost +2 us.
+    if (cs < 0) {
+      for (int c : {8, 6, 4}) {
+        const int64_t sub = (m + static_cast<int64_t>(c) * round_rows - 1) / (static_cast<int64_t>(c) * round_rows);
+        if (sub >= 2 && units * sub * c * 3 <= 4 * static_cast<int64_t>(r->num_sms) && units * sub * 8 <= r->d_units_cap) {
+          cs = c;
+          p.n_sub = static_cast<int>(sub);
+          break;
+        }
+      }
+    }
     int multi_cs = -1;
     double multi_score = 0.0;
     for (int c : {16, 12, 8}) {
-      if (cs > 0) break;  // one round fits: the single-round rule above
+      if (cs > 0) break;  // one round fits: the rules above
       const int act = sa::draft_max_active_clusters(0, c);
       const int64_t rounds = ((m + c - 1) / c + round_rows - 1) / round_rows;
       if (act < units || rounds > multi_round_max) continue;
@@ -491,7 +508,7 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
     }
     if (cs < 0 && multi_cs > 0) {
       cs = multi_cs;
-    } else if (cs < 0 || units * cs > 2 * r->num_sms) {
+    } else if (cs < 0 || units * cs * p.n_sub > 2 * r->num_sms) {
       // cost ~ waves x (rows per CTA + a fixed per-CTA overhead of one 64-row tile), where the wave
       // count comes from the occupancy API: 16-CTA clusters of one CTA per SM do not all fit on
       // 148 SMs (a cluster lives inside one GPC), and a second wave costs a whole launch
@@ -512,12 +529,16 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
     if (r->dev.draft_cs > 0) {  // dev: forced CTAs per unit, two-CTA-per-SM mode (<= 3 rounds)
       cs = std::min(r->dev.draft_cs, sa::draft_max_splits());
       p.stream = 0;
+      p.n_sub = 1;
     }
+    if (r->dev.draft_stream >= 0) p.stream = r->dev.draft_stream;  // dev: forced mode
+    if (r->dev.draft_sub > 0 && units * r->dev.draft_sub * 8 <= r->d_units_cap)  // dev: forced
+      p.n_sub = r->dev.draft_sub;
     p.n_splits = cs;
-    p.chunk = static_cast<int>(((m + cs - 1) / cs + 15) / 16 * 16);
+    p.chunk = static_cast<int>(((m + cs * p.n_sub - 1) / (cs * p.n_sub) + 15) / 16 * 16);
     if (r->dev.draft_debug) {
-      std::fprintf(stderr, "draft: units %lld m %lld -> stream %d cs %d chunk %d | active clusters (stream/non):",
-                   static_cast<long long>(units), static_cast<long long>(m), p.stream, cs, p.chunk);
+      std::fprintf(stderr, "draft: units %lld m %lld -> stream %d cs %d sub %d chunk %d | active clusters (stream/non):",
+                   static_cast<long long>(units), static_cast<long long>(m), p.stream, cs, p.n_sub, p.chunk);
       for (int c : {1, 2, 4, 8, 12, 16})
         std::fprintf(stderr, " %d:%d/%d", c, sa::draft_max_active_clusters(1, c), sa::draft_max_active_clusters(0, c));
       std::fprintf(stderr, "\n");
@@ -567,6 +588,8 @@ SA_API sa_status sa_dev_set_knob(sa_runner* r, const char* name, int64_t value) 
   else if (n == "verify_row_split") d.verify_row_split = v;
   else if (n == "draft_min_cs") d.draft_min_cs = v;
   else if (n == "draft_cs") d.draft_cs = v;
+  else if (n == "draft_sub") d.draft_sub = v;
+  else if (n == "draft_stream") d.draft_stream = v;
   else if (n == "draft_cluster_policy") d.draft_cluster_policy = v;
   else if (n == "draft_multi_rounds") d.draft_multi_rounds = v;
   else if (n == "draft_debug") d.draft_debug = v;

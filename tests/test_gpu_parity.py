@@ -299,12 +299,17 @@ def test_select_kernels_agree(cuda, ref, mode):
 # ----------------------------------------------------------------------------------- draft
 
 # (mode, Hkv, G): G <= 4 runs the packed-plane draft step (P_hi | P_mid share one n8 tile), G = 8 the
-# three-mma one; G = 1 and 3 leave padding columns inside the packed tile
-@pytest.mark.parametrize("mode,Hkv,G", [(0, 8, 4), (1, 8, 4), (0, 2, 1), (0, 4, 3), (1, 2, 8)])
-def test_draft_parity(cuda, ref, mode, Hkv, G):
+# three-mma one; G = 1 and 3 leave padding columns inside the packed tile.  sub > 0 forces the
+# two-level merge: `sub` clusters of 4 CTAs per unit, combined through global memory
+@pytest.mark.parametrize("mode,Hkv,G,sub", [(0, 8, 4, 0), (1, 8, 4, 0), (0, 2, 1, 0), (0, 4, 3, 0), (1, 2, 8, 0),
+                                            (0, 2, 8, 3), (1, 2, 4, 2)])
+def test_draft_parity(cuda, ref, mode, Hkv, G, sub):
     torch = cuda
     R, p0 = 5, 4096
     m, r, q, kn, vn, out, logits, scores, res = _run_verify(ref, Hkv, G, R, [p0], 256, seed=71, score_layout=mode)
+    if sub:
+        r.set_dev_knob("draft_cs", 4)
+        r.set_dev_knob("draft_sub", sub)
     n_sets = 1 if mode == 0 else Hkv
     idx, cnt = _gpu_select(r, 1, mode, n_sets, 2)
     sets = [idx[0, s, : cnt[0, s]].astype(np.int64) for s in range(n_sets)]

@@ -1,5 +1,6 @@
 """(needs a dev build: make -C paper_2602_07223_b200/csrc EXTRA_NVFLAGS=-DSA_PIPE_TRACE) Dev tool: draft-phase CTA timeline inside the config-2 iteration graph (knob "trace").
   SA_ITER_SKIP=3 python tools/trace_draft.py     # drafts only (selections from an earlier run)
+  HQ=32 HKV=4 CTX=131072 K_FIX=9175 LAYERS=8 ...  # config 4's per-GPU shard (4 units of G = 8)
 Per draft launch (step, layer): first CTA start, median start, median 'loaded' (after the PDL wait),
 median 'computed', max end (us relative to the first draft start)."""
 import ctypes
@@ -11,13 +12,15 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+if os.environ.get("SA_AB_ROOT"):  # a dev build from tools/ab_build.sh (e.g. EXTRA_NVFLAGS=-DSA_PIPE_TRACE)
+    sys.path.insert(0, os.path.abspath(os.environ["SA_AB_ROOT"]))
 import torch  # noqa: E402
 
 from paper_2602_07223_b200 import COLLECT2, Cache, Runner  # noqa: E402
 from paper_2602_07223_b200._lib import lib  # noqa: E402
 
 L = int(os.environ.get("LAYERS", 32))
-Hq, Hkv, p0, gamma, D = 32, 8, int(os.environ.get("CTX", 32768)), 4, 128
+Hq, Hkv, p0, gamma, D = int(os.environ.get("HQ", 32)), int(os.environ.get("HKV", 8)), int(os.environ.get("CTX", 32768)), 4, 128
 R = gamma + 1
 cache = Cache(L, Hkv, D, p0 + R + 64, page_size=256)
 for s in range(0, p0, 2048):
