@@ -192,10 +192,16 @@ SA_API sa_status sa_cache_create(const sa_cache_config* cfg, sa_cache** out) {
   c->free_pages.resize(c->num_pages);
   for (int64_t i = 0; i < c->num_pages; ++i) c->free_pages[i] = static_cast<int32_t>(c->num_pages - 1 - i);
   std::string err;
+  if (rows > static_cast<uint64_t>(INT32_MAX)) {  // tile::gather4 row coordinates are int32 (draft)
+    sa_cache_destroy(c);
+    return fail(SA_NOT_SUPPORTED, "cache rows (layers x pages x KV heads x page size) exceed 2^31");
+  }
   if (!sa::encode_tensor_map(&c->tmap_k, c->k_pool, rows, 64, &err) ||
       !sa::encode_tensor_map(&c->tmap_v, c->v_pool, rows, 64, &err) ||
       !sa::encode_tensor_map(&c->tmap_k128, c->k_pool, rows, 128, &err) ||
-      !sa::encode_tensor_map(&c->tmap_v128, c->v_pool, rows, 128, &err)) {
+      !sa::encode_tensor_map(&c->tmap_v128, c->v_pool, rows, 128, &err) ||
+      !sa::encode_tensor_map(&c->tmap_kg, c->k_pool, rows, 1, &err) ||
+      !sa::encode_tensor_map(&c->tmap_vg, c->v_pool, rows, 1, &err)) {
     sa_cache_destroy(c);
     return fail(SA_CUDA_ERROR, err);
   }

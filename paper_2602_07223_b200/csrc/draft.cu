@@ -204,10 +204,12 @@ struct DCfg {
   static constexpr int kRecvBytes = kMaxCS * kRecvPerSender * 4 > kRecvFloats * 4 ? kMaxCS * kRecvPerSender * 4
                                                                                   : kRecvFloats * 4;
   static constexpr int kOffBar = kOffRecv + kRecvBytes;
-  static constexpr int kSmem = kOffBar + 16 + 1024;
+  static constexpr int kOffGBar = kOffBar + 16;  // row-gather mbarriers, one per round buffer
+  static constexpr int kOffNew = kOffBar + 32;   // this step's new K / V row (32 x 16 B), staged
+  static constexpr int kSmem = kOffNew + 512 + 1024;
   // streaming mode (chunks of several rounds): a second K/V buffer after everything else, so round
   // r+1 is gathered while round r is computed (one CTA per SM)
-  static constexpr int kOffBuf1 = (kOffBar + 16 + 1023) / 1024 * 1024;
+  static constexpr int kOffBuf1 = (kOffNew + 512 + 1023) / 1024 * 1024;
   static constexpr int kOffBt = kOffBuf1 + 2 * kMaxTiles * kTileBytes;  // streaming: block table in smem
   static constexpr int kBtMax = 2048;
   static constexpr int kSmemStream = kOffBt + kBtMax * 4 + 1024;
@@ -255,13 +257,14 @@ __device__ __forceinline__ void dtrace(const DraftParams& p, int phase) {
 // kMode 0: one round of <= 192 rows per CTA, two CTAs per SM (config 2: the round loop compiles away);
 // 1: several rounds, two CTAs per SM; 2: streaming (double-buffered rounds, one CTA per SM)
 template <int kMode, bool kPack>
-__global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_kernel(const DraftParams p) {
+__global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_kernel(const __grid_constant__ DraftParams p) {
   constexpr bool kStream = kMode == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* part = reinterpret_cast<float*>(smem + DCfg::kOffPart);
   float* inbox = reinterpret_cast<float*>(smem + DCfg::kOffRecv);
   uint64_t* inbox_bar = reinterpret_cast<uint64_t*>(smem + DCfg::kOffBar);
+  uint64_t* gbar = reinterpret_cast<uint64_t*>(smem + DCfg::kOffGBar);  // [buffer]: a round's rows landed
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nthr = blockDim.x, nwarps = nthr >> 5;
   const int g = blockIdx.y, b = blockIdx.z;
@@ -293,6 +296,8 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   dtrace(p, 0);
   if (tid == 0) {
     mbar_init(inbox_bar, 1);
+    mbar_init(gbar, 1);
+    mbar_init(gbar + 1, 1);
     fence_mbar_init();
   }
   cluster_arrive_release();  // inbox barriers initialised (waited on just before the pushes)
@@ -313,29 +318,31 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
       src_row[r] = (p.k_new && pos == new_pos) ? -1 : cache_row(p.cache, seq, p.layer, g, pos);
     }
   };
-  auto gather = [&](int r0, int rows, bool pre_pass, int buf, const int64_t* src_row) {
-    uint8_t* const base = buf ? smem + DCfg::kOffBuf1 : smem;
-    for (int i = tid; i < rows * 16; i += nthr) {
-      const int r = i >> 4, ch = i & 15;
-      const int v = v_begin + r0 + r;
-      const bool in = v < v_end;
-      if (in ? (is_pre(v) != pre_pass) : !pre_pass) continue;
-      const int tile = r >> 6, rr = r & 63;
-      const uint32_t off = tile * DCfg::kTileBytes + swz(rr, ch, DCfg::kHalf);
-      const int64_t row = src_row[r];
-      const __nv_bfloat16 *sk = p.cache.k, *sv = p.cache.v;
-      int bytes = 16;
-      if (row >= 0) {
-        sk += row * 128 + ch * 8;
-        sv += row * 128 + ch * 8;
-      } else if (row == -1) {
-        sk = p.k_new + (static_cast<size_t>(b) * p.Hkv + g) * 128 + ch * 8;
-        sv = p.v_new + (static_cast<size_t>(b) * p.Hkv + g) * 128 + ch * 8;
-      } else {
-        bytes = 0;  // zero-fill (keeps 0 * V finite)
+  // TMA row gather (tile::gather4): per group of 4 rows, K and V x two 64-column halves, each one
+  // instruction writing 4 x 128 bytes in the 128-byte-swizzled tile layout the flash step reads;
+  // completion counted on the buffer's mbarrier (the round's bytes are expected up front).  A group
+  // goes in the pass (before / after the dependency wait) of its rows; zero-fill rows and this
+  // step's new row (out-of-range coordinates: zero-filled, the new row stored from registers once
+  // its round has landed) fit either.  `all`: every group (rounds issued after the wait).
+  auto gather = [&](int r0, int rows, bool pre_pass, int buf, const int64_t* src_row, bool all) {
+    const uint32_t base = smem_u32(buf ? smem + DCfg::kOffBuf1 : smem);
+    const uint32_t bar = smem_u32(gbar + buf);
+    for (int i = tid; i < rows; i += nthr) {  // rows (a multiple of 16) = groups x 4 instructions
+      const int r = (i >> 2) * 4, op = i & 3;  // op bit 0: column half, bit 1: V
+      int y[4];
+      bool pre = true;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int v = v_begin + r0 + r + j;
+        y[j] = -1;
+        if (v >= v_end || (p.k_new && v == new_v)) continue;
+        pre = pre && is_pre(v);
+        y[j] = static_cast<int>(src_row[r + j]);  // < 0 (new row / zero fill): out of range
       }
-      cp_async_16(base + off, sk, bytes);
-      cp_async_16(base + DCfg::kOffV + off, sv, bytes);
+      if (!all && pre != pre_pass) continue;
+      const uint32_t dst = base + ((op & 2) ? DCfg::kOffV : 0) + (r >> 6) * DCfg::kTileBytes + (op & 1) * DCfg::kHalf +
+                           (r & 63) * 128;
+      tma_gather4(dst, (op & 2) ? &p.tmv : &p.tmk, bar, (op & 1) * 64, y[0], y[1], y[2], y[3]);
     }
   };
 
@@ -353,9 +360,9 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
     resolve(0, rows0, true, src_row);
     if (early)
       for (int rd = 1; rd < n_rounds; ++rd) resolve(rd * kRoundRows, round_pad(rd), true, round_src(rd));
+    if (tid == 0) mbar_expect_tx(gbar, static_cast<uint32_t>(rows0) * 512u);  // round 0: K + V, 256 B each
     __syncthreads();
-    gather(0, rows0, true, 0, src_row);
-    cp_async_commit();
+    gather(0, rows0, true, 0, src_row, false);
     if (early)  // later rounds' rows into L2 (measured: k = 4096, 8.85 -> 8.75 us per launch)
       for (int rd = 1; rd < n_rounds; ++rd) {
         const int64_t* sr = round_src(rd);
@@ -374,18 +381,21 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
   // barrier) — its round trip overlaps the query loads below; the general path only when earlier
   // steps' rows may still be in flight (a one-layer chain)
   const int rows0_pad = (min(kRoundRows, n) + 15) & ~15;
+  // this step's new row, one 16-byte chunk per lane of the last warp (K: lanes 0-15, V: 16-31),
+  // staged in shared memory until its round's gather has landed (its TMA slot is zero-filled)
+  const bool has_new = p.k_new && warp == nwarps - 1 && new_v >= v_begin && new_v < v_end;
+  const int new_round = (new_v - v_begin) / kRoundRows;
+  if (has_new) {
+    cp_async_16(smem + DCfg::kOffNew + lane * 16,
+                (lane < 16 ? p.k_new : p.v_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128 + (lane & 15) * 8, 16);
+    cp_async_commit();
+  }
   if (!old_tail_ready) {
     __syncthreads();  // src_row of the pre pass consumed by every thread
     resolve(0, rows0_pad, false, src_row);
     __syncthreads();
-    gather(0, rows0_pad, false, 0, src_row);
-  } else if (p.k_new && warp == nwarps - 1 && new_v >= v_begin && new_v < v_begin + rows0_pad && new_v < v_end) {
-    const int r = new_v - v_begin, ch = lane & 15;
-    const uint32_t off = (r >> 6) * DCfg::kTileBytes + swz(r & 63, ch, DCfg::kHalf);
-    const __nv_bfloat16* src = (lane < 16 ? p.k_new : p.v_new) + (static_cast<size_t>(b) * p.Hkv + g) * 128 + ch * 8;
-    cp_async_16(smem + (lane < 16 ? 0 : DCfg::kOffV) + off, src, 16);
+    gather(0, rows0_pad, false, 0, src_row, false);
   }
-  cp_async_commit();
   // streaming mode: the sequence's block table staged in shared memory and each thread's T entry of
   // the next round loaded one round ahead, so resolving a round's source rows costs no dependent
   // global round trip between two rounds' compute
@@ -439,10 +449,10 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
       if (!early) resolve(rr0, rp, true, sr);
       resolve(rr0, rp, false, sr);
     }
+    if (tid == 0) mbar_expect_tx(gbar + buf, static_cast<uint32_t>(rp) * 512u);
     __syncthreads();
-    gather(rr0, rp, true, buf, sr);
-    gather(rr0, rp, false, buf, sr);
-    cp_async_commit();
+    fence_proxy_async_smem();  // the buffer's previous round, read by ldmatrix, before the async-proxy writes
+    gather(rr0, rp, true, buf, sr, true);
   };
   if (dbuf) issue_round(1, 1);
   for (int round = 0; round < n_rounds; ++round) {
@@ -451,8 +461,14 @@ __global__ void __launch_bounds__(DCfg::kMaxThreads, kMode == 2 ? 1 : 2) draft_k
     const int rows_pad = (rows + 15) & ~15;
     const int buf = dbuf ? (round & 1) : 0;
     if (!dbuf && round > 0) issue_round(round, 0);
-    if (dbuf && round + 1 < n_rounds) cp_async_wait_group<1>();  // this round landed, the next in flight
-    else cp_async_wait_all();
+    mbar_wait(gbar + buf, dbuf ? ((round >> 1) & 1) : (round & 1));  // this round landed (the next in flight)
+    if (has_new && new_round == round) {
+      const int r = new_v - v_begin - r0;
+      const uint32_t off = (r >> 6) * DCfg::kTileBytes + swz(r & 63, lane & 15, DCfg::kHalf);
+      cp_async_wait_all();  // each lane reads back its own chunk
+      *reinterpret_cast<uint4*>((buf ? smem + DCfg::kOffBuf1 : smem) + (lane < 16 ? 0 : DCfg::kOffV) + off) =
+          *reinterpret_cast<const uint4*>(smem + DCfg::kOffNew + lane * 16);
+    }
     __syncthreads();
     dtrace(p, 2);
     const int n_sub = rows_pad >> 4;

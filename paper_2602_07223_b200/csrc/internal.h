@@ -54,6 +54,7 @@ struct sa_cache {
   std::vector<int64_t> verified_end;         // p0 + n_rows of the last verify with a fused append (commit bound)
   CUtensorMap tmap_k{}, tmap_v{};            // 2-D [rows][128] bf16, box {64, 64}, SWIZZLE_128B
   CUtensorMap tmap_k128{}, tmap_v128{};      // same tensors, box {64, 128} (tcgen05 verify tiles)
+  CUtensorMap tmap_kg{}, tmap_vg{};          // same tensors, box {64, 1}: draft row gathers (tile::gather4)
   // Quest page summaries (kv_store.cpp:90-139): per (layer, page, KV head, quest page) elementwise key
   // min / max, bf16 (exact: min/max of bf16 keys); summ_valid[seq]: tokens whose quest pages are current
   int64_t qpage = 0;
@@ -151,6 +152,7 @@ struct VerifyParams {
 };
 
 struct DraftParams {
+  CUtensorMap tmk, tmv;  // K / V cache rows for tile::gather4 (box {64, 1}, SWIZZLE_128B)
   CacheView cache;
   int layer, B, Hkv, G, step;
   const int32_t* seq_ids;

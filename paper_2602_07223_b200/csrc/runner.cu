@@ -478,13 +478,14 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
     // streaming mode would need two waves of 16-CTA clusters here.
     p.n_sub = 1;
     // A few units whose rows do not fit one round of one cluster (config 4's per-GPU shard: 4 units
-    // of 9.2K rows): still ONE round per CTA, over n_sub clusters of 8 (or 6, 4) CTAs per unit merged
+    // of 9.2K rows): still ONE round per CTA, over n_sub clusters of 6 (or 8, 4) CTAs per unit merged
     // in two levels (the second through global memory, ~2 us), while the grid stays within ~4/3 CTAs
     // per SM.  Measured on config 4's shard: 13.3 us per launch for three rounds of one 16-CTA
-    // cluster, 11.8 for two rounds of 4 x 8 CTAs, 10.0 for one round of 6 x 8 (grids past ~200 CTAs
-    // or 12-CTA clusters are slower again); at config 2 the second level would cost +2 us.
+    // cluster, 11.8 for two rounds of 4 x 8 CTAs, 9.9-10.0 for one round of 8 x 6 or 6 x 8 (grids
+    // past ~200 CTAs or 12-CTA clusters are slower again); config 5 at k = 4096 (8 units): 9.0 for two
+    // rounds of 16, 9.35 for 3 x 8, 8.28 for 4 x 6.  At config 2 the second level would cost +2 us.
     if (cs < 0) {
-      for (int c : {8, 6, 4}) {
+      for (int c : {6, 8, 4}) {
         const int64_t sub = (m + static_cast<int64_t>(c) * round_rows - 1) / (static_cast<int64_t>(c) * round_rows);
         if (sub >= 2 && units * sub * c * 3 <= 4 * static_cast<int64_t>(r->num_sms) && units * sub * 8 <= r->d_units_cap) {
           cs = c;
@@ -544,6 +545,8 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
       std::fprintf(stderr, "\n");
     }
   }
+  p.tmk = r->cache->tmap_kg;
+  p.tmv = r->cache->tmap_vg;
   p.part_o = r->d_po;
   p.part_ml = r->d_pml;
   p.counters = r->d_cnt;
