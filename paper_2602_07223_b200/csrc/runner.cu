@@ -507,6 +507,16 @@ static sa_status draft_impl(sa_runner* r, const sa_draft_args* a, cudaStream_t s
         multi_score = score;
       }
     }
+    // Many units with a large k (config 3: 128 units of 4.6K rows): small clusters, still two CTAs
+    // per SM and one wave, any number of single-buffered rounds — the two CTAs of an SM overlap one's
+    // gather with the other's compute.  Config 3: 73 us per launch streaming (one CTA per SM,
+    // double-buffered), 68 us with 2-CTA clusters here (TMA row gather).
+    if (cs < 0 && multi_cs < 0)
+      for (int c : {8, 4, 2})
+        if (units * c <= 2 * r->num_sms && units <= sa::draft_max_active_clusters(0, c)) {
+          multi_cs = c;
+          break;
+        }
     if (cs < 0 && multi_cs > 0) {
       cs = multi_cs;
     } else if (cs < 0 || units * cs * p.n_sub > 2 * r->num_sms) {
