@@ -341,6 +341,30 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float* v) {
+  uint32_t r[2];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
+  v[0] = __uint_as_float(r[0]);
+  v[1] = __uint_as_float(r[1]);
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st2(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__float_as_uint(v[0])),
+               "r"(__float_as_uint(v[1]))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__float_as_uint(v[0])),
+               "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3]))
+               : "memory");
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const float* v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
                "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
@@ -367,16 +391,24 @@ __device__ __forceinline__ void tmem_ld_n(uint32_t taddr, float* v) {
 }
 // NC (a multiple of 8) consecutive columns: x16 loads, then an x8 for the remainder
 template <int NC>
-__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {  // NC even
+  static_assert(NC % 2 == 0, "even column count");
 #pragma unroll
   for (int c = 0; c + 16 <= NC; c += 16) tmem_ld16(taddr + c, v + c);
-  if (NC % 16) tmem_ld8(taddr + (NC / 16) * 16, v + (NC / 16) * 16);
+  constexpr int c8 = NC / 16 * 16, c4 = c8 + (NC % 16 >= 8 ? 8 : 0), c2 = c4 + (NC % 8 >= 4 ? 4 : 0);
+  if constexpr (NC % 16 >= 8) tmem_ld8(taddr + c8, v + c8);
+  if constexpr (NC % 8 >= 4) tmem_ld4(taddr + c4, v + c4);
+  if constexpr (NC % 4 == 2) tmem_ld2(taddr + c2, v + c2);
 }
 template <int NC>
-__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const float* v) {
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const float* v) {  // NC even
+  static_assert(NC % 2 == 0, "even column count");
 #pragma unroll
   for (int c = 0; c + 16 <= NC; c += 16) tmem_st16(taddr + c, v + c);
-  if (NC % 16) tmem_st8(taddr + (NC / 16) * 16, v + (NC / 16) * 16);
+  constexpr int c8 = NC / 16 * 16, c4 = c8 + (NC % 16 >= 8 ? 8 : 0), c2 = c4 + (NC % 8 >= 4 ? 4 : 0);
+  if constexpr (NC % 16 >= 8) tmem_st8(taddr + c8, v + c8);
+  if constexpr (NC % 8 >= 4) tmem_st4(taddr + c4, v + c4);
+  if constexpr (NC % 4 == 2) tmem_st2(taddr + c2, v + c2);
 }
 template <int N>
 __device__ __forceinline__ void tmem_st_n(uint32_t taddr, const float* v) {

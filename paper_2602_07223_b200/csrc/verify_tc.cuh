@@ -623,8 +623,10 @@ __global__ void __launch_bounds__(384, 1)
     float* pml = p.part_ml + static_cast<size_t>(unit) * p.n_splits * N * 2;
     float* my_o = po + static_cast<size_t>(split) * N * 128;
     float* out_unit = p.out + (static_cast<size_t>(b) * Hq + static_cast<size_t>(g) * p.G) * R * 128;
-    // row split of the MR softmax rows at an 8-row chunk boundary (kRS)
-    constexpr int kR0 = (MR + 8) / 16 * 8 < 8 ? 8 : (MR + 8) / 16 * 8;
+    // row split of the MR softmax rows (kRS): N = 48 at an even row (balanced halves, e.g. 18 / 18 at
+    // MR = 36, P stored per row pair), N = 64 at an 8-row chunk boundary
+    constexpr bool kPair = N == 48;
+    constexpr int kR0 = kPair ? (MR + 2) / 4 * 2 : ((MR + 8) / 16 * 8 < 8 ? 8 : (MR + 8) / 16 * 8);
     if constexpr (kRS) {
       // ------------------------------------------------------------------------------------------------
       // Row split (kRS): both warpgroups work on EVERY tile, warpgroup w on query rows [rlo, rlo + RW):
@@ -632,7 +634,7 @@ __global__ void __launch_bounds__(384, 1)
       // S / P are double-buffered by tile parity; s_empty and p_full count both warpgroups' 256 threads.
       auto rs = [&](auto rw_c, int rlo) {
         constexpr int RW = decltype(rw_c)::value;          // this warpgroup's real rows
-        constexpr int RWP = (RW + 7) / 8 * 8;               // its 8-row P chunks
+        constexpr int RWP = kPair ? (RW + 1) / 2 * 2 : (RW + 7) / 8 * 8;  // its P row pairs / 8-row chunks
         float l[RWP];
         float mr[RWP];
 #pragma unroll
@@ -769,8 +771,20 @@ __global__ void __launch_bounds__(384, 1)
             tc_wait_st();
           }
           uint8_t* pb = smem + C::kOffP + sb * C::kPlanes * C::kPBytes;
+          if constexpr (kPair) {  // my row pairs (rows rlo + 2 e2, +1): one 32-bit word per plane
 #pragma unroll
-          for (int q8 = 0; q8 < RWP / 8; ++q8) {  // my 8-row chunks (rows rlo + 8 q8 ..)
+            for (int e2 = 0; e2 < RWP / 2; ++e2) {
+              const int row = rlo + 2 * e2, row8 = row >> 3, a = row8 >> 1, ch = row8 & 1;
+              uint32_t hw, mw, lw;
+              split3_bf16(s[2 * e2], s[2 * e2 + 1], hw, mw, lw);
+              const uint32_t off = a * (C::kTile * 32) + tk * 32 + ((ch ^ ((tk >> 2) & 1)) << 4) + (row & 7) * 2;
+              *reinterpret_cast<uint32_t*>(pb + off) = hw;
+              *reinterpret_cast<uint32_t*>(pb + C::kPBytes + off) = mw;
+              *reinterpret_cast<uint32_t*>(pb + 2 * C::kPBytes + off) = lw;
+            }
+          }
+#pragma unroll
+          for (int q8 = 0; q8 < (kPair ? 0 : RWP / 8); ++q8) {  // my 8-row chunks (rows rlo + 8 q8 ..)
             const int row8 = rlo / 8 + q8, a = row8 >> 1, ch = row8 & 1;
             uint32_t hw[4], mw[4], lw[4];
 #pragma unroll
