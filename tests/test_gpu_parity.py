@@ -156,6 +156,27 @@ def test_verify_parity(cuda, ref, Hkv, G, R, p0s, page):
     torch.cuda.synchronize()
 
 
+# per-layer scores (score_layout 0) take the row-split kernel at MMA width N >= 48: balanced row pairs at
+# N = 48 (20 / 20, 18 / 18, 22 / 22 rows), 8-row chunks at N = 64 (32 / 24); outputs, raw logits and the
+# int64 Collect-2 column sums vs the reference
+@pytest.mark.parametrize("Hkv,G,R,p0s", [(2, 8, 5, [777]), (1, 4, 9, [1500]), (2, 4, 11, [900, 64]), (1, 8, 7, [300])])
+def test_verify_row_split_parity(cuda, ref, Hkv, G, R, p0s):
+    m, r, q, kn, vn, out, logits, fx, res = _run_verify(ref, Hkv, G, R, p0s, 128, seed=47, score_layout=0)
+    Hq = Hkv * G
+    for b, p0 in enumerate(p0s):
+        o_ref, l_ref = res[b]
+        assert rel_err_rows(out[b], o_ref) < 2e-4, rel_err_rows(out[b], o_ref)
+        assert rel_err_elem(out[b], o_ref) < 2e-3
+        if p0:
+            Kh = m.K[b][:p0].reshape(p0, 2, Hkv, D)[:, 1]
+            bound = np.einsum("hrd,phd->hrp", np.abs(q[b]), np.abs(Kh[:, np.arange(Hq) // G]))
+            assert np.all(np.abs(logits[b][:, :, :p0] - l_ref) <= 1e-5 * bound + 1e-30)
+            rows = [0, R - 1]
+            want = l_ref[:, rows, :].astype(np.float64).sum((0, 1))
+            got = fx[b, :p0].astype(np.float64) / 2.0 ** 32
+            assert np.all(np.abs(got - want) <= 2e-5 * bound[:, rows].sum((0, 1)) + 1e-4)
+
+
 def test_layer_scores_fixed_point(cuda, ref):
     """Per-layer score byproduct: int64 column sums over ALL KV heads (fixed point, 2^-32) ==
     score_columns' numerator (selection.cpp:93-106); consumed (zeroed) by the per-layer select."""

@@ -5,7 +5,7 @@
 # PDL-parity workspaces), select, draft (st.async inbox pushes, streaming mode), the iteration graph.
 mkdir -p gpurun_out/sanitize
 CS=compute-sanitizer
-SEL_RACE="test_verify_parity or test_draft_parity or test_draft_streaming_mode or test_select_parity or test_iteration_parity or test_layer_scores"
+SEL_RACE="test_verify_parity or test_verify_row_split_parity or test_draft_parity or test_draft_streaming_mode or test_select_parity or test_iteration_parity or test_layer_scores"
 run() {  # tool, log, pytest -k expression, timeout
   timeout $4 $CS --tool $1 --target-processes all --error-exitcode 99 --print-limit 50 \
     python -m pytest tests -x -q -m gpu -k "$3" -p no:cacheprovider > gpurun_out/sanitize/$2.log 2>&1
