@@ -4,11 +4,12 @@
 // [K_T ; K_tail], the SPEC draft-forward key set T ∪ {positions >= draft window start}
 // (SPEC.md:385,447).  The reference materialises the gathered K/V copies; here each CTA gathers
 // its slice of the virtual key list T[0..k) ++ [p0, p0+step) straight into shared memory with
-// 16-byte cp.async (16 lanes per 256-byte row, coalesced) in the swizzled layout the mma.sync
-// flash step of attn_core.cuh reads, for the G q-heads of its KV head (one 16-row tile).
+// TMA tile::gather4 (4 rows x 64 columns per instruction) in the swizzled layout the mma.sync
+// flash step reads, for the G q-heads of its KV head (one 16-row tile).
 //
-// Grid (CS, Hkv, B) launched as clusters of CS CTAs: the CS splits of one (sequence, KV head)
-// merge their partial (max, sum, O) through distributed shared memory — no global round trip.
+// Grid (CS x n_sub, Hkv, B) launched as clusters of CS CTAs: the CS splits of one cluster merge their
+// partial (max, sum, O) through distributed shared memory; with n_sub > 1 clusters per (sequence, KV
+// head) the clusters' merged slices are combined once more through global memory (two-level merge).
 //
 // Programmatic dependent launch: the selected prefix rows (T from the select kernel, positions
 // < p0, never written during the draft phase) are gathered BEFORE griddepcontrol.wait, overlapping
