@@ -316,17 +316,19 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
     v_in_iter_ms = max(ms - d_phase_ms, 1e-9)  # verify chain (+ overlapped selects) inside the iteration
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the region:
-    # every step copies its inputs host->device and reads its outputs back device->host.  Two device
-    # buffer sets (two captured graphs) pipeline the transfers: step i+1's inputs go up and step i-1's
-    # outputs come down (copy streams, both directions at once) while step i computes.
+    # every step copies its inputs host->device and reads its outputs back device->host.  Three device
+    # buffer sets (three captured graphs) pipeline the transfers: step i+1's inputs go up and step i-1's
+    # outputs come down (copy streams, both directions at once) while step i computes (two sets measured
+    # 0.1-0.3 % slower: the upload of step i+1 then waits for the read-back of step i-1).
     e2e_res = None
     if e2e:
-        dev_sets = [[qv, kvn, vvn, qd, kdn, vdn, out_v, out_d],
-                    [torch.empty_like(t) for t in (qv, kvn, vvn, qd, kdn, vdn, out_v, out_d)]]
+        NS = int(os.environ.get("SA_E2E_SETS", 3))  # device buffer sets in flight (dev A/B knob)
+        dev_sets = [[qv, kvn, vvn, qd, kdn, vdn, out_v, out_d]] + \
+                   [[torch.empty_like(t) for t in (qv, kvn, vvn, qd, kdn, vdn, out_v, out_d)] for _ in range(NS - 1)]
         set_args = [it_args(tuple(d)) for d in dev_sets]
-        n_e2e = steps + max(2, warmup // 2)  # warm-up covers both buffer sets (both graphs captured)
-        host_in = [[t.cpu().pin_memory() for t in (qv, kvn, vvn, qd, kdn, vdn)] for _ in range(2)]
-        host_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (out_v, out_d)] for _ in range(2)]
+        n_e2e = steps + max(NS, warmup // 2)  # warm-up covers every buffer set (every graph captured)
+        host_in = [[t.cpu().pin_memory() for t in (qv, kvn, vvn, qd, kdn, vdn)] for _ in range(NS)]
+        host_out = [[torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (out_v, out_d)] for _ in range(NS)]
         h2d = sum(t.numel() * t.element_size() for t in host_in[0])
         d2h = sum(t.numel() * t.element_size() for t in host_out[0])
         up, down = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
@@ -334,10 +336,10 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
         ev_done = [torch.cuda.Event() for _ in range(n_e2e)]
         ev_out = [torch.cuda.Event() for _ in range(n_e2e)]
 
-        def upload(i):  # inputs of step i into set i % 2 once step i-2 (same set) is computed AND read back
-            st = i % 2
-            if i >= 2:
-                up.wait_event(ev_out[i - 2])  # implies ev_done[i - 2]; the compute stream then waits on ev_in only
+        def upload(i):  # inputs of step i into set i % NS once step i-NS (same set) is computed AND read back
+            st = i % NS
+            if i >= NS:
+                up.wait_event(ev_out[i - NS])  # implies ev_done[i - NS]; the compute stream then waits on ev_in only
             with torch.cuda.stream(up):
                 for h, d_ in zip(host_in[st], dev_sets[st][:6]):
                     d_.copy_(h, non_blocking=True)
@@ -346,10 +348,10 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
         def e2e_run(lo, hi):
             upload(lo)
             for i in range(lo, hi):
-                st = i % 2
+                st = i % NS
                 if i + 1 < hi:
                     upload(i + 1)
-                stream.wait_event(ev_in[i])  # (ev_in[i] follows ev_out[i - 2]: set st's outputs are free)
+                stream.wait_event(ev_in[i])  # (ev_in[i] follows ev_out[i - NS]: set st's outputs are free)
                 runner.iteration(set_args[st], stream=stream)
                 ev_done[i].record(stream)
                 down.wait_event(ev_done[i])
@@ -373,7 +375,7 @@ def run_ours(args, rank, world, local_rank, workload, mode, data="gaussian", ste
         e2e_res = {"value": round(tok_per_step / (ms_e2e / 1e3), 2), "unit": "tokens/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms_e2e, 4),
                    "how": "public API (sa_iteration_run graph), pinned host inputs/outputs copied every step; "
-                          "two buffer sets pipeline step i+1's upload and step i-1's read-back with step i"}
+                          "three buffer sets pipeline step i+1's upload and step i-1's read-back with step i"}
     if comm is not None:
         comm.check()
 
