@@ -576,9 +576,14 @@ def test_iteration_collect2_weights(cuda, ref):
         check_selection(idx[0, 0, : cnt[0, 0]], sc, k, relative=True)
 
 
-def test_draft_streaming_mode(cuda, ref):
+# knobs: automatic (the streaming mode here), or forced CTAs per unit in the two-CTA-per-SM mode with
+# several rounds: 4 CTAs -> <= 4 rounds of 96 rows, all resolved before the wait (slots 0 and 1 gathered
+# early); 2 CTAs -> up to 8 rounds (resolved per round after the wait), double-buffered 96-row slots
+@pytest.mark.parametrize("knobs", [{}, {"draft_cs": 4}, {"draft_cs": 2}])
+def test_draft_streaming_mode(cuda, ref, knobs):
     """Draft launches whose chunks span several resident rounds (large k x many sequences: the
-    streaming mode, one CTA per SM with double-buffered rounds) vs the reference gather + attend."""
+    streaming mode, one CTA per SM with double-buffered rounds, or forced multi-round clusters at two
+    CTAs per SM) vs the reference gather + attend."""
     torch = cuda
     Runner, _, selection_k = _lib()
     Hkv, G, R, B = 8, 4, 3, 6
@@ -587,6 +592,8 @@ def test_draft_streaming_mode(cuda, ref):
     m = Matched(ref, L=2, Hkv=Hkv, n_tokens=0, seed=61, max_context=max(p0s) + 64, page_size=128, n_seqs=B,
                 lens=p0s)
     r = Runner(m.cache, Hq, max_rows=R, max_prefix=max(p0s), max_batch=B, sparse_ratio=0.5, k_min=16)
+    for kname, kval in knobs.items():
+        r.set_dev_knob(kname, kval)
     r.set_batch(list(range(B)), p0s)
     q = normal_bf16(62, 1, (B, Hq, R, D))
     kn, vn = normal_bf16(62, 2, (B, R, Hkv, D)), normal_bf16(62, 3, (B, R, Hkv, D))
